@@ -1,0 +1,170 @@
+"""Pins for O3 / O4 (oracle/plan_ref.py): partition rule, halo plan and the
+simulated host-cache exchange (§2.2).
+
+Pinned against SPEC's worked examples, closed forms for
+slab partitions of 3D grids, plan minimality by mutation, and the
+whole-matrix product O1 -- bitwise in the integer regime.
+"""
+import numpy as np
+import pytest
+
+import hecgen
+import oracle
+from oracle import plan_ref as PR
+
+from test_oracle_spmv import dense_exact
+
+
+def tridiag(n):
+    rows = []
+    for i in range(n):
+        r = []
+        if i > 0:
+            r.append((i - 1, -1.0))
+        r.append((i, 2.0))
+        if i < n - 1:
+            r.append((i + 1, -1.0))
+        rows.append(r)
+    return hecgen.from_rows(n, rows)
+
+
+def test_spec_tridiagonal_4_parts():
+    # tridiagonal n=100, 4 parts -> 25 rows each, off-block nnz = 6;
+    # each interior part receives exactly 2 values (one per side).
+    A = tridiag(100)
+    assert PR.part_ptr_ref(A, 4, PR.KIND_CONTIG_ROWS).tolist() == [0, 25, 50, 75, 100]
+    # CONTIG_NNZ by hand: nnz = 298, row_ptr[r] = 3r - 1 (r >= 1); targets
+    # ceil(298p/4) = 75, 149, 224 -> first rows reaching them: 26, 50, 75.
+    assert PR.part_ptr_ref(A, 4, PR.KIND_CONTIG_NNZ).tolist() == [0, 26, 50, 75, 100]
+    pp = PR.part_ptr_ref(A, 4, PR.KIND_CONTIG_ROWS)
+    parts = PR.plan_ref(A, pp)
+    off_block = sum(1 for p in parts for row in p.local_rows for c, _ in row if c >= p.n_loc)
+    assert off_block == 6
+    assert [len(p.recv) for p in parts] == [1, 2, 2, 1]
+    assert parts[1].recv.tolist() == [24, 50]
+    assert parts[1].recv_off.tolist() == [0, 1, 1, 2, 2]
+    assert parts[0].send_idx.tolist() == [24] and parts[0].send_off.tolist() == [0, 0, 1, 1, 1]
+    assert parts[1].boundary.tolist() == [0, 24]
+
+
+def test_spec_block_diagonal_has_no_halo():
+    # block-diagonal matrix -> all recv sets empty.
+    D = np.zeros((12, 12))
+    for b in range(3):
+        D[4 * b:4 * b + 4, 4 * b:4 * b + 4] = 1.0
+    A = hecgen.from_dense(D)
+    parts = PR.plan_ref(A, PR.part_ptr_ref(A, 3, PR.KIND_CONTIG_ROWS))
+    assert all(len(p.recv) == 0 and len(p.send_idx) == 0 and len(p.boundary) == 0 for p in parts)
+
+
+def test_spec_poisson_10cubed_two_parts_cut_edges():
+    # Poisson 10^3 with 2 parts -> recv set size equals the cut edges (100).
+    A = hecgen.poisson3d(10, 10, 10)
+    pp = PR.part_ptr_ref(A, 2, PR.KIND_GRID, (10, 10, 10))
+    assert pp.tolist() == [0, 500, 1000]
+    parts = PR.plan_ref(A, pp)
+    assert [len(p.recv) for p in parts] == [100, 100]
+
+
+@pytest.mark.parametrize("P", [2, 4, 8])
+def test_slab_closed_forms(P):
+    # 16^3 z-slabs: |recv_p| = 256 x #neighbours; peers {p-1, p+1}; boundary rows
+    # = the first and last plane of the slab (closed forms).
+    n1 = 16
+    A = hecgen.poisson3d(n1, n1, n1)
+    pp = PR.part_ptr_ref(A, P, PR.KIND_GRID, (n1, n1, n1))
+    assert pp.tolist() == PR.part_ptr_ref(A, P, PR.KIND_CONTIG_ROWS).tolist()   # P | nz
+    parts = PR.plan_ref(A, pp)
+    plane = n1 * n1
+    for p, part in enumerate(parts):
+        nb = [q for q in (p - 1, p + 1) if 0 <= q < P]
+        assert len(part.recv) == plane * len(nb)
+        peers = [q for q in range(P) if part.recv_off[q + 1] > part.recv_off[q]]
+        assert peers == nb
+        nloc = part.n_loc
+        expect_b = []
+        if p > 0:
+            expect_b += list(range(plane))
+        if p < P - 1:
+            expect_b += list(range(nloc - plane, nloc))
+        assert part.boundary.tolist() == sorted(expect_b)
+        assert len(part.interior) + len(part.boundary) == nloc
+
+
+def test_contig_nnz_rule_properties():
+    # CONTIG_NNZ (A9): each cut is the first row whose row_ptr reaches ceil(p nnz/P)
+    # unless clamped; every part non-empty; balanced to within one max row.
+    for seed, (n, P) in enumerate([(1000, 7), (50, 50), (3000, 8), (10, 3)]):
+        A = hecgen.powerlaw(n, seed=seed)
+        pp = PR.part_ptr_ref(A, P, PR.KIND_CONTIG_NNZ)
+        assert pp[0] == 0 and pp[-1] == n and np.all(np.diff(pp) >= 1)
+        L = np.diff(A.row_ptr)
+        per = [A.row_ptr[pp[p + 1]] - A.row_ptr[pp[p]] for p in range(P)]
+        if n >= 20 * P:
+            assert max(per) - min(per) <= 2 * L.max()
+            for p in range(1, P):
+                t = -((-p * A.nnz) // P)
+                assert A.row_ptr[pp[p]] >= t and A.row_ptr[pp[p] - 1] < t
+
+
+def test_part_ptr_errors():
+    A = tridiag(5)
+    with pytest.raises(ValueError):
+        PR.part_ptr_ref(A, 6)
+    with pytest.raises(ValueError):
+        PR.part_ptr_ref(A, 0)
+    assert PR.part_ptr_ref(A, 5).tolist() == [0, 1, 2, 3, 4, 5]   # P = n: one row per part
+
+
+@pytest.mark.parametrize("P", [1, 2, 3, 4, 8, 16])
+def test_o4_simulated_exchange_equals_whole_matrix(P):
+    # partitioned spmv == spmv for any n_parts; bitwise on
+    # integer data (every partial sum exact).
+    A = hecgen.random_csr(64, 64, 0.08, integer_values=True, seed=P)
+    x = np.array([(hecgen.ctr(P, 9, j) % 17) - 8 for j in range(64)], dtype=np.float64)
+    for kind in (PR.KIND_CONTIG_NNZ, PR.KIND_CONTIG_ROWS):
+        pp = PR.part_ptr_ref(A, P, kind)
+        parts = PR.plan_ref(A, pp)
+        y = PR.simulated_dist_spmv(A, pp, parts, x, oracle.csr_spmv, hecgen.Csr)
+        assert y.tolist() == [float(v) for v in dense_exact(A, x)]
+    B = hecgen.poisson3d(8, 8, 8)
+    xb = hecgen.vector(B.n_cols, "uniform", seed=P)
+    pp = PR.part_ptr_ref(B, min(P, 8), PR.KIND_GRID, (8, 8, 8))
+    parts = PR.plan_ref(B, pp)
+    y = PR.simulated_dist_spmv(B, pp, parts, xb, oracle.csr_spmv, hecgen.Csr)
+    assert np.all(np.abs(y - oracle.csr_spmv(B, xb)) <= oracle.tolerance(B, xb))
+
+
+def test_plan_minimality_by_mutation():
+    # removing any recv index breaks the partitioned product.
+    A = hecgen.powerlaw(200, seed=9)
+    x = hecgen.vector(200, "uniform", seed=2) + 2.0       # no zeros
+    pp = PR.part_ptr_ref(A, 4, PR.KIND_CONTIG_NNZ)
+    parts = PR.plan_ref(A, pp)
+    base = PR.simulated_dist_spmv(A, pp, parts, x, oracle.csr_spmv, hecgen.Csr)
+    checked = 0
+    for p, part in enumerate(parts):
+        for t in range(0, len(part.recv), max(1, len(part.recv) // 7)):
+            L = PR.local_csr(part, "all", hecgen.Csr)
+            halo = x[part.recv].copy()
+            halo[t] = 0.0                                # entry t "not delivered"
+            y = oracle.csr_spmv(L, np.concatenate([x[part.r0:part.r1], halo]))
+            assert not np.array_equal(y, base[part.r0:part.r1])
+            checked += 1
+    assert checked > 10
+
+
+def test_local_csr_interior_boundary_split():
+    A = hecgen.poisson3d(8, 8, 8)
+    pp = PR.part_ptr_ref(A, 2, PR.KIND_GRID, (8, 8, 8))
+    parts = PR.plan_ref(A, pp)
+    for part in parts:
+        Li = PR.local_csr(part, "interior", hecgen.Csr)
+        Lb = PR.local_csr(part, "boundary", hecgen.Csr)
+        assert Li.n_rows + Lb.n_rows == part.n_loc
+        assert Li.nnz == 0 or int(Li.col.max()) < part.n_loc       # interior reads x_loc only
+        assert Lb.n_rows == 0 or int(Lb.col.max()) >= part.n_loc    # boundary touches the halo
+        assert oracle.is_canonical(Li) and oracle.is_canonical(Lb)
+        # A12: width from all 256 local rows (halo columns count); 6x6x3 = 108 of
+        # them have 7 entries and 3*108 >= 256, so w_p = 7 (BG3 closed form).
+        assert PR.part_width(part, hecgen.Csr) == 7
