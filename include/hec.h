@@ -1,0 +1,261 @@
+/*
+ * hec.h -- C ABI of libhec.so: fp64 sparse matrix-vector multiplication
+ * y = A x in the HEC (hybrid ELL + CSR) format on NVIDIA B200 (sm_100a), on one
+ * GPU and row-partitioned across GPUs with a halo exchange of off-partition x.
+ *
+ * Source of the operations: Yang, Liu, Chen, "Development of Krylov and AMG
+ * linear solvers for large-scale sparse matrices on GPUs" (arXiv 1606.00545),
+ * cited as PAPER.md line numbers (P:n):
+ *   - HEC format: §2.1 "Matrix Format", P:50 (ELL part + CSR remainder with
+ *     arrays Ap/Aj/Ax), P:73 (column-by-column ELL storage, stride a multiple
+ *     of 32 set to 256, ELL/CSR boundary "a recommended value 20").
+ *   - SpMV: §2.2 Alg. 1, P:126-140 (ELL part first, then the CSR part, one
+ *     CUDA core per row); Eq. (1), P:73-122 (y = sum_k x_k A[:,k]).
+ *   - Distribution: §2.2 P:149-158 (row partition -- "sequence partition" for
+ *     FDM/FVM matrices; vector segments; off-segment x entries exchanged
+ *     through a shared cache, here replaced by device-to-device transfers).
+ * Readings of silent/ambiguous passages (A1..A16) are listed in DESIGN.md §3.
+ *
+ * Conventions (all functions):
+ *   - Every call returns hec_status; no C++ exception crosses the ABI.  On
+ *     failure hec_last_error() returns a thread-local message for the last
+ *     failing call on the calling thread.
+ *   - Host input arrays are BORROWED for the duration of the call (copied).
+ *   - Handles are owned by the caller and released with the matching *_free.
+ *   - Device pointers (x, y) are caller-owned, fp64, contiguous; `stream` is a
+ *     cudaStream_t passed as void* (NULL = legacy default stream).  Compute
+ *     calls are asynchronous with respect to the host; asynchronous CUDA/NCCL
+ *     faults surface at the next synchronising call.
+ *   - Indices are int32 and values fp64, as the paper's CSR (reading A8:
+ *     Table 2's Mb(CSR) = round((12 nnz + 4(n+1))/2^20) for all 12 matrices).
+ *   - There is no CPU fallback: a compute call on a handle without a device,
+ *     or on a host without a CUDA device, fails with HEC_ERR_NODEV / _CUDA.
+ */
+#ifndef HEC_H
+#define HEC_H
+
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+typedef enum {
+    HEC_OK = 0,
+    HEC_ERR_ARG = 1,     /* NULL handle/pointer, negative size, unknown enum, aliasing x/y */
+    HEC_ERR_FORMAT = 2,  /* non-canonical CSR (reading A7): row_ptr[0] != 0,
+                            decreasing row_ptr, row_ptr[n] != nnz, unsorted or duplicate
+                            columns within a row, column out of [0, n_cols) */
+    HEC_ERR_DIM = 3,     /* length mismatch (e.g. distributed mode on a non-square A) */
+    HEC_ERR_PARTS = 4,   /* n_parts < 1 or > n_rows, grid dims inconsistent with n,
+                            more parts than grid planes, part index out of range */
+    HEC_ERR_CUDA = 5,    /* a CUDA runtime call failed (message in hec_last_error) */
+    HEC_ERR_NCCL = 6,    /* an NCCL call failed */
+    HEC_ERR_NOMEM = 7,   /* host or device allocation failed */
+    HEC_ERR_STATE = 8,   /* handle used in the wrong mode (rank/plan mismatch, ...) */
+    HEC_ERR_NODEV = 9    /* compute requested on a host-only handle (device = -1) */
+} hec_status;
+
+const char* hec_last_error(void);
+const char* hec_version(void);
+
+/* ------------------------------------------------------------ matrices ---- */
+
+/* Canonical CSR (Ap = row_ptr, Aj = col_idx, Ax = val).
+ * row_ptr[n_rows+1], col_idx[nnz], val[nnz]; host memory, borrowed. */
+typedef struct {
+    int32_t n_rows, n_cols;
+    int64_t nnz;
+    const int32_t* row_ptr;
+    const int32_t* col_idx;
+    const double* val;
+} hec_csr;
+
+enum { HEC_WIDTH_BG3 = 0, HEC_WIDTH_CAP = 1, HEC_WIDTH_FIXED = 2 };
+
+/* Conversion options (NULL -> defaults: BG3, cap 20, stride_unit 256).
+ *   width_policy  HEC_WIDTH_BG3 (reading A1): w = min(cap, k*), k* = smallest
+ *                 k >= 0 with 3 * #{rows: len > k} < n_rows;
+ *                 HEC_WIDTH_CAP: w = min(cap, max row length);
+ *                 HEC_WIDTH_FIXED: w = fixed_width.
+ *   cap           ELL/CSR boundary, default 20 ("a recommended value 20").
+ *   stride_unit   ELL stride s = roundup(n_rows, stride_unit); a positive
+ *                 multiple of 32, default 256 (reading A2). */
+typedef struct {
+    int32_t width_policy;
+    int32_t cap;
+    int32_t fixed_width;
+    int32_t stride_unit;
+} hec_opts;
+
+void hec_opts_default(hec_opts* o);
+
+typedef struct hec_matrix_s* hec_matrix;
+
+typedef struct {
+    int32_t n_rows, n_cols;
+    int32_t ell_width;     /* w */
+    int32_t ell_stride;    /* s */
+    int64_t nnz;           /* nnz(A) = ell_nnz + tail_nnz */
+    int64_t ell_nnz;       /* non-padding ELL slots */
+    int32_t tail_rows;     /* rows that spill into the CSR part */
+    int32_t tail_group;    /* lanes per tail row used by the tail kernel (1..32) */
+    int64_t tail_nnz;
+    int64_t device_bytes;  /* bytes of device arrays owned by the handle */
+    int32_t device;        /* CUDA device ordinal, or -1 for a host-only handle */
+    int32_t reserved;
+} hec_matrix_info;
+
+/* Caller-allocated export buffers, sized from hec_matrix_info:
+ * ell_col/ell_val [w*s] column-major (slot j of row i at j*s + i; padding
+ * slots are (-1, +0.0), reading A4); tail_rows [tail_rows] ascending;
+ * tail_ptr [tail_rows+1]; tail_col/tail_val [tail_nnz] (reading A15: the CSR
+ * part is compact, only rows with a spill).  Any pointer may be NULL to skip. */
+typedef struct {
+    int32_t* ell_col;
+    double* ell_val;
+    int32_t* tail_rows;
+    int32_t* tail_ptr;
+    int32_t* tail_col;
+    double* tail_val;
+} hec_host_arrays;
+
+/* CSR -> HEC conversion (readings A1-A4, A15).  Validates A
+ * (HEC_ERR_FORMAT), chooses w, fills the column-major ELL part with each row's
+ * first min(len, w) entries in column order and the compact CSR tail with the
+ * rest.  device >= 0: uploads to that CUDA device on `stream` (synchronised
+ * before return).  device == -1: host-only handle, usable with hec_info and
+ * hec_export (conversion checks without a GPU) but not for compute. */
+hec_status hec_from_csr(const hec_csr* A, const hec_opts* o, int32_t device, void* stream,
+                        hec_matrix* out);
+hec_status hec_info(hec_matrix A, hec_matrix_info* out);
+hec_status hec_export(hec_matrix A, hec_host_arrays* out);
+
+/* y = A x (Alg. 1): the ELL kernel writes every row of y, then the
+ * CSR-tail kernel adds the spilled entries of the tail rows.  x: device,
+ * n_cols doubles; y: device, n_rows doubles, fully overwritten; x and y must
+ * not overlap (HEC_ERR_ARG).  Asynchronous on `stream`. */
+hec_status hec_spmv(hec_matrix A, const double* x, double* y, void* stream);
+
+/* Same product with HOST x and y (n_cols / n_rows doubles; pinned memory is
+ * fastest).  Copies x host->device, runs hec_spmv on library-owned device
+ * buffers, copies y device->host and synchronises `stream` before returning. */
+hec_status hec_spmv_host(hec_matrix A, const double* x_host, double* y_host, void* stream);
+
+/* Number of kernels one hec_spmv launches on this matrix (1 or 2). */
+int32_t hec_spmv_launches(hec_matrix A);
+
+void hec_free(hec_matrix A);
+
+/* ---------------------------------------------------------- partitions ---- */
+
+enum { HEC_PART_CONTIG_NNZ = 0, HEC_PART_CONTIG_ROWS = 1, HEC_PART_GRID = 2 };
+
+typedef struct hec_plan_s* hec_plan;
+
+/* Row partition + halo plan ("sequence partition", P:158 vector
+ * segments and the exchange of entries "a segment vector can not provide";
+ * readings A9-A12).  A must be square (the row partition is also the vector
+ * partition).  kind:
+ *   HEC_PART_GRID: grid = {nx, ny, nz} with nx*ny*nz = n; part p owns planes
+ *     [floor(p*E/P), floor((p+1)*E/P)) of the slowest axis with extent E > 1.
+ *   HEC_PART_CONTIG_ROWS: part_ptr[p] = floor(p*n/P).
+ *   HEC_PART_CONTIG_NNZ: part_ptr[p] = lower_bound(row_ptr, ceil(p*nnz/P)),
+ *     then max(., part_ptr[p-1]+1), then min(., n-(P-p)).
+ * For every part: recv = sorted global columns referenced outside the part;
+ * sends to peer q = sorted local indices of recv_q inside the part; boundary
+ * rows = rows with any off-part column; interior = the rest.  Host-only,
+ * deterministic, immutable. */
+hec_status hec_partition(const hec_csr* A, int32_t n_parts, int32_t kind, const int32_t* grid,
+                         hec_plan* out);
+
+typedef struct {
+    int32_t r0, r1;          /* owned global rows [r0, r1) */
+    int32_t n_halo;          /* |recv| */
+    int32_t n_send;          /* total entries sent to all peers */
+    int32_t n_interior, n_boundary;
+    int32_t n_recv_peers, n_send_peers;
+    int32_t width;           /* partition ELL width (reading A12) under the opts given to
+                                hec_plan_part_info_opts; BG3/20 for hec_plan_part_info */
+    int32_t reserved;
+} hec_part_info;
+
+/* Caller-allocated: recv_cols[n_halo] (global, ascending), recv_off[P+1],
+ * send_idx[n_send] (local), send_off[P+1], interior[n_interior] and
+ * boundary[n_boundary] (local row ids, ascending).  NULL entries are skipped. */
+typedef struct {
+    int32_t* recv_cols;
+    int32_t* recv_off;
+    int32_t* send_idx;
+    int32_t* send_off;
+    int32_t* interior;
+    int32_t* boundary;
+} hec_plan_arrays;
+
+hec_status hec_plan_n_parts(hec_plan P, int32_t* n_parts);
+hec_status hec_plan_part_ptr(hec_plan P, int32_t* part_ptr /* [n_parts+1] */);
+hec_status hec_plan_part_info(hec_plan P, int32_t part, hec_part_info* out);
+hec_status hec_plan_part_info_opts(hec_plan P, int32_t part, const hec_opts* o, hec_part_info* out);
+hec_status hec_plan_export(hec_plan P, int32_t part, hec_plan_arrays* out);
+
+enum { HEC_SUB_INTERIOR = 0, HEC_SUB_BOUNDARY = 1, HEC_SUB_ALL = 2 };
+
+/* HEC of one part's local rows (which = interior, boundary, or all), with local
+ * columns (owned -> [0, n_loc), halo entry g -> n_loc + position of g in recv),
+ * each row in ascending local-column order, and the partition's width
+ * (reading A12).  A must be the matrix the plan was built from. */
+hec_status hec_plan_part_hec(hec_plan P, const hec_csr* A, int32_t part, int32_t which,
+                             const hec_opts* o, int32_t device, void* stream, hec_matrix* out);
+void hec_plan_free(hec_plan P);
+
+/* -------------------------------------------------------- distributed ---- */
+
+typedef struct hec_dist_s* hec_dist;
+
+#define HEC_NCCL_ID_BYTES 128
+
+/* Rank 0 creates the NCCL unique id and broadcasts it (e.g. torch.distributed). */
+hec_status hec_nccl_unique_id(uint8_t id[HEC_NCCL_ID_BYTES]);
+
+/* COLLECTIVE over the n_parts ranks (ncclCommInitRank).  Builds this rank's
+ * interior and boundary sub-HECs on `device`, the halo send list, the send and
+ * x_halo buffers, a high-priority communication stream and events. */
+hec_status hec_dist_create(const hec_csr* A, hec_plan P, const hec_opts* o, int32_t rank,
+                           const uint8_t id[HEC_NCCL_ID_BYTES], int32_t device, hec_dist* out);
+
+/* Single-process emulation of all n_parts ranks on ONE device (for testing the
+ * distributed kernels on one GPU): out[n_parts] handles whose exchange is a
+ * device-to-device copy instead of NCCL.  Free each with hec_dist_free. */
+hec_status hec_dist_create_local(const hec_csr* A, hec_plan P, const hec_opts* o, int32_t device,
+                                 hec_dist* out);
+
+/* COLLECTIVE: y_local = (A x)[r0:r1] for this rank (every rank calls it in the
+ * same order).  x_local/y_local: device, n_loc doubles, must not overlap.
+ * On `stream`: the interior SpMV (x_local only) runs while a high-priority
+ * stream packs x_local[send_idx] and exchanges it with the peers (NCCL
+ * grouped send/recv); the boundary SpMV waits for the exchange.  Asynchronous;
+ * ordered after prior work on `stream` and before later work on it. */
+hec_status hec_spmv_dist(hec_dist D, const double* x_local, double* y_local, void* stream);
+
+/* Local emulation: one call performs the exchange and both SpMV phases for
+ * all n handles created by hec_dist_create_local, in rank order, on `stream`. */
+hec_status hec_spmv_dist_local(hec_dist* D, int32_t n, const double* const* x_locals,
+                               double* const* y_locals, void* stream);
+
+typedef struct {
+    int32_t rank, n_parts, r0, r1, n_halo, n_send;
+    int32_t n_interior, n_boundary;
+    int32_t width;
+    int32_t launches;        /* kernels this rank launches per hec_spmv_dist (excl. NCCL) */
+    int64_t device_bytes;
+    int64_t algorithmic_bytes;  /* 12 nnz_loc + 8 (n_loc + n_halo) + 8 n_loc */
+    int64_t nnz_local;
+} hec_dist_info;
+
+hec_status hec_dist_get_info(hec_dist D, hec_dist_info* out);
+void hec_dist_free(hec_dist D);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* HEC_H */

@@ -1,0 +1,314 @@
+// dist.cpp -- row-partitioned HEC SpMV with halo exchange (one process per GPU).
+//
+// PAPER.md §2.2: each GPU holds one (partition matrix, segment
+// vector) pair; the x entries a segment "can not provide" are exchanged -- in
+// the paper through a host-resident shared cache.  Here (reading A13) the
+// exchange is device to device: a pack kernel gathers x_local[send_idx] into a
+// contiguous send buffer and grouped NCCL send/recv over NVLink deliver each
+// peer's slice into this rank's x_halo (ordered by peer, reading A10).  The
+// rows are split into interior (x_local only) and boundary (reading A11): the
+// interior SpMV runs on the caller's stream while the pack + exchange run on a
+// high-priority communication stream; the boundary SpMV waits for the halo.
+#include <cstring>
+#include <memory>
+
+#include <nccl.h>
+
+#include "hec_internal.h"
+
+struct LocalGroup;
+
+struct hec_dist_s {
+    int32_t rank = 0, n_parts = 1, device = 0;
+    int32_t r0 = 0, r1 = 0, n_halo = 0, n_send = 0;
+    int32_t n_interior = 0, n_boundary = 0, width = 0;
+    int64_t nnz_local = 0;
+    hec_matrix interior = nullptr, boundary = nullptr;
+    int32_t* d_send_idx = nullptr;
+    double* d_sendbuf = nullptr;
+    double* d_x_halo = nullptr;
+    std::vector<int32_t> send_off, recv_off;
+    ncclComm_t comm = nullptr;
+    bool local = false;
+    cudaStream_t comm_stream = nullptr;
+    cudaEvent_t ev_start = nullptr, ev_halo = nullptr;
+    int64_t device_bytes = 0;
+};
+
+namespace hec {
+
+static hec_status nccl_fail(ncclResult_t r, const char* what) {
+    return fail(HEC_ERR_NCCL, std::string("NCCL error in ") + what + ": " + ncclGetErrorString(r));
+}
+
+#define HEC_NCCL_TRY(expr)                                          \
+    do {                                                            \
+        ncclResult_t _r = (expr);                                   \
+        if (_r != ncclSuccess) return ::hec::nccl_fail(_r, #expr);  \
+    } while (0)
+
+static void dist_release(hec_dist_s* d) {
+    if (!d) return;
+    int cur = 0;
+    cudaGetDevice(&cur);
+    cudaSetDevice(d->device);
+    if (d->comm) ncclCommDestroy(d->comm);
+    if (d->ev_start) cudaEventDestroy(d->ev_start);
+    if (d->ev_halo) cudaEventDestroy(d->ev_halo);
+    if (d->comm_stream) cudaStreamDestroy(d->comm_stream);
+    if (d->d_send_idx) cudaFree(d->d_send_idx);
+    if (d->d_sendbuf) cudaFree(d->d_sendbuf);
+    if (d->d_x_halo) cudaFree(d->d_x_halo);
+    hec_free(d->interior);
+    hec_free(d->boundary);
+    cudaSetDevice(cur);
+    delete d;
+}
+
+// A sub-HEC (interior or boundary rows) whose output rows are either one
+// contiguous range (row_off) or an explicit row map.
+static hec_status make_sub(const hec_plan_s& P, const CsrView& A, int32_t part, int32_t which,
+                           const hec_opts& op, int32_t width, int32_t device, cudaStream_t s,
+                           hec_matrix* out) {
+    const PartPlan& pt = P.parts[part];
+    const std::vector<int32_t>& rows = which == HEC_SUB_INTERIOR ? pt.interior : pt.boundary;
+    CsrOwned L;
+    HostHec h;
+    hec_status st = build_local_csr(P, A, part, which, &L);
+    if (st != HEC_OK) return st;
+    if ((st = convert(L.view(), width, op.stride_unit, &h)) != HEC_OK) return st;
+    bool contiguous = true;
+    for (size_t k = 1; k < rows.size() && contiguous; ++k) contiguous = rows[k] == rows[0] + (int32_t)k;
+    const int32_t n_loc = pt.r1 - pt.r0;
+    if (contiguous)
+        return make_matrix(std::move(h), device, s, nullptr, 0, rows.empty() ? 0 : rows[0], n_loc, out);
+    return make_matrix(std::move(h), device, s, rows.data(), (int32_t)rows.size(), 0, n_loc, out);
+}
+
+static hec_status dist_build(const hec_csr* A, hec_plan P, const hec_opts* o, int32_t rank,
+                             int32_t device, bool local, hec_dist_s** out) {
+    CsrView v;
+    hec_status st = validate_csr(A, &v);
+    if (st != HEC_OK) return st;
+    if (v.n_rows != P->n_rows || v.nnz != P->nnz) return fail(HEC_ERR_STATE, "matrix does not match the plan");
+    if (rank < 0 || rank >= P->n_parts) return fail(HEC_ERR_PARTS, "rank out of range");
+    const hec_opts op = normalise_opts(o);
+    if ((st = check_opts(op)) != HEC_OK) return st;
+    int n_dev = 0;
+    if (cudaGetDeviceCount(&n_dev) != cudaSuccess || n_dev == 0)
+        return fail(HEC_ERR_NODEV, "no CUDA device available");
+    if (device < 0 || device >= n_dev) return fail(HEC_ERR_ARG, "device ordinal out of range");
+    int prev = 0;
+    cudaGetDevice(&prev);
+    HEC_CUDA_TRY(cudaSetDevice(device));
+    std::unique_ptr<hec_dist_s, void (*)(hec_dist_s*)> d(new hec_dist_s(), dist_release);
+    const PartPlan& pt = P->parts[rank];
+    d->rank = rank;
+    d->n_parts = P->n_parts;
+    d->device = device;
+    d->r0 = pt.r0;
+    d->r1 = pt.r1;
+    d->n_halo = (int32_t)pt.recv.size();
+    d->n_send = (int32_t)pt.send_idx.size();
+    d->n_interior = (int32_t)pt.interior.size();
+    d->n_boundary = (int32_t)pt.boundary.size();
+    d->nnz_local = (int64_t)P->row_ptr[pt.r1] - P->row_ptr[pt.r0];
+    d->send_off = pt.send_off;
+    d->recv_off = pt.recv_off;
+    d->local = local;
+    d->width = part_width(*P, rank, op);
+    cudaStream_t s = nullptr;
+    HEC_CUDA_TRY(cudaStreamCreateWithFlags(&s, cudaStreamNonBlocking));
+    try {
+        st = make_sub(*P, v, rank, HEC_SUB_INTERIOR, op, d->width, device, s, &d->interior);
+        if (st == HEC_OK) st = make_sub(*P, v, rank, HEC_SUB_BOUNDARY, op, d->width, device, s, &d->boundary);
+    } catch (...) {
+        st = fail(HEC_ERR_NOMEM, "host allocation failed in hec_dist_create");
+    }
+    if (st != HEC_OK) { cudaStreamDestroy(s); cudaSetDevice(prev); return st; }
+    int64_t bytes = d->interior->device_bytes + d->boundary->device_bytes;
+    cudaError_t e = cudaSuccess;
+    if (d->n_send > 0) {
+        e = cudaMalloc(&d->d_send_idx, sizeof(int32_t) * d->n_send);
+        if (e == cudaSuccess) e = cudaMemcpyAsync(d->d_send_idx, pt.send_idx.data(), sizeof(int32_t) * d->n_send, cudaMemcpyHostToDevice, s);
+        if (e == cudaSuccess) e = cudaMalloc(&d->d_sendbuf, sizeof(double) * d->n_send);
+        bytes += (int64_t)d->n_send * 12;
+    }
+    if (e == cudaSuccess && d->n_halo > 0) {
+        e = cudaMalloc(&d->d_x_halo, sizeof(double) * d->n_halo);
+        bytes += (int64_t)d->n_halo * 8;
+    }
+    if (e == cudaSuccess) e = cudaStreamSynchronize(s);
+    cudaStreamDestroy(s);
+    if (e != cudaSuccess) { cudaSetDevice(prev); return cuda_fail(e, "dist buffers"); }
+    int lo = 0, hi = 0;
+    cudaDeviceGetStreamPriorityRange(&lo, &hi);  // hi = greatest priority
+    e = cudaStreamCreateWithPriority(&d->comm_stream, cudaStreamNonBlocking, hi);
+    if (e == cudaSuccess) e = cudaEventCreateWithFlags(&d->ev_start, cudaEventDisableTiming);
+    if (e == cudaSuccess) e = cudaEventCreateWithFlags(&d->ev_halo, cudaEventDisableTiming);
+    cudaSetDevice(prev);
+    if (e != cudaSuccess) return cuda_fail(e, "dist streams/events");
+    d->device_bytes = bytes;
+    *out = d.release();
+    return HEC_OK;
+}
+
+static bool has_exchange(const hec_dist_s* d) { return d->n_halo > 0 || d->n_send > 0; }
+
+}  // namespace hec
+
+using namespace hec;
+
+extern "C" {
+
+hec_status hec_nccl_unique_id(uint8_t id[HEC_NCCL_ID_BYTES]) {
+    if (!id) return fail(HEC_ERR_ARG, "NULL id");
+    static_assert(sizeof(ncclUniqueId) == HEC_NCCL_ID_BYTES, "ncclUniqueId size");
+    ncclUniqueId u;
+    HEC_NCCL_TRY(ncclGetUniqueId(&u));
+    std::memcpy(id, &u, HEC_NCCL_ID_BYTES);
+    return HEC_OK;
+}
+
+hec_status hec_dist_create(const hec_csr* A, hec_plan P, const hec_opts* o, int32_t rank,
+                           const uint8_t id[HEC_NCCL_ID_BYTES], int32_t device, hec_dist* out) {
+    if (!out || !P) return fail(HEC_ERR_ARG, "NULL argument");
+    *out = nullptr;
+    hec_dist_s* d = nullptr;
+    hec_status st = dist_build(A, P, o, rank, device, false, &d);
+    if (st != HEC_OK) return st;
+    if (P->n_parts > 1) {
+        if (!id) { dist_release(d); return fail(HEC_ERR_ARG, "NULL NCCL id"); }
+        ncclUniqueId u;
+        std::memcpy(&u, id, HEC_NCCL_ID_BYTES);
+        int prev = 0;
+        cudaGetDevice(&prev);
+        cudaSetDevice(device);
+        ncclResult_t r = ncclCommInitRank(&d->comm, P->n_parts, u, rank);
+        cudaSetDevice(prev);
+        if (r != ncclSuccess) { dist_release(d); return nccl_fail(r, "ncclCommInitRank"); }
+    }
+    *out = d;
+    return HEC_OK;
+}
+
+hec_status hec_dist_create_local(const hec_csr* A, hec_plan P, const hec_opts* o, int32_t device,
+                                 hec_dist* out) {
+    if (!out || !P) return fail(HEC_ERR_ARG, "NULL argument");
+    for (int32_t p = 0; p < P->n_parts; ++p) out[p] = nullptr;
+    for (int32_t p = 0; p < P->n_parts; ++p) {
+        hec_dist_s* d = nullptr;
+        hec_status st = dist_build(A, P, o, p, device, true, &d);
+        if (st != HEC_OK) {
+            for (int32_t q = 0; q < p; ++q) { dist_release(out[q]); out[q] = nullptr; }
+            return st;
+        }
+        out[p] = d;
+    }
+    return HEC_OK;
+}
+
+hec_status hec_spmv_dist(hec_dist D, const double* x_local, double* y_local, void* stream) {
+    if (!D) return fail(HEC_ERR_ARG, "NULL handle");
+    if (D->local) return fail(HEC_ERR_STATE, "local-emulation handle: use hec_spmv_dist_local");
+    const int32_t n_loc = D->r1 - D->r0;
+    if (n_loc > 0 && (!x_local || !y_local)) return fail(HEC_ERR_ARG, "NULL x_local/y_local");
+    if (x_local && y_local && x_local < y_local + n_loc && y_local < x_local + n_loc)
+        return fail(HEC_ERR_ARG, "x_local and y_local overlap");
+    cudaStream_t s = (cudaStream_t)stream;
+    int prev = 0;
+    cudaGetDevice(&prev);
+    if (prev != D->device) cudaSetDevice(D->device);
+    hec_status st = HEC_OK;
+    const bool ex = has_exchange(D) && D->comm;
+    if (ex) {
+        // comm stream: pack + grouped send/recv, overlapped with the interior SpMV
+        cudaError_t e = cudaEventRecord(D->ev_start, s);
+        if (e == cudaSuccess) e = cudaStreamWaitEvent(D->comm_stream, D->ev_start, 0);
+        if (e == cudaSuccess) e = launch_pack(D->d_send_idx, D->n_send, x_local, D->d_sendbuf, D->comm_stream);
+        if (e != cudaSuccess) { cudaSetDevice(prev); return cuda_fail(e, "halo pack"); }
+        ncclResult_t r = ncclGroupStart();
+        for (int32_t q = 0; q < D->n_parts && r == ncclSuccess; ++q) {
+            const int32_t sc = D->send_off[q + 1] - D->send_off[q];
+            const int32_t rc = D->recv_off[q + 1] - D->recv_off[q];
+            if (sc > 0) r = ncclSend(D->d_sendbuf + D->send_off[q], sc, ncclDouble, q, D->comm, D->comm_stream);
+            if (r == ncclSuccess && rc > 0)
+                r = ncclRecv(D->d_x_halo + D->recv_off[q], rc, ncclDouble, q, D->comm, D->comm_stream);
+        }
+        ncclResult_t r2 = ncclGroupEnd();
+        if (r != ncclSuccess || r2 != ncclSuccess) {
+            cudaSetDevice(prev);
+            return nccl_fail(r != ncclSuccess ? r : r2, "halo send/recv");
+        }
+        e = cudaEventRecord(D->ev_halo, D->comm_stream);
+        if (e != cudaSuccess) { cudaSetDevice(prev); return cuda_fail(e, "halo event"); }
+    }
+    st = launch_spmv(D->interior, x_local, nullptr, y_local, s);          // interior rows
+    if (st == HEC_OK && D->n_boundary > 0) {
+        if (ex) {
+            cudaError_t e = cudaStreamWaitEvent(s, D->ev_halo, 0);
+            if (e != cudaSuccess) { cudaSetDevice(prev); return cuda_fail(e, "wait halo"); }
+        }
+        st = launch_spmv(D->boundary, x_local, D->d_x_halo, y_local, s);  // boundary rows
+    }
+    if (prev != D->device) cudaSetDevice(prev);
+    return st;
+}
+
+hec_status hec_spmv_dist_local(hec_dist* D, int32_t n, const double* const* x_locals,
+                               double* const* y_locals, void* stream) {
+    if (!D || n < 1 || !x_locals || !y_locals) return fail(HEC_ERR_ARG, "NULL argument");
+    for (int32_t p = 0; p < n; ++p)
+        if (!D[p] || !D[p]->local || D[p]->rank != p || D[p]->n_parts != n)
+            return fail(HEC_ERR_STATE, "handles must be the n ranks from hec_dist_create_local");
+    cudaStream_t s = (cudaStream_t)stream;
+    int prev = 0;
+    cudaGetDevice(&prev);
+    cudaSetDevice(D[0]->device);
+    for (int32_t p = 0; p < n; ++p) {
+        cudaError_t e = launch_pack(D[p]->d_send_idx, D[p]->n_send, x_locals[p], D[p]->d_sendbuf, s);
+        if (e != cudaSuccess) { cudaSetDevice(prev); return cuda_fail(e, "halo pack"); }
+    }
+    for (int32_t p = 0; p < n; ++p)          // the "exchange": sender p -> receiver q
+        for (int32_t q = 0; q < n; ++q) {
+            const int32_t sc = D[p]->send_off[q + 1] - D[p]->send_off[q];
+            if (sc <= 0) continue;
+            const int32_t rc = D[q]->recv_off[p + 1] - D[q]->recv_off[p];
+            if (rc != sc) { cudaSetDevice(prev); return fail(HEC_ERR_STATE, "send/recv count mismatch"); }
+            cudaError_t e = cudaMemcpyAsync(D[q]->d_x_halo + D[q]->recv_off[p], D[p]->d_sendbuf + D[p]->send_off[q],
+                                            sizeof(double) * sc, cudaMemcpyDeviceToDevice, s);
+            if (e != cudaSuccess) { cudaSetDevice(prev); return cuda_fail(e, "local exchange"); }
+        }
+    for (int32_t p = 0; p < n; ++p) {
+        hec_status st = launch_spmv(D[p]->interior, x_locals[p], nullptr, y_locals[p], s);
+        if (st == HEC_OK && D[p]->n_boundary > 0)
+            st = launch_spmv(D[p]->boundary, x_locals[p], D[p]->d_x_halo, y_locals[p], s);
+        if (st != HEC_OK) { cudaSetDevice(prev); return st; }
+    }
+    cudaSetDevice(prev);
+    return HEC_OK;
+}
+
+hec_status hec_dist_get_info(hec_dist D, hec_dist_info* o) {
+    if (!D || !o) return fail(HEC_ERR_ARG, "NULL argument");
+    o->rank = D->rank;
+    o->n_parts = D->n_parts;
+    o->r0 = D->r0;
+    o->r1 = D->r1;
+    o->n_halo = D->n_halo;
+    o->n_send = D->n_send;
+    o->n_interior = D->n_interior;
+    o->n_boundary = D->n_boundary;
+    o->width = D->width;
+    o->launches = hec_spmv_launches(D->interior) + hec_spmv_launches(D->boundary) +
+                  (has_exchange(D) && D->n_send > 0 ? 1 : 0);
+    o->device_bytes = D->device_bytes;
+    const int64_t n_loc = D->r1 - D->r0;
+    o->algorithmic_bytes = 12 * D->nnz_local + 8 * (n_loc + D->n_halo) + 8 * n_loc;
+    o->nnz_local = D->nnz_local;
+    return HEC_OK;
+}
+
+void hec_dist_free(hec_dist D) { dist_release(D); }
+
+}  // extern "C"

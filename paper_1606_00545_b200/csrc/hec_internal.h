@@ -1,0 +1,160 @@
+// hec_internal.h -- internal declarations shared by the libhec.so sources.
+// Not part of the ABI (that is include/hec.h).
+#pragma once
+
+#include <cstdint>
+#include <string>
+#include <vector>
+
+#include <cuda_runtime.h>
+
+#include "hec.h"
+
+namespace hec {
+
+// ----------------------------------------------------------------- errors --
+void set_error(const std::string& msg);
+hec_status fail(hec_status st, const std::string& msg);
+hec_status cuda_fail(cudaError_t e, const char* what);
+
+#define HEC_CUDA_TRY(expr)                                              \
+    do {                                                                \
+        cudaError_t _e = (expr);                                        \
+        if (_e != cudaSuccess) return ::hec::cuda_fail(_e, #expr);      \
+    } while (0)
+
+// --------------------------------------------------------------- host HEC --
+// A CSR view with int64 offsets (the public struct uses int32 row_ptr).
+struct CsrView {
+    int32_t n_rows = 0, n_cols = 0;
+    int64_t nnz = 0;
+    const int32_t* row_ptr = nullptr;
+    const int32_t* col = nullptr;
+    const double* val = nullptr;
+};
+
+// Host-side local CSR (owned storage) used for partition sub-matrices.
+struct CsrOwned {
+    int32_t n_rows = 0, n_cols = 0;
+    std::vector<int32_t> row_ptr, col;
+    std::vector<double> val;
+    CsrView view() const {
+        CsrView v;
+        v.n_rows = n_rows; v.n_cols = n_cols; v.nnz = (int64_t)col.size();
+        v.row_ptr = row_ptr.data(); v.col = col.data(); v.val = val.data();
+        return v;
+    }
+};
+
+struct HostHec {
+    int32_t n_rows = 0, n_cols = 0, width = 0, stride = 0;
+    int64_t nnz = 0, ell_nnz = 0;
+    std::vector<int32_t> ell_col;   // [width*stride], column-major, -1 = padding
+    std::vector<double> ell_val;    // [width*stride], +0.0 padding
+    std::vector<int32_t> tail_rows, tail_ptr, tail_col;
+    std::vector<double> tail_val;
+};
+
+hec_status validate_csr(const hec_csr* A, CsrView* out);
+hec_opts normalise_opts(const hec_opts* o);
+hec_status check_opts(const hec_opts& o);
+// Width from a row-length histogram (reading A1).
+int32_t choose_width(const CsrView& A, const hec_opts& o);
+// CSR -> HEC fill with a given width (readings A2-A4, A15).
+hec_status convert(const CsrView& A, int32_t width, int32_t stride_unit, HostHec* out);
+int32_t tail_group_for(const HostHec& h);
+
+// ------------------------------------------------------------------ plans --
+struct PartPlan {
+    int32_t r0 = 0, r1 = 0;
+    std::vector<int32_t> recv;       // global columns, ascending
+    std::vector<int32_t> recv_off;   // [P+1]
+    std::vector<int32_t> send_idx;   // local indices, concatenated over peers
+    std::vector<int32_t> send_off;   // [P+1]
+    std::vector<int32_t> interior, boundary;
+};
+
+}  // namespace hec
+
+struct hec_plan_s {
+    int32_t n_parts = 0;
+    int32_t n_rows = 0;
+    int64_t nnz = 0;
+    std::vector<int32_t> part_ptr;
+    std::vector<int32_t> row_ptr;    // copy of the global row_ptr (row lengths, A12)
+    std::vector<hec::PartPlan> parts;
+};
+
+namespace hec {
+// Local sub-matrix of a part (which = HEC_SUB_*), local column numbering.
+hec_status build_local_csr(const hec_plan_s& P, const CsrView& A, int32_t part, int32_t which,
+                           CsrOwned* out);
+int32_t part_width(const hec_plan_s& P, int32_t part, const hec_opts& o);
+hec_status build_plan(const CsrView& A, int32_t P, int32_t kind, const int32_t* grid,
+                      hec_plan_s* plan);
+}  // namespace hec
+
+// ------------------------------------------------------------ device HEC --
+struct hec_matrix_s {
+    int32_t device = -1;
+    int32_t n_rows = 0, n_cols = 0, width = 0, stride = 0;
+    int64_t nnz = 0, ell_nnz = 0, tail_nnz = 0;
+    int32_t tail_rows = 0, tail_group = 32;
+    hec::HostHec host;                 // full copy only for host-only handles
+    std::vector<int32_t> h_tail_rows;  // local tail row ids (always kept; small)
+    // device arrays
+    int32_t* d_ell_col = nullptr;
+    double* d_ell_val = nullptr;
+    int32_t* d_tail_out = nullptr;     // output row of each tail row (after row map)
+    int32_t* d_tail_ptr = nullptr;
+    int32_t* d_tail_col = nullptr;
+    double* d_tail_val = nullptr;
+    int32_t* d_rowmap = nullptr;       // output row of each row, or null (then row_off + i)
+    int32_t row_off = 0;
+    int32_t n_loc = -1;                // >= 0: columns >= n_loc read x_halo[c - n_loc]
+    double* d_stage_x = nullptr;       // hec_spmv_host staging
+    double* d_stage_y = nullptr;
+    int64_t device_bytes = 0;
+};
+
+namespace hec {
+// Build a device (or host-only) matrix handle from a host HEC.
+hec_status make_matrix(HostHec&& h, int32_t device, cudaStream_t s, const int32_t* rowmap,
+                       int32_t n_rowmap, int32_t row_off, int32_t n_loc, hec_matrix* out);
+// Launch the HEC product (ELL kernel then tail kernel) for one handle.
+hec_status launch_spmv(const hec_matrix_s* A, const double* x, const double* x_halo, double* y,
+                       cudaStream_t s);
+}  // namespace hec
+
+// ---------------------------------------------------------------- kernels --
+namespace hec {
+struct EllArgs {
+    const int32_t* col;
+    const double* val;
+    int64_t stride;
+    int32_t n_rows;
+    int32_t width;
+    const double* x;
+    const double* x_halo;
+    int32_t n_loc;
+    double* y;
+    const int32_t* rowmap;
+    int32_t row_off;
+};
+struct TailArgs {
+    int32_t n_tail;
+    const int32_t* out_rows;
+    const int32_t* ptr;
+    const int32_t* col;
+    const double* val;
+    const double* x;
+    const double* x_halo;
+    int32_t n_loc;
+    double* y;
+    int32_t group;
+};
+cudaError_t launch_ell(const EllArgs& a, cudaStream_t s);
+cudaError_t launch_tail(const TailArgs& a, cudaStream_t s);
+cudaError_t launch_pack(const int32_t* idx, int32_t n, const double* x, double* out,
+                        cudaStream_t s);
+}  // namespace hec

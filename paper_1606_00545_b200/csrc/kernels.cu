@@ -1,0 +1,269 @@
+// kernels.cu -- sm_100a kernels of the HEC SpMV hot path.
+//
+//   ell_kernel   Alg. 1 lines 1-3: every row's ELL part,
+//                y_i = sum_{j<w, col != -1} ELLval[j*s+i] * x[ELLcol[j*s+i]].
+//                Column-major slots make a warp's slot-j loads one
+//                contiguous segment; each thread owns 2 adjacent rows so values
+//                arrive as 128-bit (double2) and indices as 64-bit (int2)
+//                loads.  The matrix streams are read once with L1::no_allocate
+//                and an L2 evict_first policy so x stays cached for the gathers.
+//   tail_kernel  Alg. 1 lines 5-7: the CSR remainder of the rows
+//                that spill, G lanes per row, reduced with __shfl_xor_sync and
+//                added into the ELL result (ordered after ell_kernel).
+//   pack_kernel  the halo export of P:158: sendbuf[k] = x_local[send_idx[k]].
+//
+// No tensor cores: SpMV is not a dense contraction (BASELINE.json north_star);
+// the roofline is HBM bandwidth.
+#include <cuda_runtime.h>
+
+#include <cstdint>
+
+#include "hec_internal.h"
+
+namespace hec {
+
+// ------------------------------------------------------------ PTX helpers --
+__device__ __forceinline__ uint64_t policy_evict_first() {
+    uint64_t p;
+    asm("createpolicy.fractional.L2::evict_first.b64 %0, 1.0;" : "=l"(p));
+    return p;
+}
+
+__device__ __forceinline__ int2 ld_stream_i2(const int32_t* ptr, uint64_t pol) {
+    int2 r;
+    asm("ld.global.nc.L1::no_allocate.L2::cache_hint.v2.s32 {%0, %1}, [%2], %3;"
+                 : "=r"(r.x), "=r"(r.y)
+                 : "l"(ptr), "l"(pol));
+    return r;
+}
+
+__device__ __forceinline__ double2 ld_stream_d2(const double* ptr, uint64_t pol) {
+    double2 r;
+    asm("ld.global.nc.L1::no_allocate.L2::cache_hint.v2.f64 {%0, %1}, [%2], %3;"
+                 : "=d"(r.x), "=d"(r.y)
+                 : "l"(ptr), "l"(pol));
+    return r;
+}
+
+// volatile variants: issue order pinned so every slot load of a row pair is in
+// flight before the first x gather (ptxas otherwise sinks them to their use).
+__device__ __forceinline__ int2 ld_stream_i2v(const int32_t* ptr, uint64_t pol) {
+    int2 r;
+    asm volatile("ld.global.nc.L1::no_allocate.L2::cache_hint.v2.s32 {%0, %1}, [%2], %3;"
+                 : "=r"(r.x), "=r"(r.y)
+                 : "l"(ptr), "l"(pol));
+    return r;
+}
+
+__device__ __forceinline__ double2 ld_stream_d2v(const double* ptr, uint64_t pol) {
+    double2 r;
+    asm volatile("ld.global.nc.L1::no_allocate.L2::cache_hint.v2.f64 {%0, %1}, [%2], %3;"
+                 : "=d"(r.x), "=d"(r.y)
+                 : "l"(ptr), "l"(pol));
+    return r;
+}
+
+__device__ __forceinline__ int32_t ld_stream_i1(const int32_t* ptr, uint64_t pol) {
+    int32_t r;
+    asm("ld.global.nc.L1::no_allocate.L2::cache_hint.s32 %0, [%1], %2;"
+                 : "=r"(r)
+                 : "l"(ptr), "l"(pol));
+    return r;
+}
+
+__device__ __forceinline__ double ld_stream_d1(const double* ptr, uint64_t pol) {
+    double r;
+    asm("ld.global.nc.L1::no_allocate.L2::cache_hint.f64 %0, [%1], %2;"
+                 : "=d"(r)
+                 : "l"(ptr), "l"(pol));
+    return r;
+}
+
+__device__ __forceinline__ void st_stream_d2(double* ptr, double a, double b) {
+    asm volatile("st.global.cs.v2.f64 [%0], {%1, %2};" ::"l"(ptr), "d"(a), "d"(b) : "memory");
+}
+
+__device__ __forceinline__ void st_stream_d1(double* ptr, double a) {
+    asm volatile("st.global.cs.f64 [%0], %1;" ::"l"(ptr), "d"(a) : "memory");
+}
+
+// x gather: columns >= n_loc live in the halo buffer (distributed boundary).
+template <bool HALO>
+__device__ __forceinline__ double gather_x(const double* __restrict__ x,
+                                           const double* __restrict__ xh, int32_t n_loc,
+                                           int32_t c) {
+    if (HALO && c >= n_loc) return __ldg(xh + (c - n_loc));
+    return __ldg(x + c);
+}
+
+// ------------------------------------------------------------- ELL kernel --
+// W > 0: width known at compile time (fully unrolled); W == 0: runtime width.
+template <int W, bool HALO, bool ROWMAP>
+__global__ void __launch_bounds__(256) ell_kernel(EllArgs a) {
+    const uint64_t pol = policy_evict_first();
+    const int32_t width = W > 0 ? W : a.width;
+    const int64_t s = a.stride;
+    const int64_t n_pairs = ((int64_t)a.n_rows + 1) >> 1;
+    for (int64_t pr = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; pr < n_pairs;
+         pr += (int64_t)gridDim.x * blockDim.x) {
+        const int64_t i0 = pr << 1;  // rows i0, i0+1 (i0+1 < s because s is even)
+        const int32_t* cp = a.col + i0;
+        const double* vp = a.val + i0;
+        double acc0 = 0.0, acc1 = 0.0;
+        if (W > 0) {
+            // All slot loads of the row pair first (2W independent 64/128-bit
+            // streams in flight), then the x gathers, then the FMAs in slot order.
+            constexpr int WW = W > 0 ? W : 1;
+            int2 c[WW];
+            double2 v[WW];
+#pragma unroll
+            for (int j = 0; j < WW; ++j) c[j] = ld_stream_i2v(cp + j * s, pol);
+#pragma unroll
+            for (int j = 0; j < WW; ++j) v[j] = ld_stream_d2v(vp + j * s, pol);
+            double x0[WW], x1[WW];
+#pragma unroll
+            for (int j = 0; j < WW; ++j) {
+                x0[j] = c[j].x >= 0 ? gather_x<HALO>(a.x, a.x_halo, a.n_loc, c[j].x) : 0.0;
+                x1[j] = c[j].y >= 0 ? gather_x<HALO>(a.x, a.x_halo, a.n_loc, c[j].y) : 0.0;
+            }
+#pragma unroll
+            for (int j = 0; j < WW; ++j) {
+                acc0 = fma(v[j].x, x0[j], acc0);
+                acc1 = fma(v[j].y, x1[j], acc1);
+            }
+        } else {
+#pragma unroll 4
+            for (int j = 0; j < width; ++j) {
+                const int2 c = ld_stream_i2(cp + j * s, pol);
+                const double2 v = ld_stream_d2(vp + j * s, pol);
+                const double x0 = c.x >= 0 ? gather_x<HALO>(a.x, a.x_halo, a.n_loc, c.x) : 0.0;
+                const double x1 = c.y >= 0 ? gather_x<HALO>(a.x, a.x_halo, a.n_loc, c.y) : 0.0;
+                acc0 = fma(v.x, x0, acc0);
+                acc1 = fma(v.y, x1, acc1);
+            }
+        }
+        if (ROWMAP) {
+            st_stream_d1(a.y + a.rowmap[i0], acc0);
+            if (i0 + 1 < a.n_rows) st_stream_d1(a.y + a.rowmap[i0 + 1], acc1);
+        } else {
+            double* yp = a.y + a.row_off + i0;
+            if (i0 + 1 < a.n_rows && ((reinterpret_cast<uintptr_t>(yp) & 15) == 0)) {
+                st_stream_d2(yp, acc0, acc1);
+            } else {
+                st_stream_d1(yp, acc0);
+                if (i0 + 1 < a.n_rows) st_stream_d1(yp + 1, acc1);
+            }
+        }
+    }
+}
+
+// ------------------------------------------------------------ tail kernel --
+template <int G, bool HALO>
+__global__ void __launch_bounds__(256) tail_kernel(TailArgs a) {
+    const uint64_t pol = policy_evict_first();
+    const int lane = threadIdx.x & (G - 1);
+    const int64_t groups_per_grid = ((int64_t)gridDim.x * blockDim.x) / G;
+    int64_t g = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) / G;
+    // Loop bound is uniform across the warp so every lane reaches the shuffles.
+    const int64_t n_iter_groups = ((int64_t)a.n_tail + groups_per_grid - 1) / groups_per_grid;
+    for (int64_t it = 0; it < n_iter_groups; ++it, g += groups_per_grid) {
+        double acc = 0.0;
+        int32_t row = -1;
+        if (g < a.n_tail) {
+            const int32_t b = __ldg(a.ptr + g), e = __ldg(a.ptr + g + 1);
+            for (int32_t k = b + lane; k < e; k += G) {
+                const int32_t c = ld_stream_i1(a.col + k, pol);
+                const double v = ld_stream_d1(a.val + k, pol);
+                acc = fma(v, gather_x<HALO>(a.x, a.x_halo, a.n_loc, c), acc);
+            }
+            row = __ldg(a.out_rows + g);
+        }
+#pragma unroll
+        for (int off = G / 2; off > 0; off >>= 1) acc += __shfl_xor_sync(0xffffffffu, acc, off, G);
+        if (lane == 0 && row >= 0) a.y[row] += acc;
+    }
+}
+
+// ------------------------------------------------------------ pack kernel --
+__global__ void __launch_bounds__(256) pack_kernel(const int32_t* __restrict__ idx, int32_t n,
+                                                   const double* __restrict__ x,
+                                                   double* __restrict__ out) {
+    for (int32_t k = blockIdx.x * blockDim.x + threadIdx.x; k < n; k += gridDim.x * blockDim.x)
+        out[k] = __ldg(x + __ldg(idx + k));
+}
+
+// --------------------------------------------------------------- launchers --
+static int g_num_sms = 0;
+
+static int num_sms() {
+    if (g_num_sms == 0) {
+        int dev = 0;
+        cudaGetDevice(&dev);
+        cudaDeviceGetAttribute(&g_num_sms, cudaDevAttrMultiProcessorCount, dev);
+        if (g_num_sms <= 0) g_num_sms = 148;
+    }
+    return g_num_sms;
+}
+
+template <bool HALO, bool ROWMAP>
+static cudaError_t launch_ell_t(const EllArgs& a, cudaStream_t s) {
+    const int64_t n_pairs = ((int64_t)a.n_rows + 1) >> 1;
+    const int threads = 256;
+    int64_t blocks = (n_pairs + threads - 1) / threads;
+    const int64_t cap = (int64_t)num_sms() * 8 * 64;  // grid-stride beyond 64 waves
+    if (blocks > cap) blocks = cap;
+    if (blocks < 1) blocks = 1;
+    const dim3 g((unsigned)blocks), b(threads);
+    switch (a.width) {
+#define HEC_W(w) \
+    case w: ell_kernel<w, HALO, ROWMAP><<<g, b, 0, s>>>(a); break;
+        HEC_W(1) HEC_W(2) HEC_W(3) HEC_W(4) HEC_W(5) HEC_W(6) HEC_W(7) HEC_W(8)
+        HEC_W(9) HEC_W(10) HEC_W(11) HEC_W(12) HEC_W(13) HEC_W(14) HEC_W(15) HEC_W(16)
+#undef HEC_W
+        default: ell_kernel<0, HALO, ROWMAP><<<g, b, 0, s>>>(a); break;
+    }
+    return cudaGetLastError();
+}
+
+cudaError_t launch_ell(const EllArgs& a, cudaStream_t s) {
+    if (a.n_rows <= 0) return cudaSuccess;
+    const bool halo = a.x_halo != nullptr;
+    const bool rowmap = a.rowmap != nullptr;
+    if (halo) return rowmap ? launch_ell_t<true, true>(a, s) : launch_ell_t<true, false>(a, s);
+    return rowmap ? launch_ell_t<false, true>(a, s) : launch_ell_t<false, false>(a, s);
+}
+
+template <bool HALO>
+static cudaError_t launch_tail_t(const TailArgs& a, cudaStream_t s) {
+    const int threads = 256;
+    const int64_t groups_per_block = threads / a.group;
+    int64_t blocks = (a.n_tail + groups_per_block - 1) / groups_per_block;
+    const int64_t cap = (int64_t)num_sms() * 8 * 16;
+    if (blocks > cap) blocks = cap;
+    if (blocks < 1) blocks = 1;
+    const dim3 g((unsigned)blocks), b(threads);
+    switch (a.group) {
+        case 2: tail_kernel<2, HALO><<<g, b, 0, s>>>(a); break;
+        case 4: tail_kernel<4, HALO><<<g, b, 0, s>>>(a); break;
+        case 8: tail_kernel<8, HALO><<<g, b, 0, s>>>(a); break;
+        case 16: tail_kernel<16, HALO><<<g, b, 0, s>>>(a); break;
+        default: tail_kernel<32, HALO><<<g, b, 0, s>>>(a); break;
+    }
+    return cudaGetLastError();
+}
+
+cudaError_t launch_tail(const TailArgs& a, cudaStream_t s) {
+    if (a.n_tail <= 0) return cudaSuccess;
+    return a.x_halo ? launch_tail_t<true>(a, s) : launch_tail_t<false>(a, s);
+}
+
+cudaError_t launch_pack(const int32_t* idx, int32_t n, const double* x, double* out,
+                        cudaStream_t s) {
+    if (n <= 0) return cudaSuccess;
+    int blocks = (n + 255) / 256;
+    if (blocks > num_sms() * 8) blocks = num_sms() * 8;
+    pack_kernel<<<blocks, 256, 0, s>>>(idx, n, x, out);
+    return cudaGetLastError();
+}
+
+}  // namespace hec

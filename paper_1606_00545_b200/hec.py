@@ -1,0 +1,484 @@
+"""Thin ctypes binding of libhec.so (include/hec.h) -- argument marshalling only.
+
+Every step of the SpMV path runs inside libhec.so (host converter/planner in
+C++, kernels in CUDA for sm_100a).  PyTorch supplies device memory, streams and
+process groups.  There is no CPU fallback: if the library cannot be loaded the
+import fails, and compute on a host-only handle raises.
+"""
+from __future__ import annotations
+
+import ctypes
+import os
+from dataclasses import dataclass
+
+import numpy as np
+
+from . import _build
+
+# ----------------------------------------------------------------- loading --
+_lib = None
+
+
+class HecError(RuntimeError):
+    def __init__(self, status: int, msg: str):
+        super().__init__(f"hec status {status}: {msg}")
+        self.status = status
+
+
+STATUS = {0: "HEC_OK", 1: "HEC_ERR_ARG", 2: "HEC_ERR_FORMAT", 3: "HEC_ERR_DIM", 4: "HEC_ERR_PARTS",
+          5: "HEC_ERR_CUDA", 6: "HEC_ERR_NCCL", 7: "HEC_ERR_NOMEM", 8: "HEC_ERR_STATE", 9: "HEC_ERR_NODEV"}
+WIDTH_BG3, WIDTH_CAP, WIDTH_FIXED = 0, 1, 2
+PART_CONTIG_NNZ, PART_CONTIG_ROWS, PART_GRID = 0, 1, 2
+SUB_INTERIOR, SUB_BOUNDARY, SUB_ALL = 0, 1, 2
+NCCL_ID_BYTES = 128
+
+i32, i64, vp, dbl = ctypes.c_int32, ctypes.c_int64, ctypes.c_void_p, ctypes.c_double
+
+
+class CsrT(ctypes.Structure):
+    _fields_ = [("n_rows", i32), ("n_cols", i32), ("nnz", i64),
+                ("row_ptr", vp), ("col_idx", vp), ("val", vp)]
+
+
+class OptsT(ctypes.Structure):
+    _fields_ = [("width_policy", i32), ("cap", i32), ("fixed_width", i32), ("stride_unit", i32)]
+
+
+class MatrixInfoT(ctypes.Structure):
+    _fields_ = [("n_rows", i32), ("n_cols", i32), ("ell_width", i32), ("ell_stride", i32),
+                ("nnz", i64), ("ell_nnz", i64), ("tail_rows", i32), ("tail_group", i32),
+                ("tail_nnz", i64), ("device_bytes", i64), ("device", i32), ("reserved", i32)]
+
+
+class HostArraysT(ctypes.Structure):
+    _fields_ = [("ell_col", vp), ("ell_val", vp), ("tail_rows", vp), ("tail_ptr", vp),
+                ("tail_col", vp), ("tail_val", vp)]
+
+
+class PartInfoT(ctypes.Structure):
+    _fields_ = [("r0", i32), ("r1", i32), ("n_halo", i32), ("n_send", i32), ("n_interior", i32),
+                ("n_boundary", i32), ("n_recv_peers", i32), ("n_send_peers", i32), ("width", i32),
+                ("reserved", i32)]
+
+
+class PlanArraysT(ctypes.Structure):
+    _fields_ = [("recv_cols", vp), ("recv_off", vp), ("send_idx", vp), ("send_off", vp),
+                ("interior", vp), ("boundary", vp)]
+
+
+class DistInfoT(ctypes.Structure):
+    _fields_ = [("rank", i32), ("n_parts", i32), ("r0", i32), ("r1", i32), ("n_halo", i32),
+                ("n_send", i32), ("n_interior", i32), ("n_boundary", i32), ("width", i32),
+                ("launches", i32), ("device_bytes", i64), ("algorithmic_bytes", i64),
+                ("nnz_local", i64)]
+
+
+EXPORTED = [
+    "hec_last_error", "hec_version", "hec_opts_default", "hec_from_csr", "hec_info", "hec_export",
+    "hec_spmv", "hec_spmv_host", "hec_spmv_launches", "hec_free", "hec_partition",
+    "hec_plan_n_parts", "hec_plan_part_ptr", "hec_plan_part_info", "hec_plan_part_info_opts",
+    "hec_plan_export", "hec_plan_part_hec", "hec_plan_free", "hec_nccl_unique_id",
+    "hec_dist_create", "hec_dist_create_local", "hec_spmv_dist", "hec_spmv_dist_local",
+    "hec_dist_get_info", "hec_dist_free",
+]
+
+
+def lib_path() -> str:
+    return _build.LIB
+
+
+def load(build: bool = True):
+    """Load libhec.so (building it in-tree first if stale).  Import torch
+    before calling this so the process shares torch's libnccl.so.2."""
+    global _lib
+    if _lib is not None:
+        return _lib
+    try:
+        import torch  # noqa: F401  (maps torch's NCCL/cudart first)
+    except Exception:
+        pass
+    path = _build.build() if build else _build.LIB
+    if not os.path.exists(path):
+        raise ImportError(f"libhec.so not built at {path}")
+    L = ctypes.CDLL(path)
+    st = ctypes.c_int
+    L.hec_last_error.restype = ctypes.c_char_p
+    L.hec_version.restype = ctypes.c_char_p
+    L.hec_opts_default.restype = None
+    L.hec_opts_default.argtypes = [ctypes.POINTER(OptsT)]
+    L.hec_from_csr.restype = st
+    L.hec_from_csr.argtypes = [ctypes.POINTER(CsrT), ctypes.POINTER(OptsT), i32, vp, ctypes.POINTER(vp)]
+    L.hec_info.restype = st
+    L.hec_info.argtypes = [vp, ctypes.POINTER(MatrixInfoT)]
+    L.hec_export.restype = st
+    L.hec_export.argtypes = [vp, ctypes.POINTER(HostArraysT)]
+    L.hec_spmv.restype = st
+    L.hec_spmv.argtypes = [vp, vp, vp, vp]
+    L.hec_spmv_host.restype = st
+    L.hec_spmv_host.argtypes = [vp, vp, vp, vp]
+    L.hec_spmv_launches.restype = i32
+    L.hec_spmv_launches.argtypes = [vp]
+    L.hec_free.restype = None
+    L.hec_free.argtypes = [vp]
+    L.hec_partition.restype = st
+    L.hec_partition.argtypes = [ctypes.POINTER(CsrT), i32, i32, vp, ctypes.POINTER(vp)]
+    L.hec_plan_n_parts.restype = st
+    L.hec_plan_n_parts.argtypes = [vp, ctypes.POINTER(i32)]
+    L.hec_plan_part_ptr.restype = st
+    L.hec_plan_part_ptr.argtypes = [vp, vp]
+    L.hec_plan_part_info.restype = st
+    L.hec_plan_part_info.argtypes = [vp, i32, ctypes.POINTER(PartInfoT)]
+    L.hec_plan_part_info_opts.restype = st
+    L.hec_plan_part_info_opts.argtypes = [vp, i32, ctypes.POINTER(OptsT), ctypes.POINTER(PartInfoT)]
+    L.hec_plan_export.restype = st
+    L.hec_plan_export.argtypes = [vp, i32, ctypes.POINTER(PlanArraysT)]
+    L.hec_plan_part_hec.restype = st
+    L.hec_plan_part_hec.argtypes = [vp, ctypes.POINTER(CsrT), i32, i32, ctypes.POINTER(OptsT), i32, vp,
+                                    ctypes.POINTER(vp)]
+    L.hec_plan_free.restype = None
+    L.hec_plan_free.argtypes = [vp]
+    L.hec_nccl_unique_id.restype = st
+    L.hec_nccl_unique_id.argtypes = [vp]
+    L.hec_dist_create.restype = st
+    L.hec_dist_create.argtypes = [ctypes.POINTER(CsrT), vp, ctypes.POINTER(OptsT), i32, vp, i32,
+                                  ctypes.POINTER(vp)]
+    L.hec_dist_create_local.restype = st
+    L.hec_dist_create_local.argtypes = [ctypes.POINTER(CsrT), vp, ctypes.POINTER(OptsT), i32, vp]
+    L.hec_spmv_dist.restype = st
+    L.hec_spmv_dist.argtypes = [vp, vp, vp, vp]
+    L.hec_spmv_dist_local.restype = st
+    L.hec_spmv_dist_local.argtypes = [vp, i32, vp, vp, vp]
+    L.hec_dist_get_info.restype = st
+    L.hec_dist_get_info.argtypes = [vp, ctypes.POINTER(DistInfoT)]
+    L.hec_dist_free.restype = None
+    L.hec_dist_free.argtypes = [vp]
+    _lib = L
+    return L
+
+
+def _check(status: int):
+    if status != 0:
+        msg = _lib.hec_last_error().decode(errors="replace")
+        raise HecError(status, f"{STATUS.get(status, '?')}: {msg}")
+
+
+def _p(a: np.ndarray) -> int:
+    return a.ctypes.data if a.size else 0
+
+
+# ------------------------------------------------------------------- inputs --
+class _CsrArgs:
+    """Keeps contiguous int32/float64 copies alive while a call borrows them."""
+
+    def __init__(self, A):
+        self.row_ptr = np.ascontiguousarray(A.row_ptr, dtype=np.int32)
+        self.col = np.ascontiguousarray(A.col, dtype=np.int32)
+        self.val = np.ascontiguousarray(A.val, dtype=np.float64)
+        self.s = CsrT(int(A.n_rows), int(A.n_cols), int(self.col.shape[0]),
+                      _p(self.row_ptr), _p(self.col), _p(self.val))
+
+    def ref(self):
+        return ctypes.byref(self.s)
+
+
+def opts(width_policy: int = WIDTH_BG3, cap: int = 20, fixed_width: int = 0,
+         stride_unit: int = 256) -> OptsT:
+    return OptsT(width_policy, cap, fixed_width, stride_unit)
+
+
+def _stream_ptr(stream) -> int:
+    if stream is None:
+        import torch
+        return torch.cuda.current_stream().cuda_stream
+    if isinstance(stream, int):
+        return stream
+    return stream.cuda_stream
+
+
+def _dptr(t, n: int, name: str) -> int:
+    import torch
+    if not isinstance(t, torch.Tensor) or t.device.type != "cuda":
+        raise TypeError(f"{name} must be a CUDA tensor")
+    if t.dtype != torch.float64 or not t.is_contiguous() or t.numel() < n:
+        raise ValueError(f"{name} must be contiguous float64 with >= {n} elements")
+    return t.data_ptr()
+
+
+@dataclass
+class HecArrays:
+    width: int
+    stride: int
+    ell_col: np.ndarray
+    ell_val: np.ndarray
+    tail_rows: np.ndarray
+    tail_ptr: np.ndarray
+    tail_col: np.ndarray
+    tail_val: np.ndarray
+
+
+# ------------------------------------------------------------------ matrix --
+class Matrix:
+    """HEC matrix handle (hec_from_csr).  device=-1 builds a host-only handle
+    (for conversion checks without a GPU; compute refuses it)."""
+
+    def __init__(self, A=None, options: OptsT | None = None, device: int = 0, stream=None,
+                 _handle: int | None = None):
+        L = load()
+        self._h = vp()
+        if _handle is not None:
+            self._h = vp(_handle)
+        else:
+            args = _CsrArgs(A)
+            o = options if options is not None else opts()
+            s = _stream_ptr(stream) if device >= 0 else 0
+            _check(L.hec_from_csr(args.ref(), ctypes.byref(o), device, s, ctypes.byref(self._h)))
+        self.info = self._info()
+
+    def _info(self) -> MatrixInfoT:
+        inf = MatrixInfoT()
+        _check(_lib.hec_info(self._h, ctypes.byref(inf)))
+        return inf
+
+    @property
+    def handle(self) -> int:
+        return self._h.value
+
+    @property
+    def n_rows(self) -> int:
+        return self.info.n_rows
+
+    @property
+    def n_cols(self) -> int:
+        return self.info.n_cols
+
+    def export(self) -> HecArrays:
+        inf = self.info
+        slots = inf.ell_width * inf.ell_stride
+        a = HecArrays(inf.ell_width, inf.ell_stride, np.empty(slots, np.int32), np.empty(slots, np.float64),
+                      np.empty(inf.tail_rows, np.int32), np.empty(inf.tail_rows + 1, np.int32),
+                      np.empty(inf.tail_nnz, np.int32), np.empty(inf.tail_nnz, np.float64))
+        h = HostArraysT(_p(a.ell_col), _p(a.ell_val), _p(a.tail_rows), _p(a.tail_ptr), _p(a.tail_col),
+                        _p(a.tail_val))
+        _check(_lib.hec_export(self._h, ctypes.byref(h)))
+        return a
+
+    def spmv(self, x, y, stream=None):
+        """y = A x on the device (async on `stream`, default torch's current)."""
+        _check(_lib.hec_spmv(self._h, _dptr(x, self.n_cols, "x"), _dptr(y, self.n_rows, "y"),
+                             _stream_ptr(stream)))
+        return y
+
+    def spmv_host(self, x: np.ndarray, y: np.ndarray | None = None, stream=None) -> np.ndarray:
+        """y = A x with host buffers (numpy or pinned torch tensors); synchronous."""
+        if y is None:
+            y = np.empty(self.n_rows, np.float64)
+        xp = x.data_ptr() if hasattr(x, "data_ptr") else _p(np.ascontiguousarray(x, dtype=np.float64))
+        yp = y.data_ptr() if hasattr(y, "data_ptr") else _p(y)
+        _check(_lib.hec_spmv_host(self._h, xp, yp, _stream_ptr(stream)))
+        return y
+
+    @property
+    def launches(self) -> int:
+        return int(_lib.hec_spmv_launches(self._h))
+
+    def free(self):
+        if self._h and self._h.value:
+            _lib.hec_free(self._h)
+            self._h = vp()
+
+    def __del__(self):
+        try:
+            self.free()
+        except Exception:
+            pass
+
+
+def from_csr(A, options: OptsT | None = None, device: int = 0, stream=None) -> Matrix:
+    return Matrix(A, options, device, stream)
+
+
+# -------------------------------------------------------------------- plan --
+@dataclass
+class PartArrays:
+    r0: int
+    r1: int
+    width: int
+    recv_cols: np.ndarray
+    recv_off: np.ndarray
+    send_idx: np.ndarray
+    send_off: np.ndarray
+    interior: np.ndarray
+    boundary: np.ndarray
+
+
+class Plan:
+    """Row partition + halo plan (hec_partition); host-only."""
+
+    def __init__(self, A, n_parts: int, kind: int = PART_CONTIG_NNZ, grid=None):
+        L = load()
+        self._h = vp()
+        args = _CsrArgs(A)
+        g = (ctypes.c_int32 * 3)(*grid) if grid is not None else None
+        _check(L.hec_partition(args.ref(), n_parts, kind, ctypes.cast(g, vp) if g is not None else None,
+                               ctypes.byref(self._h)))
+        self.n_parts = n_parts
+
+    @property
+    def handle(self) -> int:
+        return self._h.value
+
+    def part_ptr(self) -> np.ndarray:
+        pp = np.empty(self.n_parts + 1, np.int32)
+        _check(_lib.hec_plan_part_ptr(self._h, _p(pp)))
+        return pp
+
+    def part_info(self, part: int, options: OptsT | None = None) -> PartInfoT:
+        inf = PartInfoT()
+        if options is None:
+            _check(_lib.hec_plan_part_info(self._h, part, ctypes.byref(inf)))
+        else:
+            _check(_lib.hec_plan_part_info_opts(self._h, part, ctypes.byref(options), ctypes.byref(inf)))
+        return inf
+
+    def export(self, part: int, options: OptsT | None = None) -> PartArrays:
+        inf = self.part_info(part, options)
+        P = self.n_parts
+        a = PartArrays(inf.r0, inf.r1, inf.width, np.empty(inf.n_halo, np.int32), np.empty(P + 1, np.int32),
+                       np.empty(inf.n_send, np.int32), np.empty(P + 1, np.int32),
+                       np.empty(inf.n_interior, np.int32), np.empty(inf.n_boundary, np.int32))
+        h = PlanArraysT(_p(a.recv_cols), _p(a.recv_off), _p(a.send_idx), _p(a.send_off), _p(a.interior),
+                        _p(a.boundary))
+        _check(_lib.hec_plan_export(self._h, part, ctypes.byref(h)))
+        return a
+
+    def part_hec(self, A, part: int, which: int, options: OptsT | None = None, device: int = -1,
+                 stream=None) -> Matrix:
+        args = _CsrArgs(A)
+        o = options if options is not None else opts()
+        h = vp()
+        s = _stream_ptr(stream) if device >= 0 else 0
+        _check(_lib.hec_plan_part_hec(self._h, args.ref(), part, which, ctypes.byref(o), device, s,
+                                      ctypes.byref(h)))
+        return Matrix(_handle=h.value)
+
+    def free(self):
+        if self._h and self._h.value:
+            _lib.hec_plan_free(self._h)
+            self._h = vp()
+
+    def __del__(self):
+        try:
+            self.free()
+        except Exception:
+            pass
+
+
+def partition(A, n_parts: int, kind: int = PART_CONTIG_NNZ, grid=None) -> Plan:
+    return Plan(A, n_parts, kind, grid)
+
+
+# ------------------------------------------------------------- distributed --
+def nccl_unique_id() -> bytes:
+    load()
+    buf = (ctypes.c_uint8 * NCCL_ID_BYTES)()
+    _check(_lib.hec_nccl_unique_id(ctypes.cast(buf, vp)))
+    return bytes(buf)
+
+
+class Dist:
+    """One rank of the row-partitioned SpMV (hec_dist_create / hec_spmv_dist)."""
+
+    def __init__(self, A=None, plan: Plan | None = None, rank: int = 0, nccl_id: bytes | None = None,
+                 device: int = 0, options: OptsT | None = None, _handle: int | None = None):
+        load()
+        self._h = vp()
+        if _handle is not None:
+            self._h = vp(_handle)
+        else:
+            args = _CsrArgs(A)
+            o = options if options is not None else opts()
+            idbuf = (ctypes.c_uint8 * NCCL_ID_BYTES).from_buffer_copy(nccl_id) if nccl_id else None
+            _check(_lib.hec_dist_create(args.ref(), plan.handle, ctypes.byref(o), rank,
+                                        ctypes.cast(idbuf, vp) if idbuf is not None else None, device,
+                                        ctypes.byref(self._h)))
+        self.info = DistInfoT()
+        _check(_lib.hec_dist_get_info(self._h, ctypes.byref(self.info)))
+
+    @property
+    def handle(self) -> int:
+        return self._h.value
+
+    @property
+    def n_loc(self) -> int:
+        return self.info.r1 - self.info.r0
+
+    def spmv(self, x_local, y_local, stream=None):
+        _check(_lib.hec_spmv_dist(self._h, _dptr(x_local, self.n_loc, "x_local"),
+                                  _dptr(y_local, self.n_loc, "y_local"), _stream_ptr(stream)))
+        return y_local
+
+    def free(self):
+        if self._h and self._h.value:
+            _lib.hec_dist_free(self._h)
+            self._h = vp()
+
+    def __del__(self):
+        try:
+            self.free()
+        except Exception:
+            pass
+
+
+class LocalDistGroup:
+    """All ranks of a partition emulated on ONE device (hec_dist_create_local):
+    same kernels and plan, exchange by device-to-device copies."""
+
+    def __init__(self, A, plan: Plan, device: int = 0, options: OptsT | None = None):
+        load()
+        args = _CsrArgs(A)
+        o = options if options is not None else opts()
+        arr = (vp * plan.n_parts)()
+        _check(_lib.hec_dist_create_local(args.ref(), plan.handle, ctypes.byref(o), device, arr))
+        self.ranks = [Dist(_handle=arr[p]) for p in range(plan.n_parts)]
+        self._arr = arr
+
+    def spmv(self, x_locals, y_locals, stream=None):
+        n = len(self.ranks)
+        xs = (vp * n)(*[_dptr(x_locals[p], self.ranks[p].n_loc, "x_local") for p in range(n)])
+        ys = (vp * n)(*[_dptr(y_locals[p], self.ranks[p].n_loc, "y_local") for p in range(n)])
+        _check(_lib.hec_spmv_dist_local(self._arr, n, xs, ys, _stream_ptr(stream)))
+        return y_locals
+
+    def free(self):
+        for r in self.ranks:
+            r.free()
+
+
+def exchange_halo_host(plan: Plan, rank: int, x_local: np.ndarray, group=None) -> np.ndarray:
+    """Host-side halo exchange over a torch.distributed process group (e.g.
+    gloo) following the plan's send/recv lists -- the same pattern the NCCL
+    path runs on the device.  Returns x_halo (ordered as recv_cols)."""
+    import torch
+    import torch.distributed as dist
+    a = plan.export(rank)
+    P = plan.n_parts
+    halo = np.empty(len(a.recv_cols), np.float64)
+    reqs, bufs = [], []
+    for q in range(P):
+        lo, hi = int(a.send_off[q]), int(a.send_off[q + 1])
+        if hi > lo:
+            t = torch.from_numpy(np.ascontiguousarray(x_local[a.send_idx[lo:hi]]))
+            bufs.append(t)
+            reqs.append(dist.isend(t, dst=q, group=group))
+    recvs = []
+    for q in range(P):
+        lo, hi = int(a.recv_off[q]), int(a.recv_off[q + 1])
+        if hi > lo:
+            t = torch.empty(hi - lo, dtype=torch.float64)
+            recvs.append((lo, hi, t))
+            reqs.append(dist.irecv(t, src=q, group=group))
+    for r in reqs:
+        r.wait()
+    for lo, hi, t in recvs:
+        halo[lo:hi] = t.numpy()
+    return halo

@@ -1,0 +1,207 @@
+"""GPU parity of hec_spmv (ELL kernel + CSR-tail kernel, sm_100a) against the
+serial CPU oracle O1, called through the C ABI.
+
+Bar (BASELINE.json north_star): |y_gpu - y_ref|_i <= 1e-12 (|A||x|)_i in fp64;
+bitwise in the integer-exact regime (pin P3: every partial sum is an exact
+integer, so any summation order gives the same bits)."""
+import numpy as np
+import pytest
+
+import hecgen
+import oracle
+
+pytestmark = pytest.mark.gpu
+
+torch = pytest.importorskip("torch")
+if not torch.cuda.is_available():  # pragma: no cover
+    pytest.skip("needs a CUDA device", allow_module_level=True)
+
+import paper_1606_00545_b200 as hec  # noqa: E402
+
+
+def gpu_spmv(A, x, o=None, M=None):
+    M = M or hec.from_csr(A, o)
+    xd = torch.from_numpy(np.ascontiguousarray(x)).cuda()
+    yd = torch.full((A.n_rows,), float("nan"), dtype=torch.float64, device="cuda")
+    M.spmv(xd, yd)
+    torch.cuda.synchronize()
+    return yd.cpu().numpy(), M
+
+
+def assert_parity(A, x, y, r0=0, r1=None):
+    ref = oracle.csr_spmv(A, x, r0, r1)
+    tol = oracle.tolerance(A, x, r0, r1)
+    bad = np.nonzero(~(np.abs(y - ref) <= tol))[0]
+    assert bad.size == 0, f"{bad.size} rows out of tolerance, first {bad[:5]}: {y[bad[:5]]} vs {ref[bad[:5]]}"
+
+
+CONFIGS = [
+    ("poisson2d_64", lambda: hecgen.poisson2d(64, 64)),          # BASELINE configs[0]
+    ("poisson3d_32", lambda: hecgen.poisson3d(32, 32, 32)),
+    ("spe10", lambda: hecgen.spe10(60, 220, 85)),                # configs[3], full size
+    ("powerlaw_64k", lambda: hecgen.powerlaw(1 << 16)),
+    ("random_rect", lambda: hecgen.random_csr(300, 170, 0.05, seed=3)),
+]
+
+
+@pytest.mark.parametrize("name,maker", CONFIGS)
+def test_parity_uniform_x(name, maker):
+    A = maker()
+    x = hecgen.vector(A.n_cols, "uniform", seed=1606)
+    y, M = gpu_spmv(A, x)
+    assert_parity(A, x, y)
+    if name == "spe10":
+        assert M.info.tail_rows > 0 and M.launches == 2        # the CSR tail is exercised
+
+
+@pytest.mark.parametrize("name,maker", CONFIGS[:4])
+def test_integer_regime_bitwise(name, maker):
+    A = maker()
+    if name == "spe10":
+        pytest.skip("SPE10 coefficients are not integers")
+    if name.startswith("powerlaw"):
+        A = hecgen.powerlaw(1 << 16, integer_values=True)
+    x = hecgen.vector(A.n_cols, "int", seed=7)
+    y, _ = gpu_spmv(A, x)
+    assert y.tobytes() == oracle.csr_spmv(A, x).tobytes()
+
+
+def test_poisson_128_full_parity():
+    # BASELINE configs[1] at full size, element by element.
+    A = hecgen.poisson3d(128, 128, 128)
+    x = hecgen.vector(A.n_cols, "uniform", seed=1606)
+    y, M = gpu_spmv(A, x)
+    assert (M.info.ell_width, M.info.tail_rows) == (7, 0)
+    assert_parity(A, x, y)
+
+
+def test_poisson_256_sampled_and_closed_form():
+    # BASELINE configs[2] at full size in the bench's launch configuration:
+    # sampled rows against the oracle row by row, plus the closed form
+    # (A 1)_i = 6 - deg(i) on every row (exact, bitwise).
+    A = hecgen.poisson3d(256, 256, 256)
+    M = hec.from_csr(A)
+    x = hecgen.vector(A.n_cols, "uniform", seed=1606)
+    y, _ = gpu_spmv(A, x, M=M)
+    rng = np.random.default_rng(0)
+    for r0 in np.concatenate([[0, A.n_rows - 4096], rng.integers(0, A.n_rows - 4096, 30)]):
+        assert_parity(A, x, y[r0:r0 + 4096], int(r0), int(r0) + 4096)
+    ones = np.ones(A.n_cols)
+    y1, _ = gpu_spmv(A, ones, M=M)
+    deg = np.diff(A.row_ptr) - 1
+    assert y1.tobytes() == (6.0 - deg).astype(np.float64).tobytes()
+    # the integer regime at full size: bitwise equal to the oracle everywhere
+    xi = hecgen.vector(A.n_cols, "int", seed=5)
+    yi, _ = gpu_spmv(A, xi, M=M)
+    assert yi.tobytes() == oracle.csr_spmv(A, xi).tobytes()
+
+
+def test_powerlaw_full_size_sampled():
+    # BASELINE configs[4]: 2^23 rows, heavy CSR tail (~31% of rows spill).
+    A = hecgen.powerlaw(1 << 23)
+    x = hecgen.vector(A.n_cols, "uniform", seed=1606)
+    y, M = gpu_spmv(A, x)
+    assert M.info.ell_width == 9 and M.info.tail_rows > 2_000_000
+    rng = np.random.default_rng(1)
+    for r0 in np.concatenate([[0, A.n_rows - 2048], rng.integers(0, A.n_rows - 2048, 20)]):
+        assert_parity(A, x, y[r0:r0 + 2048], int(r0), int(r0) + 2048)
+
+
+@pytest.mark.parametrize("n", [1, 31, 32, 33, 255, 256, 257, 1023])
+@pytest.mark.parametrize("unit", [32, 256])
+def test_sizes_and_strides(n, unit):
+    A = hecgen.random_csr(n, n, min(1.0, 6.0 / n), seed=n)
+    x = hecgen.vector(n, "uniform", seed=n)
+    y, M = gpu_spmv(A, x, hec.opts(stride_unit=unit))
+    assert M.info.ell_stride % unit == 0
+    assert_parity(A, x, y)
+
+
+def test_edge_rows_and_long_tail_row():
+    rows = [[], [(0, 1.0)], [(c, 1.0) for c in range(5)], [(c, -2.0) for c in range(6)], [],
+            [(c, 0.5 + c % 3) for c in range(4000)], []]
+    A = hecgen.from_rows(4000, rows)
+    x = hecgen.vector(4000, "uniform", seed=2)
+    for o in (hec.opts(), hec.opts(hec.WIDTH_FIXED, 0, 5), hec.opts(hec.WIDTH_CAP, 0), hec.opts(hec.WIDTH_CAP, 20)):
+        y, M = gpu_spmv(A, x, o)
+        assert_parity(A, x, y)
+        assert y[0] == 0.0 and y[4] == 0.0 and y[6] == 0.0      # empty rows -> +0.0 (A6)
+
+
+def test_cap_zero_all_tail_and_no_tail():
+    A = hecgen.powerlaw(5000, seed=4)
+    x = hecgen.vector(A.n_cols, "uniform", seed=4)
+    for o in (hec.opts(hec.WIDTH_CAP, 0), hec.opts(hec.WIDTH_CAP, 2000)):
+        y, M = gpu_spmv(A, x, o)
+        assert_parity(A, x, y)
+    assert M.info.tail_rows == 0
+
+
+@pytest.mark.parametrize("shape", [(5, 3), (3, 5), (1000, 10), (10, 1000)])
+def test_rectangular(shape):
+    A = hecgen.random_csr(shape[0], shape[1], 0.4, integer_values=True, seed=sum(shape))
+    x = hecgen.vector(shape[1], "int", seed=1)
+    y, _ = gpu_spmv(A, x)
+    assert y.tobytes() == oracle.csr_spmv(A, x).tobytes()
+
+
+def test_padding_and_unreachable_inf():
+    # Reading A4: padding is (-1, +0.0) and the kernel predicates the x load and
+    # the FMA on col >= 0, so x entries no stored entry references may be Inf/NaN.
+    A = hecgen.random_csr(200, 200, 0.03, seed=8)
+    used = np.zeros(200, bool)
+    used[A.col] = True
+    x = hecgen.vector(200, "uniform", seed=3)
+    x[~used] = np.inf
+    assert (~used).any()
+    y, M = gpu_spmv(A, x, hec.opts(hec.WIDTH_CAP, 20))
+    assert np.all(np.isfinite(y))
+    assert_parity(A, x, y)
+
+
+def test_empty_matrix_and_zero_rows():
+    A = hecgen.from_dense(np.zeros((6, 4)))
+    y, _ = gpu_spmv(A, np.ones(4))
+    assert y.tolist() == [0.0] * 6
+
+
+def test_spmv_host_matches_device():
+    A = hecgen.spe10(20, 30, 10, seed=5)
+    x = hecgen.vector(A.n_cols, "uniform", seed=9)
+    M = hec.from_csr(A)
+    yd, _ = gpu_spmv(A, x, M=M)
+    xp = torch.from_numpy(x).pin_memory()
+    yp = torch.empty(A.n_rows, dtype=torch.float64).pin_memory()
+    M.spmv_host(xp, yp)
+    assert yp.numpy().tobytes() == yd.tobytes()
+    yn = M.spmv_host(x)
+    assert yn.tobytes() == yd.tobytes()
+
+
+def test_export_from_device_matches_host_handle():
+    A = hecgen.powerlaw(3000, seed=12)
+    Md = hec.from_csr(A)
+    Mh = hec.from_csr(A, device=-1)
+    a, b = Md.export(), Mh.export()
+    for f in ("ell_col", "ell_val", "tail_rows", "tail_ptr", "tail_col", "tail_val"):
+        assert getattr(a, f).tobytes() == getattr(b, f).tobytes()
+
+
+def test_aliasing_rejected_and_stream_order():
+    A = hecgen.poisson2d(16, 16)
+    M = hec.from_csr(A)
+    buf = torch.zeros(256, dtype=torch.float64, device="cuda")
+    with pytest.raises(hec.HecError) as e:
+        M.spmv(buf, buf)
+    assert e.value.status == 1
+    # async on a user stream, ordered with torch work on that stream
+    s = torch.cuda.Stream()
+    x = torch.ones(256, dtype=torch.float64, device="cuda")
+    y = torch.empty(256, dtype=torch.float64, device="cuda")
+    with torch.cuda.stream(s):
+        x.mul_(2.0)
+        M.spmv(x, y, stream=s)
+        y.add_(1.0)
+    s.synchronize()
+    ref = oracle.csr_spmv(A, 2.0 * np.ones(256)) + 1.0
+    assert y.cpu().numpy().tobytes() == ref.tobytes()
