@@ -148,15 +148,17 @@ def test_rectangular(shape):
 def test_padding_and_unreachable_inf():
     # Reading A4: padding is (-1, +0.0) and the kernel predicates the x load and
     # the FMA on col >= 0, so x entries no stored entry references may be Inf/NaN.
-    A = hecgen.random_csr(200, 200, 0.03, seed=8)
+    R = hecgen.random_csr(200, 100, 0.06, seed=8)
+    A = hecgen.Csr(200, 200, R.row_ptr, (2 * R.col).astype(np.int32), R.val)   # only even columns stored
     used = np.zeros(200, bool)
     used[A.col] = True
     x = hecgen.vector(200, "uniform", seed=3)
     x[~used] = np.inf
-    assert (~used).any()
-    y, M = gpu_spmv(A, x, hec.opts(hec.WIDTH_CAP, 20))
-    assert np.all(np.isfinite(y))
-    assert_parity(A, x, y)
+    assert (~used).sum() >= 100
+    for o in (hec.opts(hec.WIDTH_CAP, 20), hec.opts(), hec.opts(hec.WIDTH_FIXED, 0, 3)):
+        y, M = gpu_spmv(A, x, o)
+        assert np.all(np.isfinite(y))
+        assert_parity(A, x, y)
 
 
 def test_empty_matrix_and_zero_rows():
