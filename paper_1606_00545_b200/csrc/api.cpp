@@ -27,7 +27,7 @@ static void release(hec_matrix_s* m) {
         int cur = 0;
         cudaGetDevice(&cur);
         cudaSetDevice(m->device);
-        void* ptrs[] = {m->d_ell_col, m->d_ell_val, m->d_tail_out, m->d_tail_ptr, m->d_tail_col,
+        void* ptrs[] = {m->d_ell_col, m->d_ell_val, m->d_tail_out, m->d_tail_order, m->d_tail_ptr, m->d_tail_col,
                         m->d_tail_val, m->d_rowmap, m->d_stage_x, m->d_stage_y};
         for (void* p : ptrs)
             if (p) cudaFree(p);
@@ -61,7 +61,21 @@ hec_status make_matrix(HostHec&& h, int32_t device, cudaStream_t s, const int32_
     m->ell_nnz = h.ell_nnz;
     m->tail_rows = (int32_t)h.tail_rows.size();
     m->tail_nnz = (int64_t)h.tail_col.size();
-    m->tail_group = tail_group_for(h);
+    // bin the tail rows by spilled length (tail kernel lanes per row)
+    std::vector<int32_t> order(h.tail_rows.size());
+    {
+        int64_t cnt[kTailBins] = {0};
+        for (size_t t = 0; t < order.size(); ++t) cnt[tail_bin_of(h.tail_ptr[t + 1] - h.tail_ptr[t])]++;
+        m->tail_bin_off[0] = 0;
+        for (int b = 0; b < kTailBins; ++b) m->tail_bin_off[b + 1] = m->tail_bin_off[b] + cnt[b];
+        int64_t pos[kTailBins];
+        for (int b = 0; b < kTailBins; ++b) pos[b] = m->tail_bin_off[b];
+        for (size_t t = 0; t < order.size(); ++t)
+            order[pos[tail_bin_of(h.tail_ptr[t + 1] - h.tail_ptr[t])]++] = (int32_t)t;
+        int best = 0;
+        for (int b = 1; b < kTailBins; ++b) if (cnt[b] > cnt[best]) best = b;
+        m->tail_group = 1 << best;
+    }
     m->h_tail_rows = h.tail_rows;
     m->row_off = row_off;
     m->n_loc = n_loc;
@@ -83,6 +97,7 @@ hec_status make_matrix(HostHec&& h, int32_t device, cudaStream_t s, const int32_
     for (size_t t = 0; t < tail_out.size(); ++t)
         tail_out[t] = rowmap ? rowmap[h.tail_rows[t]] : row_off + h.tail_rows[t];
     if ((st = dmalloc_copy(&m->d_tail_out, tail_out.data(), tail_out.size(), s, &bytes))) return st;
+    if ((st = dmalloc_copy(&m->d_tail_order, order.data(), order.size(), s, &bytes))) return st;
     if (!h.tail_rows.empty())
         if ((st = dmalloc_copy(&m->d_tail_ptr, h.tail_ptr.data(), h.tail_ptr.size(), s, &bytes))) return st;
     if ((st = dmalloc_copy(&m->d_tail_col, h.tail_col.data(), h.tail_col.size(), s, &bytes))) return st;
@@ -114,6 +129,8 @@ hec_status launch_spmv(const hec_matrix_s* A, const double* x, const double* x_h
     if (A->tail_rows > 0) {              // Alg. 1 lines 5-7: then the CSR part
         TailArgs t;
         t.n_tail = A->tail_rows;
+        t.order = A->d_tail_order;
+        for (int b = 0; b <= kTailBins; ++b) t.bin_off[b] = A->tail_bin_off[b];
         t.out_rows = A->d_tail_out;
         t.ptr = A->d_tail_ptr;
         t.col = A->d_tail_col;
@@ -122,7 +139,6 @@ hec_status launch_spmv(const hec_matrix_s* A, const double* x, const double* x_h
         t.x_halo = x_halo;
         t.n_loc = e.n_loc;
         t.y = y;
-        t.group = A->tail_group;
         err = launch_tail(t, s);
         if (err != cudaSuccess) return cuda_fail(err, "tail_kernel launch");
     }

@@ -155,17 +155,6 @@ hec_status convert(const CsrView& A, int32_t width, int32_t stride_unit, HostHec
     return HEC_OK;
 }
 
-// Lanes per tail row for the CSR-tail kernel: the power of two >= the mean
-// spilled length, in [2, 32] (a tuning choice, not part of the format).
-int32_t tail_group_for(const HostHec& h) {
-    const int64_t tr = (int64_t)h.tail_rows.size();
-    if (tr == 0) return 32;
-    const double mean = (double)h.tail_col.size() / (double)tr;
-    int32_t g = 2;
-    while (g < 32 && g < mean) g *= 2;
-    return g;
-}
-
 }  // namespace hec
 
 extern "C" {

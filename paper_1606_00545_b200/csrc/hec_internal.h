@@ -62,7 +62,15 @@ hec_status check_opts(const hec_opts& o);
 int32_t choose_width(const CsrView& A, const hec_opts& o);
 // CSR -> HEC fill with a given width (readings A2-A4, A15).
 hec_status convert(const CsrView& A, int32_t width, int32_t stride_unit, HostHec* out);
-int32_t tail_group_for(const HostHec& h);
+// Tail rows are binned by spilled length L: bin b uses G = 2^b lanes per row,
+// G = smallest power of two >= ceil(L/2), capped at 32 (a tuning choice, not
+// part of the format).  bin_of(L) is shared by the planner and the launcher.
+constexpr int kTailBins = 6;
+inline int tail_bin_of(int32_t L) {
+    int b = 0;
+    while (b < kTailBins - 1 && (1 << b) * 2 < L) ++b;
+    return b;
+}
 
 // ------------------------------------------------------------------ plans --
 struct PartPlan {
@@ -106,6 +114,8 @@ struct hec_matrix_s {
     int32_t* d_ell_col = nullptr;
     double* d_ell_val = nullptr;
     int32_t* d_tail_out = nullptr;     // output row of each tail row (after row map)
+    int32_t* d_tail_order = nullptr;   // tail row ids grouped by length bin
+    int64_t tail_bin_off[hec::kTailBins + 1] = {0};
     int32_t* d_tail_ptr = nullptr;
     int32_t* d_tail_col = nullptr;
     double* d_tail_val = nullptr;
@@ -143,6 +153,9 @@ struct EllArgs {
 };
 struct TailArgs {
     int32_t n_tail;
+    const int32_t* order;                 // tail rows grouped by bin
+    int64_t bin_off[kTailBins + 1];       // bin b = order[bin_off[b] : bin_off[b+1]]
+    int64_t blk_off[kTailBins + 1];       // first block of bin b (filled by launch_tail)
     const int32_t* out_rows;
     const int32_t* ptr;
     const int32_t* col;
@@ -151,10 +164,10 @@ struct TailArgs {
     const double* x_halo;
     int32_t n_loc;
     double* y;
-    int32_t group;
 };
 cudaError_t launch_ell(const EllArgs& a, cudaStream_t s);
 cudaError_t launch_tail(const TailArgs& a, cudaStream_t s);
+cudaError_t launch_ell_tma(const EllArgs& a, cudaStream_t s, int num_sms);
 cudaError_t launch_pack(const int32_t* idx, int32_t n, const double* x, double* out,
                         cudaStream_t s);
 }  // namespace hec

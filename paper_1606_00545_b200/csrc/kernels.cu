@@ -17,6 +17,8 @@
 #include <cuda_runtime.h>
 
 #include <cstdint>
+#include <cstdlib>
+#include <cstring>
 
 #include "hec_internal.h"
 
@@ -158,30 +160,33 @@ __global__ void __launch_bounds__(256) ell_kernel(EllArgs a) {
 }
 
 // ------------------------------------------------------------ tail kernel --
-template <int G, bool HALO>
+// Tail rows are grouped by spilled length (bin b: G = 2^b lanes per row, each
+// lane handling about two entries); every block belongs to one bin, so G is
+// block-uniform and the xor-shuffle tree runs on whole G-lane groups.
+template <bool HALO>
 __global__ void __launch_bounds__(256) tail_kernel(TailArgs a) {
     const uint64_t pol = policy_evict_first();
+    const int64_t blk = blockIdx.x;
+    int b = 0;
+    while (b < kTailBins - 1 && blk >= a.blk_off[b + 1]) ++b;
+    const int G = 1 << b;
     const int lane = threadIdx.x & (G - 1);
-    const int64_t groups_per_grid = ((int64_t)gridDim.x * blockDim.x) / G;
-    int64_t g = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) / G;
-    // Loop bound is uniform across the warp so every lane reaches the shuffles.
-    const int64_t n_iter_groups = ((int64_t)a.n_tail + groups_per_grid - 1) / groups_per_grid;
-    for (int64_t it = 0; it < n_iter_groups; ++it, g += groups_per_grid) {
-        double acc = 0.0;
-        int32_t row = -1;
-        if (g < a.n_tail) {
-            const int32_t b = __ldg(a.ptr + g), e = __ldg(a.ptr + g + 1);
-            for (int32_t k = b + lane; k < e; k += G) {
-                const int32_t c = ld_stream_i1(a.col + k, pol);
-                const double v = ld_stream_d1(a.val + k, pol);
-                acc = fma(v, gather_x<HALO>(a.x, a.x_halo, a.n_loc, c), acc);
-            }
-            row = __ldg(a.out_rows + g);
+    const int64_t gi = a.bin_off[b] + (blk - a.blk_off[b]) * (256 >> b) + (threadIdx.x >> b);
+    double acc = 0.0;
+    int32_t row = -1;
+    if (gi < a.bin_off[b + 1]) {
+        const int32_t t = __ldg(a.order + gi);
+        const int32_t kb = __ldg(a.ptr + t), ke = __ldg(a.ptr + t + 1);
+#pragma unroll 4
+        for (int32_t k = kb + lane; k < ke; k += G) {
+            const int32_t c = ld_stream_i1(a.col + k, pol);
+            const double v = ld_stream_d1(a.val + k, pol);
+            acc = fma(v, gather_x<HALO>(a.x, a.x_halo, a.n_loc, c), acc);
         }
-#pragma unroll
-        for (int off = G / 2; off > 0; off >>= 1) acc += __shfl_xor_sync(0xffffffffu, acc, off, G);
-        if (lane == 0 && row >= 0) a.y[row] += acc;
+        row = __ldg(a.out_rows + t);
     }
+    for (int off = G >> 1; off > 0; off >>= 1) acc += __shfl_xor_sync(0xffffffffu, acc, off, G);
+    if (lane == 0 && row >= 0) a.y[row] += acc;
 }
 
 // ------------------------------------------------------------ pack kernel --
@@ -225,36 +230,45 @@ static cudaError_t launch_ell_t(const EllArgs& a, cudaStream_t s) {
     return cudaGetLastError();
 }
 
+// ELL kernel choice: "reg" (register-streaming ell_kernel) or "tma" (bulk-copy
+// pipeline, ell_tma.cu).  HEC_ELL_KERNEL overrides the default (tuning only).
+static int ell_variant() {
+    static int v = -1;
+    if (v < 0) {
+        const char* e = std::getenv("HEC_ELL_KERNEL");
+        v = (e && std::strcmp(e, "tma") == 0) ? 1 : 0;
+    }
+    return v;
+}
+
 cudaError_t launch_ell(const EllArgs& a, cudaStream_t s) {
     if (a.n_rows <= 0) return cudaSuccess;
+    if (ell_variant() == 1) {
+        cudaError_t e = launch_ell_tma(a, s, num_sms());
+        if (e != cudaErrorNotSupported) return e;
+        cudaGetLastError();  // clear the sticky-free "not supported" status
+    }
     const bool halo = a.x_halo != nullptr;
     const bool rowmap = a.rowmap != nullptr;
     if (halo) return rowmap ? launch_ell_t<true, true>(a, s) : launch_ell_t<true, false>(a, s);
     return rowmap ? launch_ell_t<false, true>(a, s) : launch_ell_t<false, false>(a, s);
 }
 
-template <bool HALO>
-static cudaError_t launch_tail_t(const TailArgs& a, cudaStream_t s) {
-    const int threads = 256;
-    const int64_t groups_per_block = threads / a.group;
-    int64_t blocks = (a.n_tail + groups_per_block - 1) / groups_per_block;
-    const int64_t cap = (int64_t)num_sms() * 8 * 16;
-    if (blocks > cap) blocks = cap;
-    if (blocks < 1) blocks = 1;
-    const dim3 g((unsigned)blocks), b(threads);
-    switch (a.group) {
-        case 2: tail_kernel<2, HALO><<<g, b, 0, s>>>(a); break;
-        case 4: tail_kernel<4, HALO><<<g, b, 0, s>>>(a); break;
-        case 8: tail_kernel<8, HALO><<<g, b, 0, s>>>(a); break;
-        case 16: tail_kernel<16, HALO><<<g, b, 0, s>>>(a); break;
-        default: tail_kernel<32, HALO><<<g, b, 0, s>>>(a); break;
+cudaError_t launch_tail(const TailArgs& a0, cudaStream_t s) {
+    if (a0.n_tail <= 0) return cudaSuccess;
+    TailArgs a = a0;
+    a.blk_off[0] = 0;
+    for (int b = 0; b < kTailBins; ++b) {
+        const int64_t rows = a.bin_off[b + 1] - a.bin_off[b];
+        const int64_t per_block = 256 >> b;
+        a.blk_off[b + 1] = a.blk_off[b] + (rows + per_block - 1) / per_block;
     }
+    const int64_t blocks = a.blk_off[kTailBins];
+    if (blocks <= 0) return cudaSuccess;
+    if (blocks > 0x7fffffff) return cudaErrorInvalidValue;
+    if (a.x_halo) tail_kernel<true><<<(unsigned)blocks, 256, 0, s>>>(a);
+    else tail_kernel<false><<<(unsigned)blocks, 256, 0, s>>>(a);
     return cudaGetLastError();
-}
-
-cudaError_t launch_tail(const TailArgs& a, cudaStream_t s) {
-    if (a.n_tail <= 0) return cudaSuccess;
-    return a.x_halo ? launch_tail_t<true>(a, s) : launch_tail_t<false>(a, s);
 }
 
 cudaError_t launch_pack(const int32_t* idx, int32_t n, const double* x, double* out,
