@@ -4,6 +4,7 @@
 // hec_spmv is Alg. 1 of PAPER.md: the ELL part "is performed
 // firstly" by ell_kernel, then the CSR part by tail_kernel, both on the
 // caller's stream (stream order gives the ELL -> CSR ordering).
+#include <algorithm>
 #include <cstring>
 #include <memory>
 
@@ -27,10 +28,15 @@ static void release(hec_matrix_s* m) {
         int cur = 0;
         cudaGetDevice(&cur);
         cudaSetDevice(m->device);
-        void* ptrs[] = {m->d_ell_col, m->d_ell_val, m->d_tail_out, m->d_tail_order, m->d_tail_ptr, m->d_tail_col,
-                        m->d_tail_val, m->d_rowmap, m->d_stage_x, m->d_stage_y};
+        void* ptrs[] = {m->d_ell_col, m->d_ell_val, m->d_tail_out, m->d_warp_row, m->d_tail_ptr,
+                        m->d_tail_col, m->d_tail_val, m->d_rowmap, m->d_stage_x, m->d_stage_y};
         for (void* p : ptrs)
             if (p) cudaFree(p);
+        for (cudaEvent_t e : m->ev_x) cudaEventDestroy(e);
+        for (cudaEvent_t e : m->ev_y) cudaEventDestroy(e);
+        if (m->ev_start) cudaEventDestroy(m->ev_start);
+        if (m->s_h2d) cudaStreamDestroy(m->s_h2d);
+        if (m->s_d2h) cudaStreamDestroy(m->s_d2h);
         cudaSetDevice(cur);
     }
     delete m;
@@ -47,6 +53,65 @@ struct DeviceGuard {
     }
 };
 
+// Row chunks (for hec_spmv_host; one chunk for sub-matrices and small
+// matrices), the x prefix each chunk reads, and the tail work partition:
+// within each chunk the spilled entries are cut into warp units of
+// kTailWarpEntries; a unit owns the tail rows whose first spilled entry falls
+// inside it (so no row is split between warps and every row's sum is formed
+// in one place, deterministically).  warp_row[w] = first tail row of unit w;
+// unit w handles tail rows [warp_row[w], warp_row[w+1]).
+static void plan_chunks(hec_matrix_s* m, const HostHec& h, bool pipelined, std::vector<int32_t>* warp_row) {
+    const int32_t n = h.n_rows;
+    int32_t K = pipelined ? n / (1 << 20) : 1;
+    K = K < 1 ? 1 : (K > 16 ? 16 : K);
+    int64_t per = ((int64_t)n + K - 1) / K;
+    per = (per + 511) / 512 * 512;
+    m->chunk_row.assign(1, 0);
+    while (m->chunk_row.back() < n)
+        m->chunk_row.push_back((int32_t)std::min<int64_t>(n, m->chunk_row.back() + per));
+    if (m->chunk_row.size() == 1) m->chunk_row.push_back(0);  // n == 0: one empty chunk
+    m->n_chunks = (int32_t)m->chunk_row.size() - 1;
+    const int C = m->n_chunks;
+    // x prefix per chunk (pipelined host path only)
+    m->chunk_xend.assign(C, h.n_cols);
+    if (pipelined && C > 1) {
+        std::vector<int32_t> cmax(C, -1);
+        for (int c = 0; c < C; ++c)
+            for (int32_t j = 0; j < h.width; ++j) {
+                const int32_t* colj = h.ell_col.data() + (size_t)j * h.stride;
+                for (int32_t i = m->chunk_row[c]; i < m->chunk_row[c + 1]; ++i) cmax[c] = std::max(cmax[c], colj[i]);
+            }
+        int c = 0;
+        for (size_t t = 0; t < h.tail_rows.size(); ++t) {
+            while (h.tail_rows[t] >= m->chunk_row[c + 1]) ++c;
+            for (int32_t k = h.tail_ptr[t]; k < h.tail_ptr[t + 1]; ++k) cmax[c] = std::max(cmax[c], h.tail_col[k]);
+        }
+        int32_t run = -1;
+        for (int q = 0; q < C; ++q) {
+            run = std::max(run, cmax[q]);
+            m->chunk_xend[q] = run + 1;
+        }
+    }
+    // tail rows of each chunk (contiguous, tail rows are ascending) and warp units
+    const int32_t tr = (int32_t)h.tail_rows.size();
+    const int32_t* tp = h.tail_ptr.data();
+    m->chunk_warp.assign(C + 1, 0);
+    warp_row->clear();
+    int32_t t0 = 0;
+    for (int c = 0; c < C; ++c) {
+        int32_t t1 = t0;
+        while (t1 < tr && h.tail_rows[t1] < m->chunk_row[c + 1]) ++t1;
+        const int64_t k0 = tr ? tp[t0] : 0, k1 = tr ? tp[t1] : 0;
+        for (int64_t kb = k0; kb < k1; kb += kTailWarpEntries) {
+            const int32_t* r = std::lower_bound(tp + t0, tp + t1, (int32_t)kb);  // first row starting >= kb
+            warp_row->push_back((int32_t)(r - tp));
+        }
+        m->chunk_warp[c + 1] = (int64_t)warp_row->size();
+        t0 = t1;
+    }
+    warp_row->push_back(tr);
+}
+
 hec_status make_matrix(HostHec&& h, int32_t device, cudaStream_t s, const int32_t* rowmap,
                        int32_t n_rowmap, int32_t row_off, int32_t n_loc, hec_matrix* out) {
     std::unique_ptr<hec_matrix_s, void (*)(hec_matrix_s*)> m(new (std::nothrow) hec_matrix_s(),
@@ -61,21 +126,6 @@ hec_status make_matrix(HostHec&& h, int32_t device, cudaStream_t s, const int32_
     m->ell_nnz = h.ell_nnz;
     m->tail_rows = (int32_t)h.tail_rows.size();
     m->tail_nnz = (int64_t)h.tail_col.size();
-    // bin the tail rows by spilled length (tail kernel lanes per row)
-    std::vector<int32_t> order(h.tail_rows.size());
-    {
-        int64_t cnt[kTailBins] = {0};
-        for (size_t t = 0; t < order.size(); ++t) cnt[tail_bin_of(h.tail_ptr[t + 1] - h.tail_ptr[t])]++;
-        m->tail_bin_off[0] = 0;
-        for (int b = 0; b < kTailBins; ++b) m->tail_bin_off[b + 1] = m->tail_bin_off[b] + cnt[b];
-        int64_t pos[kTailBins];
-        for (int b = 0; b < kTailBins; ++b) pos[b] = m->tail_bin_off[b];
-        for (size_t t = 0; t < order.size(); ++t)
-            order[pos[tail_bin_of(h.tail_ptr[t + 1] - h.tail_ptr[t])]++] = (int32_t)t;
-        int best = 0;
-        for (int b = 1; b < kTailBins; ++b) if (cnt[b] > cnt[best]) best = b;
-        m->tail_group = 1 << best;
-    }
     m->h_tail_rows = h.tail_rows;
     m->row_off = row_off;
     m->n_loc = n_loc;
@@ -89,48 +139,59 @@ hec_status make_matrix(HostHec&& h, int32_t device, cudaStream_t s, const int32_
         return fail(HEC_ERR_NODEV, "no CUDA device available");
     if (device >= n_dev) return fail(HEC_ERR_ARG, "device ordinal out of range");
     DeviceGuard g(device);
+    std::vector<int32_t> warp_row;
+    plan_chunks(m.get(), h, n_loc < 0 && !rowmap, &warp_row);
     int64_t bytes = 0;
     hec_status st;
     if ((st = dmalloc_copy(&m->d_ell_col, h.ell_col.data(), h.ell_col.size(), s, &bytes))) return st;
     if ((st = dmalloc_copy(&m->d_ell_val, h.ell_val.data(), h.ell_val.size(), s, &bytes))) return st;
-    std::vector<int32_t> tail_out(h.tail_rows.size());
-    for (size_t t = 0; t < tail_out.size(); ++t)
-        tail_out[t] = rowmap ? rowmap[h.tail_rows[t]] : row_off + h.tail_rows[t];
-    if ((st = dmalloc_copy(&m->d_tail_out, tail_out.data(), tail_out.size(), s, &bytes))) return st;
-    if ((st = dmalloc_copy(&m->d_tail_order, order.data(), order.size(), s, &bytes))) return st;
-    if (!h.tail_rows.empty())
+    if (!h.tail_rows.empty()) {
+        std::vector<int32_t> tail_out(h.tail_rows.size());
+        for (size_t t = 0; t < tail_out.size(); ++t)
+            tail_out[t] = rowmap ? rowmap[h.tail_rows[t]] : row_off + h.tail_rows[t];
+        if ((st = dmalloc_copy(&m->d_tail_out, tail_out.data(), tail_out.size(), s, &bytes))) return st;
+        if ((st = dmalloc_copy(&m->d_warp_row, warp_row.data(), warp_row.size(), s, &bytes))) return st;
         if ((st = dmalloc_copy(&m->d_tail_ptr, h.tail_ptr.data(), h.tail_ptr.size(), s, &bytes))) return st;
-    if ((st = dmalloc_copy(&m->d_tail_col, h.tail_col.data(), h.tail_col.size(), s, &bytes))) return st;
-    if ((st = dmalloc_copy(&m->d_tail_val, h.tail_val.data(), h.tail_val.size(), s, &bytes))) return st;
+        if ((st = dmalloc_copy(&m->d_tail_col, h.tail_col.data(), h.tail_col.size(), s, &bytes))) return st;
+        if ((st = dmalloc_copy(&m->d_tail_val, h.tail_val.data(), h.tail_val.size(), s, &bytes))) return st;
+        HEC_CUDA_TRY(cudaStreamSynchronize(s));  // host vectors die after return
+    }
     if (rowmap)
         if ((st = dmalloc_copy(&m->d_rowmap, rowmap, (size_t)n_rowmap, s, &bytes))) return st;
-    HEC_CUDA_TRY(cudaStreamSynchronize(s));  // host vectors die after return
+    HEC_CUDA_TRY(cudaStreamSynchronize(s));
     m->device_bytes = bytes;
     *out = m.release();
     return HEC_OK;
 }
 
-hec_status launch_spmv(const hec_matrix_s* A, const double* x, const double* x_halo, double* y,
-                       cudaStream_t s) {
+// Chunk c of the handle (rows [chunk_row[c], chunk_row[c+1]), r0 a multiple
+// of 512), or all chunks when c < 0: ELL kernel then tail kernel.
+static hec_status launch_chunks(const hec_matrix_s* A, int c, const double* x, const double* x_halo,
+                                double* y, cudaStream_t s) {
+    const int32_t r0 = c < 0 ? 0 : A->chunk_row[c];
+    const int32_t r1 = c < 0 ? A->n_rows : A->chunk_row[c + 1];
     EllArgs e;
-    e.col = A->d_ell_col;
-    e.val = A->d_ell_val;
+    e.col = A->d_ell_col ? A->d_ell_col + r0 : nullptr;
+    e.val = A->d_ell_val ? A->d_ell_val + r0 : nullptr;
     e.stride = A->stride;
-    e.n_rows = A->n_rows;
+    e.avail = (int64_t)A->stride - r0;
+    e.n_rows = r1 - r0;
     e.width = A->width;
     e.x = x;
     e.x_halo = x_halo;
     e.n_loc = A->n_loc >= 0 ? A->n_loc : A->n_cols;
-    e.y = y;
-    e.rowmap = A->d_rowmap;
+    e.y = A->d_rowmap ? y : y + r0;
+    e.rowmap = A->d_rowmap ? A->d_rowmap + r0 : nullptr;
     e.row_off = A->row_off;
     cudaError_t err = launch_ell(e, s);  // Alg. 1 lines 1-3: ELL first
     if (err != cudaSuccess) return cuda_fail(err, "ell_kernel launch");
-    if (A->tail_rows > 0) {              // Alg. 1 lines 5-7: then the CSR part
+    const int64_t w0 = c < 0 ? 0 : A->chunk_warp[c];
+    const int64_t w1 = c < 0 ? A->chunk_warp[A->n_chunks] : A->chunk_warp[c + 1];
+    if (A->tail_rows > 0 && w1 > w0) {  // Alg. 1 lines 5-7: then the CSR part
         TailArgs t;
-        t.n_tail = A->tail_rows;
-        t.order = A->d_tail_order;
-        for (int b = 0; b <= kTailBins; ++b) t.bin_off[b] = A->tail_bin_off[b];
+        t.warp_row = A->d_warp_row;
+        t.warp_begin = w0;
+        t.warp_end = w1;
         t.out_rows = A->d_tail_out;
         t.ptr = A->d_tail_ptr;
         t.col = A->d_tail_col;
@@ -143,6 +204,11 @@ hec_status launch_spmv(const hec_matrix_s* A, const double* x, const double* x_h
         if (err != cudaSuccess) return cuda_fail(err, "tail_kernel launch");
     }
     return HEC_OK;
+}
+
+hec_status launch_spmv(const hec_matrix_s* A, const double* x, const double* x_halo, double* y,
+                       cudaStream_t s) {
+    return launch_chunks(A, -1, x, x_halo, y, s);
 }
 
 }  // namespace hec
@@ -180,7 +246,7 @@ hec_status hec_info(hec_matrix A, hec_matrix_info* o) {
     o->nnz = A->nnz;
     o->ell_nnz = A->ell_nnz;
     o->tail_rows = A->tail_rows;
-    o->tail_group = A->tail_group;
+    o->tail_group = 32;
     o->tail_nnz = A->tail_nnz;
     o->device_bytes = A->device_bytes;
     o->device = A->device;
@@ -255,13 +321,68 @@ hec_status hec_spmv_host(hec_matrix A, const double* x_host, double* y_host, voi
         HEC_CUDA_TRY(cudaMalloc(&A->d_stage_y, sizeof(double) * (size_t)A->n_rows));
         A->device_bytes += sizeof(double) * (int64_t)A->n_rows;
     }
-    if (A->n_cols > 0)
-        HEC_CUDA_TRY(cudaMemcpyAsync(A->d_stage_x, x_host, sizeof(double) * (size_t)A->n_cols,
-                                     cudaMemcpyHostToDevice, s));
-    hec_status st = launch_spmv(A, A->d_stage_x, nullptr, A->d_stage_y, s);
-    if (st != HEC_OK) return st;
-    HEC_CUDA_TRY(cudaMemcpyAsync(y_host, A->d_stage_y, sizeof(double) * (size_t)A->n_rows,
-                                 cudaMemcpyDeviceToHost, s));
+    const int K = A->n_chunks;
+    if (K <= 1) {  // small matrix: copy, compute, copy back
+        if (A->n_cols > 0)
+            HEC_CUDA_TRY(cudaMemcpyAsync(A->d_stage_x, x_host, sizeof(double) * (size_t)A->n_cols,
+                                         cudaMemcpyHostToDevice, s));
+        hec_status st = launch_spmv(A, A->d_stage_x, nullptr, A->d_stage_y, s);
+        if (st != HEC_OK) return st;
+        HEC_CUDA_TRY(cudaMemcpyAsync(y_host, A->d_stage_y, sizeof(double) * (size_t)A->n_rows,
+                                     cudaMemcpyDeviceToHost, s));
+        HEC_CUDA_TRY(cudaStreamSynchronize(s));
+        return HEC_OK;
+    }
+    // Pipelined: x arrives in K pieces on s_h2d; row chunk c computes on s as
+    // soon as the x prefix it reads (chunk_xend[c]) is resident; its y slice
+    // goes back on s_d2h while later chunks compute (PCIe is full duplex).
+    // The chunks' ELL rows and tail warp units are exactly those of a whole
+    // hec_spmv, so the result is bitwise identical.
+    if (!A->s_h2d) {
+        HEC_CUDA_TRY(cudaStreamCreateWithFlags(&A->s_h2d, cudaStreamNonBlocking));
+        HEC_CUDA_TRY(cudaStreamCreateWithFlags(&A->s_d2h, cudaStreamNonBlocking));
+        HEC_CUDA_TRY(cudaEventCreateWithFlags(&A->ev_start, cudaEventDisableTiming));
+        A->ev_x.resize(K, nullptr);
+        A->ev_y.resize(K, nullptr);
+        for (int c = 0; c < K; ++c) {
+            HEC_CUDA_TRY(cudaEventCreateWithFlags(&A->ev_x[c], cudaEventDisableTiming));
+            HEC_CUDA_TRY(cudaEventCreateWithFlags(&A->ev_y[c], cudaEventDisableTiming));
+        }
+    }
+    std::vector<int64_t> xb(K + 1);
+    for (int p = 0; p <= K; ++p) {
+        int64_t b = ((int64_t)p * A->n_cols / K + 511) / 512 * 512;
+        xb[p] = std::min<int64_t>(b, A->n_cols);
+    }
+    xb[K] = A->n_cols;
+    HEC_CUDA_TRY(cudaEventRecord(A->ev_start, s));  // ordered after prior work on s
+    HEC_CUDA_TRY(cudaStreamWaitEvent(A->s_h2d, A->ev_start, 0));
+    HEC_CUDA_TRY(cudaStreamWaitEvent(A->s_d2h, A->ev_start, 0));
+    for (int p = 0; p < K; ++p) {
+        if (xb[p + 1] > xb[p])
+            HEC_CUDA_TRY(cudaMemcpyAsync(A->d_stage_x + xb[p], x_host + xb[p], sizeof(double) * (xb[p + 1] - xb[p]),
+                                         cudaMemcpyHostToDevice, A->s_h2d));
+        HEC_CUDA_TRY(cudaEventRecord(A->ev_x[p], A->s_h2d));
+    }
+    int waited = -1;
+    for (int c = 0; c < K; ++c) {
+        int need = 0;  // last x piece overlapping [0, chunk_xend[c])
+        while (need < K - 1 && xb[need + 1] < A->chunk_xend[c]) ++need;
+        if (need > waited) {
+            HEC_CUDA_TRY(cudaStreamWaitEvent(s, A->ev_x[need], 0));
+            waited = need;
+        }
+        hec_status st = launch_chunks(A, c, A->d_stage_x, nullptr, A->d_stage_y, s);
+        if (st != HEC_OK) return st;
+        HEC_CUDA_TRY(cudaEventRecord(A->ev_y[c], s));
+        HEC_CUDA_TRY(cudaStreamWaitEvent(A->s_d2h, A->ev_y[c], 0));
+        const int32_t r0 = A->chunk_row[c], r1 = A->chunk_row[c + 1];
+        HEC_CUDA_TRY(cudaMemcpyAsync(y_host + r0, A->d_stage_y + r0, sizeof(double) * (size_t)(r1 - r0),
+                                     cudaMemcpyDeviceToHost, A->s_d2h));
+    }
+    if (waited < K - 1) HEC_CUDA_TRY(cudaStreamWaitEvent(s, A->ev_x[K - 1], 0));  // x buffer reuse order
+    HEC_CUDA_TRY(cudaEventRecord(A->ev_start, A->s_d2h));
+    HEC_CUDA_TRY(cudaStreamWaitEvent(s, A->ev_start, 0));
     HEC_CUDA_TRY(cudaStreamSynchronize(s));
     return HEC_OK;
 }

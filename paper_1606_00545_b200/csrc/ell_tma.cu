@@ -104,7 +104,7 @@ __global__ void __launch_bounds__(kThreads, 1) ell_tma_kernel(EllArgs a, int sta
                 const int round = k / stages;
                 if (round > 0) mbar_wait(&empty[st], (round - 1) & 1);
                 const int64_t r0 = tile * kRows;
-                const int64_t rows = (s - r0) < kRows ? (s - r0) : kRows;  // within the stride
+                const int64_t rows = (a.avail - r0) < kRows ? (a.avail - r0) : kRows;  // within the stride
                 const uint32_t cb = (uint32_t)(rows * 4), vb = (uint32_t)(rows * 8);
                 mbar_arrive_expect_tx(&full[st], (uint32_t)W * (cb + vb));
 #pragma unroll

@@ -62,15 +62,8 @@ hec_status check_opts(const hec_opts& o);
 int32_t choose_width(const CsrView& A, const hec_opts& o);
 // CSR -> HEC fill with a given width (readings A2-A4, A15).
 hec_status convert(const CsrView& A, int32_t width, int32_t stride_unit, HostHec* out);
-// Tail rows are binned by spilled length L: bin b uses G = 2^b lanes per row,
-// G = smallest power of two >= ceil(L/2), capped at 32 (a tuning choice, not
-// part of the format).  bin_of(L) is shared by the planner and the launcher.
-constexpr int kTailBins = 6;
-inline int tail_bin_of(int32_t L) {
-    int b = 0;
-    while (b < kTailBins - 1 && (1 << b) * 2 < L) ++b;
-    return b;
-}
+// CSR-tail work unit: spilled entries per warp (see plan_chunks in api.cpp).
+constexpr int kTailWarpEntries = 256;
 
 // ------------------------------------------------------------------ plans --
 struct PartPlan {
@@ -107,15 +100,14 @@ struct hec_matrix_s {
     int32_t device = -1;
     int32_t n_rows = 0, n_cols = 0, width = 0, stride = 0;
     int64_t nnz = 0, ell_nnz = 0, tail_nnz = 0;
-    int32_t tail_rows = 0, tail_group = 32;
+    int32_t tail_rows = 0;
     hec::HostHec host;                 // full copy only for host-only handles
     std::vector<int32_t> h_tail_rows;  // local tail row ids (always kept; small)
     // device arrays
     int32_t* d_ell_col = nullptr;
     double* d_ell_val = nullptr;
     int32_t* d_tail_out = nullptr;     // output row of each tail row (after row map)
-    int32_t* d_tail_order = nullptr;   // tail row ids grouped by length bin
-    int64_t tail_bin_off[hec::kTailBins + 1] = {0};
+    int32_t* d_warp_row = nullptr;     // first tail row of each warp unit (+ terminal)
     int32_t* d_tail_ptr = nullptr;
     int32_t* d_tail_col = nullptr;
     double* d_tail_val = nullptr;
@@ -124,6 +116,16 @@ struct hec_matrix_s {
     int32_t n_loc = -1;                // >= 0: columns >= n_loc read x_halo[c - n_loc]
     double* d_stage_x = nullptr;       // hec_spmv_host staging
     double* d_stage_y = nullptr;
+    // hec_spmv_host pipeline: row chunks whose ELL+tail run as soon as the x
+    // prefix they read has arrived, and whose y goes back while later chunks
+    // compute (H2D, compute and D2H overlap; PCIe is full duplex).
+    int32_t n_chunks = 1;
+    std::vector<int32_t> chunk_row;    // [n_chunks+1], multiples of 512
+    std::vector<int32_t> chunk_xend;   // [n_chunks]: x[0 : xend) needed by rows < chunk_row[c+1]
+    std::vector<int64_t> chunk_warp;   // [n_chunks+1]: tail warp units of each chunk
+    cudaStream_t s_h2d = nullptr, s_d2h = nullptr;
+    std::vector<cudaEvent_t> ev_x, ev_y;
+    cudaEvent_t ev_start = nullptr;
     int64_t device_bytes = 0;
 };
 
@@ -142,6 +144,7 @@ struct EllArgs {
     const int32_t* col;
     const double* val;
     int64_t stride;
+    int64_t avail;     // slot-column entries readable from `col`/`val` (stride - row offset)
     int32_t n_rows;
     int32_t width;
     const double* x;
@@ -152,10 +155,8 @@ struct EllArgs {
     int32_t row_off;
 };
 struct TailArgs {
-    int32_t n_tail;
-    const int32_t* order;                 // tail rows grouped by bin
-    int64_t bin_off[kTailBins + 1];       // bin b = order[bin_off[b] : bin_off[b+1]]
-    int64_t blk_off[kTailBins + 1];       // first block of bin b (filled by launch_tail)
+    const int32_t* warp_row;    // unit w owns tail rows [warp_row[w], warp_row[w+1])
+    int64_t warp_begin, warp_end;
     const int32_t* out_rows;
     const int32_t* ptr;
     const int32_t* col;

@@ -160,33 +160,67 @@ __global__ void __launch_bounds__(256) ell_kernel(EllArgs a) {
 }
 
 // ------------------------------------------------------------ tail kernel --
-// Tail rows are grouped by spilled length (bin b: G = 2^b lanes per row, each
-// lane handling about two entries); every block belongs to one bin, so G is
-// block-uniform and the xor-shuffle tree runs on whole G-lane groups.
+// One warp per work unit: the tail rows whose first spilled entry falls in a
+// 256-entry slice of the tail (plan_chunks, api.cpp), processed in row order
+// as a contiguous entry range [ptr[rb], ptr[re]).  Each 32-entry window is
+// loaded coalesced, every lane finds its row by a 5-step shuffle search over
+// the ends of the next 32 rows, a segmented inclusive scan (__shfl_up_sync)
+// sums each row's products inside the window, a carry joins rows that cross
+// windows, and the lane holding a row's last entry adds the row sum into y
+// (after the ELL kernel).  Every lane does useful work whatever the row
+// lengths; the order of additions is fixed, so results are deterministic.
 template <bool HALO>
 __global__ void __launch_bounds__(256) tail_kernel(TailArgs a) {
     const uint64_t pol = policy_evict_first();
-    const int64_t blk = blockIdx.x;
-    int b = 0;
-    while (b < kTailBins - 1 && blk >= a.blk_off[b + 1]) ++b;
-    const int G = 1 << b;
-    const int lane = threadIdx.x & (G - 1);
-    const int64_t gi = a.bin_off[b] + (blk - a.blk_off[b]) * (256 >> b) + (threadIdx.x >> b);
-    double acc = 0.0;
-    int32_t row = -1;
-    if (gi < a.bin_off[b + 1]) {
-        const int32_t t = __ldg(a.order + gi);
-        const int32_t kb = __ldg(a.ptr + t), ke = __ldg(a.ptr + t + 1);
-#pragma unroll 4
-        for (int32_t k = kb + lane; k < ke; k += G) {
+    const unsigned FULL = 0xffffffffu;
+    const int lane = threadIdx.x & 31;
+    const int64_t w = a.warp_begin + (int64_t)blockIdx.x * 8 + (threadIdx.x >> 5);
+    if (w >= a.warp_end) return;  // warp-uniform
+    const int32_t rb = __ldg(a.warp_row + w), re = __ldg(a.warp_row + w + 1);
+    if (rb >= re) return;
+    const int32_t ke = __ldg(a.ptr + re);
+    int32_t rw = rb;      // row of the window's first entry
+    double carry = 0.0;   // partial sum of row rw from earlier windows
+    for (int32_t k0 = __ldg(a.ptr + rb); k0 < ke; k0 += 32) {
+        const int32_t k = k0 + lane;
+        const bool valid = k < ke;
+        double p = 0.0;
+        if (valid) {
             const int32_t c = ld_stream_i1(a.col + k, pol);
             const double v = ld_stream_d1(a.val + k, pol);
-            acc = fma(v, gather_x<HALO>(a.x, a.x_halo, a.n_loc, c), acc);
+            p = v * gather_x<HALO>(a.x, a.x_halo, a.n_loc, c);
         }
-        row = __ldg(a.out_rows + t);
+        // end (one past the last entry) of row rw + lane; rows past re end at ke
+        const int32_t rl = rw + 1 + lane;
+        const int32_t end_l = rl <= re ? __ldg(a.ptr + rl) : ke;
+        // lo = #{j : end_j <= k}: the window holds <= 32 rows, so lo <= 31
+        int lo = 0;
+#pragma unroll
+        for (int step = 16; step > 0; step >>= 1) {
+            const int32_t e = __shfl_sync(FULL, end_l, lo + step - 1);
+            if (e <= k) lo += step;
+        }
+        const int32_t my_end = __shfl_sync(FULL, end_l, lo);
+        const int32_t row = valid ? rw + lo : 0x7fffffff;
+        double sum = (lane == 0) ? p + carry : p;  // entry k0 always belongs to row rw
+#pragma unroll
+        for (int d = 1; d < 32; d <<= 1) {
+            const double su = __shfl_up_sync(FULL, sum, d);
+            const int32_t ru = __shfl_up_sync(FULL, row, d);
+            if (lane >= d && ru == row) sum += su;
+        }
+        if (valid && k + 1 == my_end) {  // last entry of its row: the row is complete
+            double* yp = a.y + __ldg(a.out_rows + row);
+            *yp += sum;
+        }
+        const double s31 = __shfl_sync(FULL, sum, 31);
+        const int32_t row31 = __shfl_sync(FULL, row, 31);
+        const int32_t end31 = __shfl_sync(FULL, my_end, 31);
+        if (k0 + 32 < ke) {  // next window exists (lane 31 was valid)
+            if (k0 + 32 < end31) { carry = s31; rw = row31; }
+            else { carry = 0.0; rw = row31 + 1; }
+        }
     }
-    for (int off = G >> 1; off > 0; off >>= 1) acc += __shfl_xor_sync(0xffffffffu, acc, off, G);
-    if (lane == 0 && row >= 0) a.y[row] += acc;
 }
 
 // ------------------------------------------------------------ pack kernel --
@@ -254,17 +288,10 @@ cudaError_t launch_ell(const EllArgs& a, cudaStream_t s) {
     return rowmap ? launch_ell_t<false, true>(a, s) : launch_ell_t<false, false>(a, s);
 }
 
-cudaError_t launch_tail(const TailArgs& a0, cudaStream_t s) {
-    if (a0.n_tail <= 0) return cudaSuccess;
-    TailArgs a = a0;
-    a.blk_off[0] = 0;
-    for (int b = 0; b < kTailBins; ++b) {
-        const int64_t rows = a.bin_off[b + 1] - a.bin_off[b];
-        const int64_t per_block = 256 >> b;
-        a.blk_off[b + 1] = a.blk_off[b] + (rows + per_block - 1) / per_block;
-    }
-    const int64_t blocks = a.blk_off[kTailBins];
-    if (blocks <= 0) return cudaSuccess;
+cudaError_t launch_tail(const TailArgs& a, cudaStream_t s) {
+    const int64_t warps = a.warp_end - a.warp_begin;
+    if (warps <= 0) return cudaSuccess;
+    const int64_t blocks = (warps + 7) / 8;
     if (blocks > 0x7fffffff) return cudaErrorInvalidValue;
     if (a.x_halo) tail_kernel<true><<<(unsigned)blocks, 256, 0, s>>>(a);
     else tail_kernel<false><<<(unsigned)blocks, 256, 0, s>>>(a);

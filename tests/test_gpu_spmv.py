@@ -180,6 +180,25 @@ def test_spmv_host_matches_device():
     assert yn.tobytes() == yd.tobytes()
 
 
+@pytest.mark.parametrize("maker", [lambda: hecgen.poisson3d(128, 128, 160),
+                                   lambda: hecgen.powerlaw(3 << 20, seed=6),
+                                   lambda: hecgen.random_csr(2_200_000, 40, 0.1, seed=2)])
+def test_spmv_host_pipelined_chunks_bitwise(maker):
+    # >= 2M rows: hec_spmv_host splits rows into chunks that start as soon as
+    # their x prefix has arrived; the result must equal hec_spmv bit for bit.
+    A = maker()
+    x = hecgen.vector(A.n_cols, "uniform", seed=4)
+    M = hec.from_csr(A)
+    yd, _ = gpu_spmv(A, x, M=M)
+    xp = torch.from_numpy(x).pin_memory()
+    yp = torch.full((A.n_rows,), float("nan"), dtype=torch.float64).pin_memory()
+    for _ in range(2):                       # reuse of the staging buffers and events
+        M.spmv_host(xp, yp)
+        assert yp.numpy().tobytes() == yd.tobytes()
+    r0 = A.n_rows // 2
+    assert_parity(A, x, yp.numpy()[r0:r0 + 3000], r0, r0 + 3000)
+
+
 def test_export_from_device_matches_host_handle():
     A = hecgen.powerlaw(3000, seed=12)
     Md = hec.from_csr(A)
