@@ -95,6 +95,10 @@ static void plan_chunks(hec_matrix_s* m, const HostHec& h, bool pipelined, std::
     // tail rows of each chunk (contiguous, tail rows are ascending) and warp units
     const int32_t tr = (int32_t)h.tail_rows.size();
     const int32_t* tp = h.tail_ptr.data();
+    // unit size: 256 entries, smaller (down to one 32-entry window) when the
+    // tail is too small to give every SM warp a unit
+    int64_t E = (int64_t)h.tail_col.size() / (148 * 32);
+    E = E >= kTailWarpEntries ? kTailWarpEntries : (E < 32 ? 32 : E / 32 * 32);
     m->chunk_warp.assign(C + 1, 0);
     warp_row->clear();
     int32_t t0 = 0;
@@ -102,7 +106,7 @@ static void plan_chunks(hec_matrix_s* m, const HostHec& h, bool pipelined, std::
         int32_t t1 = t0;
         while (t1 < tr && h.tail_rows[t1] < m->chunk_row[c + 1]) ++t1;
         const int64_t k0 = tr ? tp[t0] : 0, k1 = tr ? tp[t1] : 0;
-        for (int64_t kb = k0; kb < k1; kb += kTailWarpEntries) {
+        for (int64_t kb = k0; kb < k1; kb += E) {
             const int32_t* r = std::lower_bound(tp + t0, tp + t1, (int32_t)kb);  // first row starting >= kb
             warp_row->push_back((int32_t)(r - tp));
         }

@@ -62,7 +62,8 @@ hec_status check_opts(const hec_opts& o);
 int32_t choose_width(const CsrView& A, const hec_opts& o);
 // CSR -> HEC fill with a given width (readings A2-A4, A15).
 hec_status convert(const CsrView& A, int32_t width, int32_t stride_unit, HostHec* out);
-// CSR-tail work unit: spilled entries per warp (see plan_chunks in api.cpp).
+// CSR-tail work unit: at most this many spilled entries start rows owned by
+// one warp (see plan_chunks in api.cpp), so a unit owns <= 256 rows.
 constexpr int kTailWarpEntries = 256;
 
 // ------------------------------------------------------------------ plans --

@@ -161,64 +161,84 @@ __global__ void __launch_bounds__(256) ell_kernel(EllArgs a) {
 
 // ------------------------------------------------------------ tail kernel --
 // One warp per work unit: the tail rows whose first spilled entry falls in a
-// 256-entry slice of the tail (plan_chunks, api.cpp), processed in row order
-// as a contiguous entry range [ptr[rb], ptr[re]).  Each 32-entry window is
-// loaded coalesced, every lane finds its row by a 5-step shuffle search over
-// the ends of the next 32 rows, a segmented inclusive scan (__shfl_up_sync)
-// sums each row's products inside the window, a carry joins rows that cross
-// windows, and the lane holding a row's last entry adds the row sum into y
-// (after the ELL kernel).  Every lane does useful work whatever the row
-// lengths; the order of additions is fixed, so results are deterministic.
+// slice of <= 256 entries (plan_chunks, api.cpp), processed in row order as
+// the contiguous entry range [ptr[rb], ptr[re]).  The unit's <= 257 row
+// pointers are staged in shared memory once; entries are handled in batches
+// of 8 windows of 32: all 16 coalesced col/val loads of a batch, then its 8 x
+// gathers, are in flight before any is used.  Per window, every lane finds
+// its row by a 5-step shuffle search over the ends of the next 32 rows, a
+// segmented inclusive scan (__shfl_up_sync) sums each row's products, a carry
+// joins rows that cross windows, and the lane holding a row's last entry adds
+// the row sum into y (after the ELL kernel).  All lanes do useful work
+// whatever the row lengths; the order of additions is fixed (deterministic).
+constexpr int kTailBatch = 8;
+
 template <bool HALO>
 __global__ void __launch_bounds__(256) tail_kernel(TailArgs a) {
+    __shared__ int32_t s_ptr[8][kTailWarpEntries + 1];
     const uint64_t pol = policy_evict_first();
     const unsigned FULL = 0xffffffffu;
-    const int lane = threadIdx.x & 31;
-    const int64_t w = a.warp_begin + (int64_t)blockIdx.x * 8 + (threadIdx.x >> 5);
+    const int lane = threadIdx.x & 31, wib = threadIdx.x >> 5;
+    const int64_t w = a.warp_begin + (int64_t)blockIdx.x * 8 + wib;
     if (w >= a.warp_end) return;  // warp-uniform
     const int32_t rb = __ldg(a.warp_row + w), re = __ldg(a.warp_row + w + 1);
     if (rb >= re) return;
-    const int32_t ke = __ldg(a.ptr + re);
-    int32_t rw = rb;      // row of the window's first entry
+    const int32_t R = re - rb;  // <= 256 rows
+    int32_t* sp = s_ptr[wib];
+    for (int32_t i = lane; i <= R; i += 32) sp[i] = __ldg(a.ptr + rb + i);
+    __syncwarp();
+    const int32_t ke = sp[R];
+    int32_t rw = rb;      // row of the current window's first entry
     double carry = 0.0;   // partial sum of row rw from earlier windows
-    for (int32_t k0 = __ldg(a.ptr + rb); k0 < ke; k0 += 32) {
-        const int32_t k = k0 + lane;
-        const bool valid = k < ke;
-        double p = 0.0;
-        if (valid) {
-            const int32_t c = ld_stream_i1(a.col + k, pol);
-            const double v = ld_stream_d1(a.val + k, pol);
-            p = v * gather_x<HALO>(a.x, a.x_halo, a.n_loc, c);
-        }
-        // end (one past the last entry) of row rw + lane; rows past re end at ke
-        const int32_t rl = rw + 1 + lane;
-        const int32_t end_l = rl <= re ? __ldg(a.ptr + rl) : ke;
-        // lo = #{j : end_j <= k}: the window holds <= 32 rows, so lo <= 31
-        int lo = 0;
+    for (int32_t kb = sp[0]; kb < ke; kb += 32 * kTailBatch) {
+        int32_t c[kTailBatch];
+        double v[kTailBatch], xg[kTailBatch];
 #pragma unroll
-        for (int step = 16; step > 0; step >>= 1) {
-            const int32_t e = __shfl_sync(FULL, end_l, lo + step - 1);
-            if (e <= k) lo += step;
+        for (int i = 0; i < kTailBatch; ++i) {
+            const int32_t k = kb + 32 * i + lane;
+            c[i] = k < ke ? ld_stream_i1(a.col + k, pol) : -1;
+            v[i] = k < ke ? ld_stream_d1(a.val + k, pol) : 0.0;
         }
-        const int32_t my_end = __shfl_sync(FULL, end_l, lo);
-        const int32_t row = valid ? rw + lo : 0x7fffffff;
-        double sum = (lane == 0) ? p + carry : p;  // entry k0 always belongs to row rw
 #pragma unroll
-        for (int d = 1; d < 32; d <<= 1) {
-            const double su = __shfl_up_sync(FULL, sum, d);
-            const int32_t ru = __shfl_up_sync(FULL, row, d);
-            if (lane >= d && ru == row) sum += su;
-        }
-        if (valid && k + 1 == my_end) {  // last entry of its row: the row is complete
-            double* yp = a.y + __ldg(a.out_rows + row);
-            *yp += sum;
-        }
-        const double s31 = __shfl_sync(FULL, sum, 31);
-        const int32_t row31 = __shfl_sync(FULL, row, 31);
-        const int32_t end31 = __shfl_sync(FULL, my_end, 31);
-        if (k0 + 32 < ke) {  // next window exists (lane 31 was valid)
-            if (k0 + 32 < end31) { carry = s31; rw = row31; }
-            else { carry = 0.0; rw = row31 + 1; }
+        for (int i = 0; i < kTailBatch; ++i)
+            xg[i] = c[i] >= 0 ? gather_x<HALO>(a.x, a.x_halo, a.n_loc, c[i]) : 0.0;
+#pragma unroll
+        for (int i = 0; i < kTailBatch; ++i) {
+            const int32_t k0 = kb + 32 * i;
+            if (k0 >= ke) break;  // warp-uniform
+            const int32_t k = k0 + lane;
+            const bool valid = k < ke;
+            const double p = v[i] * xg[i];
+            // end (one past the last entry) of row rw + lane; rows past re end at ke
+            const int32_t rl = rw - rb + 1 + lane;
+            const int32_t end_l = rl <= R ? sp[rl] : ke;
+            // lo = #{j : end_j <= k}: a window holds <= 32 rows, so lo <= 31
+            int lo = 0;
+#pragma unroll
+            for (int step = 16; step > 0; step >>= 1) {
+                const int32_t e = __shfl_sync(FULL, end_l, lo + step - 1);
+                if (e <= k) lo += step;
+            }
+            const int32_t my_end = __shfl_sync(FULL, end_l, lo);
+            const int32_t row = valid ? rw + lo : 0x7fffffff;
+            double sum = (lane == 0) ? p + carry : p;  // entry k0 always belongs to row rw
+#pragma unroll
+            for (int d = 1; d < 32; d <<= 1) {
+                const double su = __shfl_up_sync(FULL, sum, d);
+                const int32_t ru = __shfl_up_sync(FULL, row, d);
+                if (lane >= d && ru == row) sum += su;
+            }
+            if (valid && k + 1 == my_end) {  // last entry of its row: the row is complete
+                double* yp = a.y + __ldg(a.out_rows + row);
+                *yp += sum;
+            }
+            const double s31 = __shfl_sync(FULL, sum, 31);
+            const int32_t row31 = __shfl_sync(FULL, row, 31);
+            const int32_t end31 = __shfl_sync(FULL, my_end, 31);
+            if (k0 + 32 < ke) {  // next window exists (lane 31 was valid)
+                if (k0 + 32 < end31) { carry = s31; rw = row31; }
+                else { carry = 0.0; rw = row31 + 1; }
+            }
         }
     }
 }
