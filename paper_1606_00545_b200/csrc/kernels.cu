@@ -162,20 +162,28 @@ __global__ void __launch_bounds__(256) ell_kernel(EllArgs a) {
 // ------------------------------------------------------------ tail kernel --
 // One warp per work unit: the tail rows whose first spilled entry falls in a
 // slice of <= 256 entries (plan_chunks, api.cpp), processed in row order as
-// the contiguous entry range [ptr[rb], ptr[re]).  The unit's <= 257 row
-// pointers are staged in shared memory once; entries are handled in batches
-// of 8 windows of 32: all 16 coalesced col/val loads of a batch, then its 8 x
-// gathers, are in flight before any is used.  Per window, every lane finds
-// its row by a 5-step shuffle search over the ends of the next 32 rows, a
-// segmented inclusive scan (__shfl_up_sync) sums each row's products, a carry
-// joins rows that cross windows, and the lane holding a row's last entry adds
-// the row sum into y (after the ELL kernel).  All lanes do useful work
-// whatever the row lengths; the order of additions is fixed (deterministic).
-constexpr int kTailBatch = 8;
+// the contiguous entry range [ptr[rb], ptr[re]) in batches of 256 entries.
+//   1. the unit's <= 257 row pointers are staged in shared memory once;
+//   2. per batch, 8 coalesced col/val loads and 8 x gathers per lane are in
+//      flight together; the products are transposed through shared memory
+//      (padded, conflict-free) so lane l owns entries kb + 8l .. kb + 8l + 7;
+//   3. each lane finds the row of its first entry (binary search in shared
+//      memory) and walks its 8 entries: rows that start and end inside the
+//      lane are added into y directly; the partial of the lane's last open
+//      row is its carry-out;
+//   4. a segmented inclusive scan of the carry-outs (__shfl_up_sync, keyed by
+//      row) gives each lane the carry-in of its first row, which completes
+//      rows spanning lanes; a warp carry joins rows spanning batches.
+// Every row is summed in one place in a fixed order: deterministic, no atomics.
+// The CSR part runs after the ELL kernel on the same stream.
+constexpr int kTailRun = 8;  // entries per lane per batch
+
+__device__ __forceinline__ int tail_pad(int i) { return i + (i >> 3); }
 
 template <bool HALO>
 __global__ void __launch_bounds__(256) tail_kernel(TailArgs a) {
     __shared__ int32_t s_ptr[8][kTailWarpEntries + 1];
+    __shared__ double s_p[8][256 + 32];
     const uint64_t pol = policy_evict_first();
     const unsigned FULL = 0xffffffffu;
     const int lane = threadIdx.x & 31, wib = threadIdx.x >> 5;
@@ -185,61 +193,75 @@ __global__ void __launch_bounds__(256) tail_kernel(TailArgs a) {
     if (rb >= re) return;
     const int32_t R = re - rb;  // <= 256 rows
     int32_t* sp = s_ptr[wib];
+    double* pp = s_p[wib];
     for (int32_t i = lane; i <= R; i += 32) sp[i] = __ldg(a.ptr + rb + i);
     __syncwarp();
     const int32_t ke = sp[R];
-    int32_t rw = rb;      // row of the current window's first entry
-    double carry = 0.0;   // partial sum of row rw from earlier windows
-    for (int32_t kb = sp[0]; kb < ke; kb += 32 * kTailBatch) {
-        int32_t c[kTailBatch];
-        double v[kTailBatch], xg[kTailBatch];
+    int32_t rw = 0;       // (relative) row containing the batch's first entry
+    double carry = 0.0;   // partial sum of row rw from earlier batches
+    for (int32_t kb = sp[0]; kb < ke; kb += 32 * kTailRun) {
+        int32_t c[kTailRun];
+        double v[kTailRun];
 #pragma unroll
-        for (int i = 0; i < kTailBatch; ++i) {
+        for (int i = 0; i < kTailRun; ++i) {
             const int32_t k = kb + 32 * i + lane;
             c[i] = k < ke ? ld_stream_i1(a.col + k, pol) : -1;
             v[i] = k < ke ? ld_stream_d1(a.val + k, pol) : 0.0;
         }
 #pragma unroll
-        for (int i = 0; i < kTailBatch; ++i)
-            xg[i] = c[i] >= 0 ? gather_x<HALO>(a.x, a.x_halo, a.n_loc, c[i]) : 0.0;
-#pragma unroll
-        for (int i = 0; i < kTailBatch; ++i) {
-            const int32_t k0 = kb + 32 * i;
-            if (k0 >= ke) break;  // warp-uniform
-            const int32_t k = k0 + lane;
-            const bool valid = k < ke;
-            const double p = v[i] * xg[i];
-            // end (one past the last entry) of row rw + lane; rows past re end at ke
-            const int32_t rl = rw - rb + 1 + lane;
-            const int32_t end_l = rl <= R ? sp[rl] : ke;
-            // lo = #{j : end_j <= k}: a window holds <= 32 rows, so lo <= 31
-            int lo = 0;
-#pragma unroll
-            for (int step = 16; step > 0; step >>= 1) {
-                const int32_t e = __shfl_sync(FULL, end_l, lo + step - 1);
-                if (e <= k) lo += step;
+        for (int i = 0; i < kTailRun; ++i) {
+            const double xg = c[i] >= 0 ? gather_x<HALO>(a.x, a.x_halo, a.n_loc, c[i]) : 0.0;
+            pp[tail_pad(32 * i + lane)] = v[i] * xg;
+        }
+        __syncwarp();
+        const int32_t kl = kb + kTailRun * lane;
+        int32_t rr = R - 1, first_row = -1;
+        double acc = 0.0, head = 0.0;
+        bool head_done = false;
+        if (kl < ke) {
+            int32_t lo = rw, hi = R - 1;  // first row whose end exceeds kl
+            while (lo < hi) {
+                const int32_t mid = (lo + hi) >> 1;
+                if (sp[mid + 1] > kl) hi = mid; else lo = mid + 1;
             }
-            const int32_t my_end = __shfl_sync(FULL, end_l, lo);
-            const int32_t row = valid ? rw + lo : 0x7fffffff;
-            double sum = (lane == 0) ? p + carry : p;  // entry k0 always belongs to row rw
+            rr = lo;
+            first_row = lo;
+            int32_t rend = sp[rr + 1];
+            bool first = true;
 #pragma unroll
-            for (int d = 1; d < 32; d <<= 1) {
-                const double su = __shfl_up_sync(FULL, sum, d);
-                const int32_t ru = __shfl_up_sync(FULL, row, d);
-                if (lane >= d && ru == row) sum += su;
-            }
-            if (valid && k + 1 == my_end) {  // last entry of its row: the row is complete
-                double* yp = a.y + __ldg(a.out_rows + row);
-                *yp += sum;
-            }
-            const double s31 = __shfl_sync(FULL, sum, 31);
-            const int32_t row31 = __shfl_sync(FULL, row, 31);
-            const int32_t end31 = __shfl_sync(FULL, my_end, 31);
-            if (k0 + 32 < ke) {  // next window exists (lane 31 was valid)
-                if (k0 + 32 < end31) { carry = s31; rw = row31; }
-                else { carry = 0.0; rw = row31 + 1; }
+            for (int j = 0; j < kTailRun; ++j) {
+                const int32_t k = kl + j;
+                if (k < ke) {
+                    acc += pp[tail_pad(kTailRun * lane + j)];
+                    if (k + 1 == rend) {  // row rr ends at entry k
+                        if (first) { head = acc; head_done = true; first = false; }
+                        else { a.y[__ldg(a.out_rows + rb + rr)] += acc; }
+                        acc = 0.0;
+                        ++rr;
+                        rend = rr < R ? sp[rr + 1] : ke;
+                    }
+                }
             }
         }
+        __syncwarp();  // pp is rewritten by the next batch
+        const int32_t row_out = kl < ke ? rr : 0x7fffffff;
+        double cs = acc;
+        if (lane == 0 && row_out == rw) cs += carry;
+#pragma unroll
+        for (int d = 1; d < 32; d <<= 1) {
+            const double cu = __shfl_up_sync(FULL, cs, d);
+            const int32_t ru = __shfl_up_sync(FULL, row_out, d);
+            if (lane >= d && ru == row_out) cs += cu;
+        }
+        const double prev_cs = __shfl_up_sync(FULL, cs, 1);
+        const int32_t prev_row = __shfl_up_sync(FULL, row_out, 1);
+        if (head_done) {
+            const double cin = lane == 0 ? carry : (prev_row == first_row ? prev_cs : 0.0);
+            a.y[__ldg(a.out_rows + rb + first_row)] += head + cin;
+        }
+        const double cs31 = __shfl_sync(FULL, cs, 31);
+        const int32_t row31 = __shfl_sync(FULL, row_out, 31);
+        if (kb + 32 * kTailRun < ke) { carry = cs31; rw = row31; }
     }
 }
 
