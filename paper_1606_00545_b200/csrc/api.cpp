@@ -5,6 +5,7 @@
 // firstly" by ell_kernel, then the CSR part by tail_kernel, both on the
 // caller's stream (stream order gives the ELL -> CSR ordering).
 #include <algorithm>
+#include <cstdlib>
 #include <cstring>
 #include <memory>
 
@@ -97,8 +98,10 @@ static void plan_chunks(hec_matrix_s* m, const HostHec& h, bool pipelined, std::
     const int32_t* tp = h.tail_ptr.data();
     // unit size: 256 entries, smaller (down to one 32-entry window) when the
     // tail is too small to give every SM warp a unit
+    int64_t Emax = 256;
+    if (const char* ev = std::getenv("HEC_TAIL_E")) Emax = std::max(32, std::min(kTailWarpEntries, std::atoi(ev)));
     int64_t E = (int64_t)h.tail_col.size() / (148 * 32);
-    E = E >= kTailWarpEntries ? kTailWarpEntries : (E < 32 ? 32 : E / 32 * 32);
+    E = E >= Emax ? Emax : (E < 32 ? 32 : E / 32 * 32);
     m->chunk_warp.assign(C + 1, 0);
     warp_row->clear();
     int32_t t0 = 0;

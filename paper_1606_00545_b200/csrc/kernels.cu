@@ -90,12 +90,29 @@ __device__ __forceinline__ void st_stream_d1(double* ptr, double a) {
 }
 
 // x gather: columns >= n_loc live in the halo buffer (distributed boundary).
+__device__ __forceinline__ double ld_keep_d1(const double* ptr, uint64_t pol) {
+    double r;
+    asm("ld.global.nc.L2::cache_hint.f64 %0, [%1], %2;" : "=d"(r) : "l"(ptr), "l"(pol));
+    return r;
+}
+
+__device__ __forceinline__ uint64_t policy_evict_last() {
+    uint64_t p;
+    asm("createpolicy.fractional.L2::evict_last.b64 %0, 1.0;" : "=l"(p));
+    return p;
+}
+
+// x gather: columns >= n_loc live in the halo buffer (distributed boundary).
+// __constant__ flag (tuning experiment): 1 = gathers carry an L2 evict_last hint.
+__constant__ int c_x_keep = 0;
+
 template <bool HALO>
 __device__ __forceinline__ double gather_x(const double* __restrict__ x,
                                            const double* __restrict__ xh, int32_t n_loc,
                                            int32_t c) {
-    if (HALO && c >= n_loc) return __ldg(xh + (c - n_loc));
-    return __ldg(x + c);
+    const double* p = (HALO && c >= n_loc) ? xh + (c - n_loc) : x + c;
+    if (c_x_keep) return ld_keep_d1(p, policy_evict_last());
+    return __ldg(p);
 }
 
 // ------------------------------------------------------------- ELL kernel --
@@ -176,22 +193,25 @@ __global__ void __launch_bounds__(256) ell_kernel(EllArgs a) {
 //      rows spanning lanes; a warp carry joins rows spanning batches.
 // Every row is summed in one place in a fixed order: deterministic, no atomics.
 // The CSR part runs after the ELL kernel on the same stream.
-constexpr int kTailRun = 8;  // entries per lane per batch
+// kTailRun = entries per lane per batch (template RUN); the product buffer is
+// padded one slot per RUN so both the row-major write and the lane-run read
+// are bank-conflict free.
+template <int RUN>
+__device__ __forceinline__ int tail_pad(int i) { return i + i / RUN; }
 
-__device__ __forceinline__ int tail_pad(int i) { return i + (i >> 3); }
-
-template <bool HALO>
-__global__ void __launch_bounds__(256) tail_kernel(TailArgs a) {
-    __shared__ int32_t s_ptr[8][kTailWarpEntries + 1];
-    __shared__ double s_p[8][256 + 32];
+template <bool HALO, int RUN>
+__global__ void __launch_bounds__(128) tail_kernel(TailArgs a) {
+    constexpr int kTailRun = RUN;
+    __shared__ int32_t s_ptr[4][kTailWarpEntries + 1];
+    __shared__ double s_p[4][32 * RUN + 32];
     const uint64_t pol = policy_evict_first();
     const unsigned FULL = 0xffffffffu;
     const int lane = threadIdx.x & 31, wib = threadIdx.x >> 5;
-    const int64_t w = a.warp_begin + (int64_t)blockIdx.x * 8 + wib;
+    const int64_t w = a.warp_begin + (int64_t)blockIdx.x * 4 + wib;
     if (w >= a.warp_end) return;  // warp-uniform
     const int32_t rb = __ldg(a.warp_row + w), re = __ldg(a.warp_row + w + 1);
     if (rb >= re) return;
-    const int32_t R = re - rb;  // <= 256 rows
+    const int32_t R = re - rb;  // <= kTailWarpEntries rows
     int32_t* sp = s_ptr[wib];
     double* pp = s_p[wib];
     for (int32_t i = lane; i <= R; i += 32) sp[i] = __ldg(a.ptr + rb + i);
@@ -211,7 +231,7 @@ __global__ void __launch_bounds__(256) tail_kernel(TailArgs a) {
 #pragma unroll
         for (int i = 0; i < kTailRun; ++i) {
             const double xg = c[i] >= 0 ? gather_x<HALO>(a.x, a.x_halo, a.n_loc, c[i]) : 0.0;
-            pp[tail_pad(32 * i + lane)] = v[i] * xg;
+            pp[tail_pad<RUN>(32 * i + lane)] = v[i] * xg;
         }
         __syncwarp();
         const int32_t kl = kb + kTailRun * lane;
@@ -232,7 +252,7 @@ __global__ void __launch_bounds__(256) tail_kernel(TailArgs a) {
             for (int j = 0; j < kTailRun; ++j) {
                 const int32_t k = kl + j;
                 if (k < ke) {
-                    acc += pp[tail_pad(kTailRun * lane + j)];
+                    acc += pp[tail_pad<RUN>(kTailRun * lane + j)];
                     if (k + 1 == rend) {  // row rr ends at entry k
                         if (first) { head = acc; head_done = true; first = false; }
                         else { a.y[__ldg(a.out_rows + rb + rr)] += acc; }
@@ -278,6 +298,10 @@ static int g_num_sms = 0;
 
 static int num_sms() {
     if (g_num_sms == 0) {
+        if (const char* e = std::getenv("HEC_X_KEEP")) {
+            const int one = std::atoi(e) != 0;
+            cudaMemcpyToSymbol(c_x_keep, &one, sizeof(int));
+        }
         int dev = 0;
         cudaGetDevice(&dev);
         cudaDeviceGetAttribute(&g_num_sms, cudaDevAttrMultiProcessorCount, dev);
@@ -333,10 +357,20 @@ cudaError_t launch_ell(const EllArgs& a, cudaStream_t s) {
 cudaError_t launch_tail(const TailArgs& a, cudaStream_t s) {
     const int64_t warps = a.warp_end - a.warp_begin;
     if (warps <= 0) return cudaSuccess;
-    const int64_t blocks = (warps + 7) / 8;
+    const int64_t blocks = (warps + 3) / 4;
     if (blocks > 0x7fffffff) return cudaErrorInvalidValue;
-    if (a.x_halo) tail_kernel<true><<<(unsigned)blocks, 256, 0, s>>>(a);
-    else tail_kernel<false><<<(unsigned)blocks, 256, 0, s>>>(a);
+    static int run = -1;
+    if (run < 0) {
+        const char* e = std::getenv("HEC_TAIL_RUN");
+        run = (e && std::atoi(e) == 16) ? 16 : 8;
+    }
+    if (run == 16) {
+        if (a.x_halo) tail_kernel<true, 16><<<(unsigned)blocks, 128, 0, s>>>(a);
+        else tail_kernel<false, 16><<<(unsigned)blocks, 128, 0, s>>>(a);
+    } else {
+        if (a.x_halo) tail_kernel<true, 8><<<(unsigned)blocks, 128, 0, s>>>(a);
+        else tail_kernel<false, 8><<<(unsigned)blocks, 128, 0, s>>>(a);
+    }
     return cudaGetLastError();
 }
 
