@@ -64,7 +64,7 @@ int32_t choose_width(const CsrView& A, const hec_opts& o);
 hec_status convert(const CsrView& A, int32_t width, int32_t stride_unit, HostHec* out);
 // CSR-tail work unit: at most this many spilled entries start rows owned by
 // one warp (see plan_chunks in api.cpp), so a unit owns <= 256 rows.
-constexpr int kTailWarpEntries = 512;
+constexpr int kTailWarpEntries = 256;
 
 // ------------------------------------------------------------------ plans --
 struct PartPlan {

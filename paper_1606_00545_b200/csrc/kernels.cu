@@ -204,6 +204,7 @@ __global__ void __launch_bounds__(128) tail_kernel(TailArgs a) {
     constexpr int kTailRun = RUN;
     __shared__ int32_t s_ptr[4][kTailWarpEntries + 1];
     __shared__ double s_p[4][32 * RUN + 32];
+    __shared__ double s_sum[4][kTailWarpEntries];
     const uint64_t pol = policy_evict_first();
     const unsigned FULL = 0xffffffffu;
     const int lane = threadIdx.x & 31, wib = threadIdx.x >> 5;
@@ -214,12 +215,11 @@ __global__ void __launch_bounds__(128) tail_kernel(TailArgs a) {
     const int32_t R = re - rb;  // <= kTailWarpEntries rows
     int32_t* sp = s_ptr[wib];
     double* pp = s_p[wib];
-    for (int32_t i = lane; i <= R; i += 32) sp[i] = __ldg(a.ptr + rb + i);
-    __syncwarp();
-    const int32_t ke = sp[R];
+    double* ss = s_sum[wib];   // completed row sums, written once per row
+    const int32_t k_first = __ldg(a.ptr + rb), ke = __ldg(a.ptr + re);
     int32_t rw = 0;       // (relative) row containing the batch's first entry
     double carry = 0.0;   // partial sum of row rw from earlier batches
-    for (int32_t kb = sp[0]; kb < ke; kb += 32 * kTailRun) {
+    for (int32_t kb = k_first; kb < ke; kb += 32 * kTailRun) {
         int32_t c[kTailRun];
         double v[kTailRun];
 #pragma unroll
@@ -228,6 +228,8 @@ __global__ void __launch_bounds__(128) tail_kernel(TailArgs a) {
             c[i] = k < ke ? ld_stream_i1(a.col + k, pol) : -1;
             v[i] = k < ke ? ld_stream_d1(a.val + k, pol) : 0.0;
         }
+        if (kb == k_first)  // stage the row pointers while the first batch is in flight
+            for (int32_t i = lane; i <= R; i += 32) sp[i] = __ldg(a.ptr + rb + i);
 #pragma unroll
         for (int i = 0; i < kTailRun; ++i) {
             const double xg = c[i] >= 0 ? gather_x<HALO>(a.x, a.x_halo, a.n_loc, c[i]) : 0.0;
@@ -255,7 +257,7 @@ __global__ void __launch_bounds__(128) tail_kernel(TailArgs a) {
                     acc += pp[tail_pad<RUN>(kTailRun * lane + j)];
                     if (k + 1 == rend) {  // row rr ends at entry k
                         if (first) { head = acc; head_done = true; first = false; }
-                        else { a.y[__ldg(a.out_rows + rb + rr)] += acc; }
+                        else { ss[rr] = acc; }
                         acc = 0.0;
                         ++rr;
                         rend = rr < R ? sp[rr + 1] : ke;
@@ -277,11 +279,17 @@ __global__ void __launch_bounds__(128) tail_kernel(TailArgs a) {
         const int32_t prev_row = __shfl_up_sync(FULL, row_out, 1);
         if (head_done) {
             const double cin = lane == 0 ? carry : (prev_row == first_row ? prev_cs : 0.0);
-            a.y[__ldg(a.out_rows + rb + first_row)] += head + cin;
+            ss[first_row] = head + cin;
         }
         const double cs31 = __shfl_sync(FULL, cs, 31);
         const int32_t row31 = __shfl_sync(FULL, row_out, 31);
         if (kb + 32 * kTailRun < ke) { carry = cs31; rw = row31; }
+    }
+    __syncwarp();
+    // add the unit's row sums into y: independent, coalesced out_rows loads
+    for (int32_t r = lane; r < R; r += 32) {
+        double* yp = a.y + __ldg(a.out_rows + rb + r);
+        *yp += ss[r];
     }
 }
 
