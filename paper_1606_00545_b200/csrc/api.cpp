@@ -29,8 +29,9 @@ static void release(hec_matrix_s* m) {
         int cur = 0;
         cudaGetDevice(&cur);
         cudaSetDevice(m->device);
-        void* ptrs[] = {m->d_ell_col, m->d_ell_val, m->d_tail_out, m->d_warp_row, m->d_tail_ptr,
-                        m->d_tail_col, m->d_tail_val, m->d_rowmap, m->d_stage_x, m->d_stage_y};
+        void* ptrs[] = {m->d_ell_col, m->d_ell_val, m->d_tail_out, m->d_tail_order, m->d_tail_blk,
+                        m->d_tail_ptr, m->d_tail_col, m->d_tail_val, m->d_rowmap, m->d_stage_x,
+                        m->d_stage_y};
         for (void* p : ptrs)
             if (p) cudaFree(p);
         for (cudaEvent_t e : m->ev_x) cudaEventDestroy(e);
@@ -55,13 +56,9 @@ struct DeviceGuard {
 };
 
 // Row chunks (for hec_spmv_host; one chunk for sub-matrices and small
-// matrices), the x prefix each chunk reads, and the tail work partition:
-// within each chunk the spilled entries are cut into warp units of
-// kTailWarpEntries; a unit owns the tail rows whose first spilled entry falls
-// inside it (so no row is split between warps and every row's sum is formed
-// in one place, deterministically).  warp_row[w] = first tail row of unit w;
-// unit w handles tail rows [warp_row[w], warp_row[w+1]).
-static void plan_chunks(hec_matrix_s* m, const HostHec& h, bool pipelined, std::vector<int32_t>* warp_row) {
+// matrices), the x prefix each chunk reads, and the tail-kernel work list.
+static void plan_chunks(hec_matrix_s* m, const HostHec& h, bool pipelined, std::vector<int32_t>* order,
+                        std::vector<int4>* blk) {
     const int32_t n = h.n_rows;
     int32_t K = pipelined ? n / (1 << 20) : 1;
     K = K < 1 ? 1 : (K > 16 ? 16 : K);
@@ -93,30 +90,37 @@ static void plan_chunks(hec_matrix_s* m, const HostHec& h, bool pipelined, std::
             m->chunk_xend[q] = run + 1;
         }
     }
-    // tail rows of each chunk (contiguous, tail rows are ascending) and warp units
+    // Tail rows of each chunk (contiguous: tail rows are ascending), cut into
+    // super-blocks of kTailSuperRows consecutive tail rows; inside a
+    // super-block the rows are regrouped by lanes-per-row G = 2^lg (stable), and
+    // each CUDA block takes 256/G rows of one group.  Consecutive blocks cover
+    // one super-block, so its entries and x window are still reused in L2
+    // while every group gets a row width that keeps its lanes busy.
     const int32_t tr = (int32_t)h.tail_rows.size();
     const int32_t* tp = h.tail_ptr.data();
-    // unit size: 256 entries, smaller (down to one 32-entry window) when the
-    // tail is too small to give every SM warp a unit
-    int64_t Emax = 256;
-    if (const char* ev = std::getenv("HEC_TAIL_E")) Emax = std::max(32, std::min(kTailWarpEntries, std::atoi(ev)));
-    int64_t E = (int64_t)h.tail_col.size() / (148 * 32);
-    E = E >= Emax ? Emax : (E < 32 ? 32 : E / 32 * 32);
-    m->chunk_warp.assign(C + 1, 0);
-    warp_row->clear();
+    order->assign(tr, 0);
+    blk->clear();
+    m->chunk_blk.assign(C + 1, 0);
     int32_t t0 = 0;
     for (int c = 0; c < C; ++c) {
         int32_t t1 = t0;
         while (t1 < tr && h.tail_rows[t1] < m->chunk_row[c + 1]) ++t1;
-        const int64_t k0 = tr ? tp[t0] : 0, k1 = tr ? tp[t1] : 0;
-        for (int64_t kb = k0; kb < k1; kb += E) {
-            const int32_t* r = std::lower_bound(tp + t0, tp + t1, (int32_t)kb);  // first row starting >= kb
-            warp_row->push_back((int32_t)(r - tp));
+        for (int32_t sb = t0; sb < t1; sb += kTailSuperRows) {
+            const int32_t se = std::min(t1, sb + kTailSuperRows);
+            int32_t cnt[6] = {0, 0, 0, 0, 0, 0}, pos[6];
+            for (int32_t t = sb; t < se; ++t) cnt[tail_lg_for(tp[t + 1] - tp[t])]++;
+            pos[0] = sb;
+            for (int g = 1; g < 6; ++g) pos[g] = pos[g - 1] + cnt[g - 1];
+            for (int g = 0; g < 6; ++g) {
+                const int32_t per_blk = 256 >> g;
+                for (int32_t f = pos[g]; f < pos[g] + cnt[g]; f += per_blk)
+                    blk->push_back(make_int4(f, std::min(per_blk, pos[g] + cnt[g] - f), g, 0));
+            }
+            for (int32_t t = sb; t < se; ++t) (*order)[pos[tail_lg_for(tp[t + 1] - tp[t])]++] = t;
         }
-        m->chunk_warp[c + 1] = (int64_t)warp_row->size();
+        m->chunk_blk[c + 1] = (int64_t)blk->size();
         t0 = t1;
     }
-    warp_row->push_back(tr);
 }
 
 hec_status make_matrix(HostHec&& h, int32_t device, cudaStream_t s, const int32_t* rowmap,
@@ -146,8 +150,9 @@ hec_status make_matrix(HostHec&& h, int32_t device, cudaStream_t s, const int32_
         return fail(HEC_ERR_NODEV, "no CUDA device available");
     if (device >= n_dev) return fail(HEC_ERR_ARG, "device ordinal out of range");
     DeviceGuard g(device);
-    std::vector<int32_t> warp_row;
-    plan_chunks(m.get(), h, n_loc < 0 && !rowmap, &warp_row);
+    std::vector<int32_t> order;
+    std::vector<int4> blk;
+    plan_chunks(m.get(), h, n_loc < 0 && !rowmap, &order, &blk);
     int64_t bytes = 0;
     hec_status st;
     if ((st = dmalloc_copy(&m->d_ell_col, h.ell_col.data(), h.ell_col.size(), s, &bytes))) return st;
@@ -157,7 +162,8 @@ hec_status make_matrix(HostHec&& h, int32_t device, cudaStream_t s, const int32_
         for (size_t t = 0; t < tail_out.size(); ++t)
             tail_out[t] = rowmap ? rowmap[h.tail_rows[t]] : row_off + h.tail_rows[t];
         if ((st = dmalloc_copy(&m->d_tail_out, tail_out.data(), tail_out.size(), s, &bytes))) return st;
-        if ((st = dmalloc_copy(&m->d_warp_row, warp_row.data(), warp_row.size(), s, &bytes))) return st;
+        if ((st = dmalloc_copy(&m->d_tail_order, order.data(), order.size(), s, &bytes))) return st;
+        if ((st = dmalloc_copy(&m->d_tail_blk, blk.data(), blk.size(), s, &bytes))) return st;
         if ((st = dmalloc_copy(&m->d_tail_ptr, h.tail_ptr.data(), h.tail_ptr.size(), s, &bytes))) return st;
         if ((st = dmalloc_copy(&m->d_tail_col, h.tail_col.data(), h.tail_col.size(), s, &bytes))) return st;
         if ((st = dmalloc_copy(&m->d_tail_val, h.tail_val.data(), h.tail_val.size(), s, &bytes))) return st;
@@ -192,13 +198,14 @@ static hec_status launch_chunks(const hec_matrix_s* A, int c, const double* x, c
     e.row_off = A->row_off;
     cudaError_t err = launch_ell(e, s);  // Alg. 1 lines 1-3: ELL first
     if (err != cudaSuccess) return cuda_fail(err, "ell_kernel launch");
-    const int64_t w0 = c < 0 ? 0 : A->chunk_warp[c];
-    const int64_t w1 = c < 0 ? A->chunk_warp[A->n_chunks] : A->chunk_warp[c + 1];
-    if (A->tail_rows > 0 && w1 > w0) {  // Alg. 1 lines 5-7: then the CSR part
+    const int64_t b0 = c < 0 ? 0 : A->chunk_blk[c];
+    const int64_t b1 = c < 0 ? A->chunk_blk[A->n_chunks] : A->chunk_blk[c + 1];
+    if (A->tail_rows > 0 && b1 > b0) {  // Alg. 1 lines 5-7: then the CSR part
         TailArgs t;
-        t.warp_row = A->d_warp_row;
-        t.warp_begin = w0;
-        t.warp_end = w1;
+        t.blk = A->d_tail_blk;
+        t.blk_begin = b0;
+        t.blk_end = b1;
+        t.order = A->d_tail_order;
         t.out_rows = A->d_tail_out;
         t.ptr = A->d_tail_ptr;
         t.col = A->d_tail_col;

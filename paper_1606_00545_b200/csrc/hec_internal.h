@@ -64,7 +64,14 @@ int32_t choose_width(const CsrView& A, const hec_opts& o);
 hec_status convert(const CsrView& A, int32_t width, int32_t stride_unit, HostHec* out);
 // CSR-tail work unit: at most this many spilled entries start rows owned by
 // one warp (see plan_chunks in api.cpp), so a unit owns <= 256 rows.
-constexpr int kTailWarpEntries = 256;
+constexpr int kTailSuperRows = 4096;   // tail rows regrouped by length within blocks of this many
+
+// Lanes per tail row: the smallest power of two >= ceil(L/2), capped at 32.
+inline int tail_lg_for(int32_t L) {
+    int lg = 0;
+    while (lg < 5 && (2 << lg) < L) ++lg;
+    return lg;
+}
 
 // ------------------------------------------------------------------ plans --
 struct PartPlan {
@@ -108,7 +115,8 @@ struct hec_matrix_s {
     int32_t* d_ell_col = nullptr;
     double* d_ell_val = nullptr;
     int32_t* d_tail_out = nullptr;     // output row of each tail row (after row map)
-    int32_t* d_warp_row = nullptr;     // first tail row of each warp unit (+ terminal)
+    int32_t* d_tail_order = nullptr;   // tail rows regrouped by length inside super-blocks
+    int4* d_tail_blk = nullptr;        // per CUDA block: {first, count, lg, 0} into d_tail_order
     int32_t* d_tail_ptr = nullptr;
     int32_t* d_tail_col = nullptr;
     double* d_tail_val = nullptr;
@@ -123,7 +131,7 @@ struct hec_matrix_s {
     int32_t n_chunks = 1;
     std::vector<int32_t> chunk_row;    // [n_chunks+1], multiples of 512
     std::vector<int32_t> chunk_xend;   // [n_chunks]: x[0 : xend) needed by rows < chunk_row[c+1]
-    std::vector<int64_t> chunk_warp;   // [n_chunks+1]: tail warp units of each chunk
+    std::vector<int64_t> chunk_blk;    // [n_chunks+1]: tail-kernel blocks of each chunk
     cudaStream_t s_h2d = nullptr, s_d2h = nullptr;
     std::vector<cudaEvent_t> ev_x, ev_y;
     cudaEvent_t ev_start = nullptr;
@@ -156,8 +164,9 @@ struct EllArgs {
     int32_t row_off;
 };
 struct TailArgs {
-    const int32_t* warp_row;    // unit w owns tail rows [warp_row[w], warp_row[w+1])
-    int64_t warp_begin, warp_end;
+    const int4* blk;            // block descriptors {first, count, lg, 0}
+    int64_t blk_begin, blk_end;
+    const int32_t* order;       // tail row ids, grouped (see plan_chunks in api.cpp)
     const int32_t* out_rows;
     const int32_t* ptr;
     const int32_t* col;

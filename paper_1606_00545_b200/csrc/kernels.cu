@@ -90,29 +90,13 @@ __device__ __forceinline__ void st_stream_d1(double* ptr, double a) {
 }
 
 // x gather: columns >= n_loc live in the halo buffer (distributed boundary).
-__device__ __forceinline__ double ld_keep_d1(const double* ptr, uint64_t pol) {
-    double r;
-    asm("ld.global.nc.L2::cache_hint.f64 %0, [%1], %2;" : "=d"(r) : "l"(ptr), "l"(pol));
-    return r;
-}
-
-__device__ __forceinline__ uint64_t policy_evict_last() {
-    uint64_t p;
-    asm("createpolicy.fractional.L2::evict_last.b64 %0, 1.0;" : "=l"(p));
-    return p;
-}
-
-// x gather: columns >= n_loc live in the halo buffer (distributed boundary).
-// __constant__ flag (tuning experiment): 1 = gathers carry an L2 evict_last hint.
-__constant__ int c_x_keep = 0;
-
+// (An L2 evict_last hint on the gathers was measured: no gain, r06.)
 template <bool HALO>
 __device__ __forceinline__ double gather_x(const double* __restrict__ x,
                                            const double* __restrict__ xh, int32_t n_loc,
                                            int32_t c) {
-    const double* p = (HALO && c >= n_loc) ? xh + (c - n_loc) : x + c;
-    if (c_x_keep) return ld_keep_d1(p, policy_evict_last());
-    return __ldg(p);
+    if (HALO && c >= n_loc) return __ldg(xh + (c - n_loc));
+    return __ldg(x + c);
 }
 
 // ------------------------------------------------------------- ELL kernel --
@@ -177,120 +161,37 @@ __global__ void __launch_bounds__(256) ell_kernel(EllArgs a) {
 }
 
 // ------------------------------------------------------------ tail kernel --
-// One warp per work unit: the tail rows whose first spilled entry falls in a
-// slice of <= 256 entries (plan_chunks, api.cpp), processed in row order as
-// the contiguous entry range [ptr[rb], ptr[re]) in batches of 256 entries.
-//   1. the unit's <= 257 row pointers are staged in shared memory once;
-//   2. per batch, 8 coalesced col/val loads and 8 x gathers per lane are in
-//      flight together; the products are transposed through shared memory
-//      (padded, conflict-free) so lane l owns entries kb + 8l .. kb + 8l + 7;
-//   3. each lane finds the row of its first entry (binary search in shared
-//      memory) and walks its 8 entries: rows that start and end inside the
-//      lane are added into y directly; the partial of the lane's last open
-//      row is its carry-out;
-//   4. a segmented inclusive scan of the carry-outs (__shfl_up_sync, keyed by
-//      row) gives each lane the carry-in of its first row, which completes
-//      rows spanning lanes; a warp carry joins rows spanning batches.
-// Every row is summed in one place in a fixed order: deterministic, no atomics.
-// The CSR part runs after the ELL kernel on the same stream.
-// kTailRun = entries per lane per batch (template RUN); the product buffer is
-// padded one slot per RUN so both the row-major write and the lane-run read
-// are bank-conflict free.
-template <int RUN>
-__device__ __forceinline__ int tail_pad(int i) { return i + i / RUN; }
-
-template <bool HALO, int RUN>
-__global__ void __launch_bounds__(128) tail_kernel(TailArgs a) {
-    constexpr int kTailRun = RUN;
-    __shared__ int32_t s_ptr[4][kTailWarpEntries + 1];
-    __shared__ double s_p[4][32 * RUN + 32];
-    __shared__ double s_sum[4][kTailWarpEntries];
+// The CSR part (Alg. 1 lines 5-7) for the rows that spill.  Rows
+// are regrouped by length inside super-blocks of consecutive tail rows
+// (plan_chunks, api.cpp): a CUDA block takes 256/G rows that all use G = 2^lg
+// lanes (G ~ half the spilled length, so each lane handles about two entries;
+// long rows loop).  The G lanes of a row read its contiguous entries, gather
+// x, reduce with __shfl_xor_sync and the first lane adds the row sum into the
+// ELL result (this kernel runs after ell_kernel on the same stream).
+// Blocks of one super-block run back to back, so its entries and the x window
+// they touch are reused in L2.  Fixed reduction order: deterministic.
+template <bool HALO>
+__global__ void __launch_bounds__(256) tail_kernel(TailArgs a) {
     const uint64_t pol = policy_evict_first();
-    const unsigned FULL = 0xffffffffu;
-    const int lane = threadIdx.x & 31, wib = threadIdx.x >> 5;
-    const int64_t w = a.warp_begin + (int64_t)blockIdx.x * 4 + wib;
-    if (w >= a.warp_end) return;  // warp-uniform
-    const int32_t rb = __ldg(a.warp_row + w), re = __ldg(a.warp_row + w + 1);
-    if (rb >= re) return;
-    const int32_t R = re - rb;  // <= kTailWarpEntries rows
-    int32_t* sp = s_ptr[wib];
-    double* pp = s_p[wib];
-    double* ss = s_sum[wib];   // completed row sums, written once per row
-    const int32_t k_first = __ldg(a.ptr + rb), ke = __ldg(a.ptr + re);
-    int32_t rw = 0;       // (relative) row containing the batch's first entry
-    double carry = 0.0;   // partial sum of row rw from earlier batches
-    for (int32_t kb = k_first; kb < ke; kb += 32 * kTailRun) {
-        int32_t c[kTailRun];
-        double v[kTailRun];
-#pragma unroll
-        for (int i = 0; i < kTailRun; ++i) {
-            const int32_t k = kb + 32 * i + lane;
-            c[i] = k < ke ? ld_stream_i1(a.col + k, pol) : -1;
-            v[i] = k < ke ? ld_stream_d1(a.val + k, pol) : 0.0;
+    const int4 d = __ldg(a.blk + a.blk_begin + blockIdx.x);  // {first, count, lg, 0}
+    const int lg = d.z;
+    const int G = 1 << lg;
+    const int lane = threadIdx.x & (G - 1);
+    const int grp = threadIdx.x >> lg;
+    double acc = 0.0;
+    int32_t t = -1;
+    if (grp < d.y) {
+        t = __ldg(a.order + d.x + grp);
+        const int32_t kb = __ldg(a.ptr + t), ke = __ldg(a.ptr + t + 1);
+#pragma unroll 4
+        for (int32_t k = kb + lane; k < ke; k += G) {
+            const int32_t c = ld_stream_i1(a.col + k, pol);
+            const double v = ld_stream_d1(a.val + k, pol);
+            acc = fma(v, gather_x<HALO>(a.x, a.x_halo, a.n_loc, c), acc);
         }
-        if (kb == k_first)  // stage the row pointers while the first batch is in flight
-            for (int32_t i = lane; i <= R; i += 32) sp[i] = __ldg(a.ptr + rb + i);
-#pragma unroll
-        for (int i = 0; i < kTailRun; ++i) {
-            const double xg = c[i] >= 0 ? gather_x<HALO>(a.x, a.x_halo, a.n_loc, c[i]) : 0.0;
-            pp[tail_pad<RUN>(32 * i + lane)] = v[i] * xg;
-        }
-        __syncwarp();
-        const int32_t kl = kb + kTailRun * lane;
-        int32_t rr = R - 1, first_row = -1;
-        double acc = 0.0, head = 0.0;
-        bool head_done = false;
-        if (kl < ke) {
-            int32_t lo = rw, hi = R - 1;  // first row whose end exceeds kl
-            while (lo < hi) {
-                const int32_t mid = (lo + hi) >> 1;
-                if (sp[mid + 1] > kl) hi = mid; else lo = mid + 1;
-            }
-            rr = lo;
-            first_row = lo;
-            int32_t rend = sp[rr + 1];
-            bool first = true;
-#pragma unroll
-            for (int j = 0; j < kTailRun; ++j) {
-                const int32_t k = kl + j;
-                if (k < ke) {
-                    acc += pp[tail_pad<RUN>(kTailRun * lane + j)];
-                    if (k + 1 == rend) {  // row rr ends at entry k
-                        if (first) { head = acc; head_done = true; first = false; }
-                        else { ss[rr] = acc; }
-                        acc = 0.0;
-                        ++rr;
-                        rend = rr < R ? sp[rr + 1] : ke;
-                    }
-                }
-            }
-        }
-        __syncwarp();  // pp is rewritten by the next batch
-        const int32_t row_out = kl < ke ? rr : 0x7fffffff;
-        double cs = acc;
-        if (lane == 0 && row_out == rw) cs += carry;
-#pragma unroll
-        for (int d = 1; d < 32; d <<= 1) {
-            const double cu = __shfl_up_sync(FULL, cs, d);
-            const int32_t ru = __shfl_up_sync(FULL, row_out, d);
-            if (lane >= d && ru == row_out) cs += cu;
-        }
-        const double prev_cs = __shfl_up_sync(FULL, cs, 1);
-        const int32_t prev_row = __shfl_up_sync(FULL, row_out, 1);
-        if (head_done) {
-            const double cin = lane == 0 ? carry : (prev_row == first_row ? prev_cs : 0.0);
-            ss[first_row] = head + cin;
-        }
-        const double cs31 = __shfl_sync(FULL, cs, 31);
-        const int32_t row31 = __shfl_sync(FULL, row_out, 31);
-        if (kb + 32 * kTailRun < ke) { carry = cs31; rw = row31; }
     }
-    __syncwarp();
-    // add the unit's row sums into y: independent, coalesced out_rows loads
-    for (int32_t r = lane; r < R; r += 32) {
-        double* yp = a.y + __ldg(a.out_rows + rb + r);
-        *yp += ss[r];
-    }
+    for (int off = G >> 1; off > 0; off >>= 1) acc += __shfl_xor_sync(0xffffffffu, acc, off, G);
+    if (lane == 0 && t >= 0) a.y[__ldg(a.out_rows + t)] += acc;
 }
 
 // ------------------------------------------------------------ pack kernel --
@@ -306,10 +207,6 @@ static int g_num_sms = 0;
 
 static int num_sms() {
     if (g_num_sms == 0) {
-        if (const char* e = std::getenv("HEC_X_KEEP")) {
-            const int one = std::atoi(e) != 0;
-            cudaMemcpyToSymbol(c_x_keep, &one, sizeof(int));
-        }
         int dev = 0;
         cudaGetDevice(&dev);
         cudaDeviceGetAttribute(&g_num_sms, cudaDevAttrMultiProcessorCount, dev);
@@ -363,22 +260,11 @@ cudaError_t launch_ell(const EllArgs& a, cudaStream_t s) {
 }
 
 cudaError_t launch_tail(const TailArgs& a, cudaStream_t s) {
-    const int64_t warps = a.warp_end - a.warp_begin;
-    if (warps <= 0) return cudaSuccess;
-    const int64_t blocks = (warps + 3) / 4;
+    const int64_t blocks = a.blk_end - a.blk_begin;
+    if (blocks <= 0) return cudaSuccess;
     if (blocks > 0x7fffffff) return cudaErrorInvalidValue;
-    static int run = -1;
-    if (run < 0) {
-        const char* e = std::getenv("HEC_TAIL_RUN");
-        run = (e && std::atoi(e) == 16) ? 16 : 8;
-    }
-    if (run == 16) {
-        if (a.x_halo) tail_kernel<true, 16><<<(unsigned)blocks, 128, 0, s>>>(a);
-        else tail_kernel<false, 16><<<(unsigned)blocks, 128, 0, s>>>(a);
-    } else {
-        if (a.x_halo) tail_kernel<true, 8><<<(unsigned)blocks, 128, 0, s>>>(a);
-        else tail_kernel<false, 8><<<(unsigned)blocks, 128, 0, s>>>(a);
-    }
+    if (a.x_halo) tail_kernel<true><<<(unsigned)blocks, 256, 0, s>>>(a);
+    else tail_kernel<false><<<(unsigned)blocks, 256, 0, s>>>(a);
     return cudaGetLastError();
 }
 
