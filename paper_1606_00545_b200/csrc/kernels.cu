@@ -19,6 +19,7 @@
 #include <cstdint>
 #include <cstdlib>
 #include <cstring>
+#include <utility>
 
 #include "hec_internal.h"
 
@@ -215,6 +216,52 @@ static int num_sms() {
     return g_num_sms;
 }
 
+// L2 residency of x: with HEC_X_PERSIST=1 the kernels are launched with an
+// access-policy window marking x "persisting" in L2 (set-aside sized once per
+// process from cudaDevAttrMaxPersistingL2CacheSize), so the matrix streams
+// cannot evict the vector the gathers reuse.  Tuning experiment.
+static int x_persist() {
+    static int v = -1;
+    if (v < 0) {
+        const char* e = std::getenv("HEC_X_PERSIST");
+        v = (e && std::atoi(e) != 0) ? 1 : 0;
+        if (v) {
+            int dev = 0, maxp = 0;
+            cudaGetDevice(&dev);
+            cudaDeviceGetAttribute(&maxp, cudaDevAttrMaxPersistingL2CacheSize, dev);
+            if (maxp <= 0 || cudaDeviceSetLimit(cudaLimitPersistingL2CacheSize, (size_t)maxp) != cudaSuccess) v = 0;
+        }
+    }
+    return v;
+}
+
+template <typename... KArgs, typename... Args>
+static cudaError_t launch_k(void (*kernel)(KArgs...), dim3 g, dim3 b, cudaStream_t s, const void* x,
+                            size_t x_bytes, Args&&... args) {
+    cudaLaunchConfig_t cfg = {};
+    cfg.gridDim = g;
+    cfg.blockDim = b;
+    cfg.stream = s;
+    cudaLaunchAttribute attr[1];
+    cfg.attrs = attr;
+    cfg.numAttrs = 0;
+    if (x && x_bytes && x_persist()) {
+        int dev = 0, maxw = 0, maxp = 0;
+        cudaGetDevice(&dev);
+        cudaDeviceGetAttribute(&maxw, cudaDevAttrMaxAccessPolicyWindowSize, dev);
+        cudaDeviceGetAttribute(&maxp, cudaDevAttrMaxPersistingL2CacheSize, dev);
+        const size_t nb = x_bytes < (size_t)maxw ? x_bytes : (size_t)maxw;
+        attr[0].id = cudaLaunchAttributeAccessPolicyWindow;
+        attr[0].val.accessPolicyWindow.base_ptr = const_cast<void*>(x);
+        attr[0].val.accessPolicyWindow.num_bytes = nb;
+        attr[0].val.accessPolicyWindow.hitRatio = nb <= (size_t)maxp ? 1.0f : (float)maxp / (float)nb;
+        attr[0].val.accessPolicyWindow.hitProp = cudaAccessPropertyPersisting;
+        attr[0].val.accessPolicyWindow.missProp = cudaAccessPropertyStreaming;
+        cfg.numAttrs = 1;
+    }
+    return cudaLaunchKernelEx(&cfg, kernel, std::forward<Args>(args)...);
+}
+
 template <bool HALO, bool ROWMAP>
 static cudaError_t launch_ell_t(const EllArgs& a, cudaStream_t s) {
     const int64_t n_pairs = ((int64_t)a.n_rows + 1) >> 1;
@@ -224,15 +271,15 @@ static cudaError_t launch_ell_t(const EllArgs& a, cudaStream_t s) {
     if (blocks > cap) blocks = cap;
     if (blocks < 1) blocks = 1;
     const dim3 g((unsigned)blocks), b(threads);
+    const size_t xb = (size_t)a.n_loc * sizeof(double);
     switch (a.width) {
 #define HEC_W(w) \
-    case w: ell_kernel<w, HALO, ROWMAP><<<g, b, 0, s>>>(a); break;
+    case w: return launch_k(ell_kernel<w, HALO, ROWMAP>, g, b, s, a.x, xb, a);
         HEC_W(1) HEC_W(2) HEC_W(3) HEC_W(4) HEC_W(5) HEC_W(6) HEC_W(7) HEC_W(8)
         HEC_W(9) HEC_W(10) HEC_W(11) HEC_W(12) HEC_W(13) HEC_W(14) HEC_W(15) HEC_W(16)
 #undef HEC_W
-        default: ell_kernel<0, HALO, ROWMAP><<<g, b, 0, s>>>(a); break;
+        default: return launch_k(ell_kernel<0, HALO, ROWMAP>, g, b, s, a.x, xb, a);
     }
-    return cudaGetLastError();
 }
 
 // ELL kernel choice: "reg" (register-streaming ell_kernel) or "tma" (bulk-copy
@@ -263,9 +310,9 @@ cudaError_t launch_tail(const TailArgs& a, cudaStream_t s) {
     const int64_t blocks = a.blk_end - a.blk_begin;
     if (blocks <= 0) return cudaSuccess;
     if (blocks > 0x7fffffff) return cudaErrorInvalidValue;
-    if (a.x_halo) tail_kernel<true><<<(unsigned)blocks, 256, 0, s>>>(a);
-    else tail_kernel<false><<<(unsigned)blocks, 256, 0, s>>>(a);
-    return cudaGetLastError();
+    const size_t xb = (size_t)a.n_loc * sizeof(double);
+    if (a.x_halo) return launch_k(tail_kernel<true>, dim3((unsigned)blocks), dim3(256), s, a.x, xb, a);
+    return launch_k(tail_kernel<false>, dim3((unsigned)blocks), dim3(256), s, a.x, xb, a);
 }
 
 cudaError_t launch_pack(const int32_t* idx, int32_t n, const double* x, double* out,
