@@ -29,7 +29,7 @@ static void release(hec_matrix_s* m) {
         int cur = 0;
         cudaGetDevice(&cur);
         cudaSetDevice(m->device);
-        void* ptrs[] = {m->d_ell_col, m->d_ell_val, m->d_tail_out, m->d_tail_order, m->d_tail_blk,
+        void* ptrs[] = {m->d_ell_col, m->d_ell_val, m->d_tail_out, m->d_tail_blk,
                         m->d_tail_ptr, m->d_tail_col, m->d_tail_val, m->d_rowmap, m->d_stage_x,
                         m->d_stage_y};
         for (void* p : ptrs)
@@ -158,15 +158,28 @@ hec_status make_matrix(HostHec&& h, int32_t device, cudaStream_t s, const int32_
     if ((st = dmalloc_copy(&m->d_ell_col, h.ell_col.data(), h.ell_col.size(), s, &bytes))) return st;
     if ((st = dmalloc_copy(&m->d_ell_val, h.ell_val.data(), h.ell_val.size(), s, &bytes))) return st;
     if (!h.tail_rows.empty()) {
-        std::vector<int32_t> tail_out(h.tail_rows.size());
-        for (size_t t = 0; t < tail_out.size(); ++t)
-            tail_out[t] = rowmap ? rowmap[h.tail_rows[t]] : row_off + h.tail_rows[t];
-        if ((st = dmalloc_copy(&m->d_tail_out, tail_out.data(), tail_out.size(), s, &bytes))) return st;
-        if ((st = dmalloc_copy(&m->d_tail_order, order.data(), order.size(), s, &bytes))) return st;
+        // Device copy of the CSR tail in the kernel's order (rows regrouped
+        // inside super-blocks, plan_chunks): a block's rows and their entries
+        // are contiguous, and the kernel needs no indirection.  hec_export
+        // undoes the permutation with m->h_tail_order.
+        const size_t tr = h.tail_rows.size();
+        std::vector<int32_t> dptr(tr + 1), dout(tr), dcol(h.tail_col.size());
+        std::vector<double> dval(h.tail_val.size());
+        dptr[0] = 0;
+        for (size_t p = 0; p < tr; ++p) {
+            const int32_t t = order[p];
+            const int32_t b = h.tail_ptr[t], e = h.tail_ptr[t + 1];
+            std::copy(h.tail_col.begin() + b, h.tail_col.begin() + e, dcol.begin() + dptr[p]);
+            std::copy(h.tail_val.begin() + b, h.tail_val.begin() + e, dval.begin() + dptr[p]);
+            dptr[p + 1] = dptr[p] + (e - b);
+            dout[p] = rowmap ? rowmap[h.tail_rows[t]] : row_off + h.tail_rows[t];
+        }
+        m->h_tail_order = order;
+        if ((st = dmalloc_copy(&m->d_tail_out, dout.data(), dout.size(), s, &bytes))) return st;
         if ((st = dmalloc_copy(&m->d_tail_blk, blk.data(), blk.size(), s, &bytes))) return st;
-        if ((st = dmalloc_copy(&m->d_tail_ptr, h.tail_ptr.data(), h.tail_ptr.size(), s, &bytes))) return st;
-        if ((st = dmalloc_copy(&m->d_tail_col, h.tail_col.data(), h.tail_col.size(), s, &bytes))) return st;
-        if ((st = dmalloc_copy(&m->d_tail_val, h.tail_val.data(), h.tail_val.size(), s, &bytes))) return st;
+        if ((st = dmalloc_copy(&m->d_tail_ptr, dptr.data(), dptr.size(), s, &bytes))) return st;
+        if ((st = dmalloc_copy(&m->d_tail_col, dcol.data(), dcol.size(), s, &bytes))) return st;
+        if ((st = dmalloc_copy(&m->d_tail_val, dval.data(), dval.size(), s, &bytes))) return st;
         HEC_CUDA_TRY(cudaStreamSynchronize(s));  // host vectors die after return
     }
     if (rowmap)
@@ -205,7 +218,6 @@ static hec_status launch_chunks(const hec_matrix_s* A, int c, const double* x, c
         t.blk = A->d_tail_blk;
         t.blk_begin = b0;
         t.blk_end = b1;
-        t.order = A->d_tail_order;
         t.out_rows = A->d_tail_out;
         t.ptr = A->d_tail_ptr;
         t.col = A->d_tail_col;
@@ -285,14 +297,28 @@ hec_status hec_export(hec_matrix A, hec_host_arrays* o) {
     DeviceGuard g(A->device);
     if (o->ell_col && slots) HEC_CUDA_TRY(cudaMemcpy(o->ell_col, A->d_ell_col, slots * sizeof(int32_t), cudaMemcpyDeviceToHost));
     if (o->ell_val && slots) HEC_CUDA_TRY(cudaMemcpy(o->ell_val, A->d_ell_val, slots * sizeof(double), cudaMemcpyDeviceToHost));
-    if (o->tail_ptr) {
-        if (A->tail_rows)
-            HEC_CUDA_TRY(cudaMemcpy(o->tail_ptr, A->d_tail_ptr, ((size_t)A->tail_rows + 1) * sizeof(int32_t), cudaMemcpyDeviceToHost));
-        else
-            o->tail_ptr[0] = 0;
+    if (!A->tail_rows) {
+        if (o->tail_ptr) o->tail_ptr[0] = 0;
+        return HEC_OK;
     }
-    if (o->tail_col && A->tail_nnz) HEC_CUDA_TRY(cudaMemcpy(o->tail_col, A->d_tail_col, A->tail_nnz * sizeof(int32_t), cudaMemcpyDeviceToHost));
-    if (o->tail_val && A->tail_nnz) HEC_CUDA_TRY(cudaMemcpy(o->tail_val, A->d_tail_val, A->tail_nnz * sizeof(double), cudaMemcpyDeviceToHost));
+    // the device tail is stored in kernel order (see make_matrix): undo it
+    const size_t tr = (size_t)A->tail_rows;
+    std::vector<int32_t> dptr(tr + 1), dcol((size_t)A->tail_nnz);
+    std::vector<double> dval((size_t)A->tail_nnz);
+    HEC_CUDA_TRY(cudaMemcpy(dptr.data(), A->d_tail_ptr, (tr + 1) * sizeof(int32_t), cudaMemcpyDeviceToHost));
+    HEC_CUDA_TRY(cudaMemcpy(dcol.data(), A->d_tail_col, dcol.size() * sizeof(int32_t), cudaMemcpyDeviceToHost));
+    HEC_CUDA_TRY(cudaMemcpy(dval.data(), A->d_tail_val, dval.size() * sizeof(double), cudaMemcpyDeviceToHost));
+    std::vector<int32_t> where(tr);  // tail row t -> device position
+    for (size_t p = 0; p < tr; ++p) where[A->h_tail_order[p]] = (int32_t)p;
+    int32_t k = 0;
+    for (size_t t = 0; t < tr; ++t) {
+        const int32_t p = where[t], b = dptr[p], e = dptr[p + 1];
+        if (o->tail_ptr) o->tail_ptr[t] = k;
+        if (o->tail_col) std::copy(dcol.begin() + b, dcol.begin() + e, o->tail_col + k);
+        if (o->tail_val) std::copy(dval.begin() + b, dval.begin() + e, o->tail_val + k);
+        k += e - b;
+    }
+    if (o->tail_ptr) o->tail_ptr[tr] = k;
     return HEC_OK;
 }
 

@@ -115,8 +115,8 @@ struct hec_matrix_s {
     int32_t* d_ell_col = nullptr;
     double* d_ell_val = nullptr;
     int32_t* d_tail_out = nullptr;     // output row of each tail row (after row map)
-    int32_t* d_tail_order = nullptr;   // tail rows regrouped by length inside super-blocks
-    int4* d_tail_blk = nullptr;        // per CUDA block: {first, count, lg, 0} into d_tail_order
+    std::vector<int32_t> h_tail_order; // device tail position p holds tail row h_tail_order[p]
+    int4* d_tail_blk = nullptr;        // per CUDA block: {first position, count, lg, 0}
     int32_t* d_tail_ptr = nullptr;
     int32_t* d_tail_col = nullptr;
     double* d_tail_val = nullptr;
@@ -166,7 +166,6 @@ struct EllArgs {
 struct TailArgs {
     const int4* blk;            // block descriptors {first, count, lg, 0}
     int64_t blk_begin, blk_end;
-    const int32_t* order;       // tail row ids, grouped (see plan_chunks in api.cpp)
     const int32_t* out_rows;
     const int32_t* ptr;
     const int32_t* col;

@@ -179,11 +179,16 @@ __global__ void __launch_bounds__(256) tail_kernel(TailArgs a) {
     const int G = 1 << lg;
     const int lane = threadIdx.x & (G - 1);
     const int grp = threadIdx.x >> lg;
-    double acc = 0.0;
-    int32_t t = -1;
-    if (grp < d.y) {
-        t = __ldg(a.order + d.x + grp);
+    double acc = 0.0, y_old = 0.0;
+    double* yp = nullptr;
+    const bool active = grp < d.y;
+    if (active) {
+        const int32_t t = d.x + grp;  // device position: the block's rows are contiguous
         const int32_t kb = __ldg(a.ptr + t), ke = __ldg(a.ptr + t + 1);
+        if (lane == 0) {  // the ELL result this row adds to (written by the previous kernel)
+            yp = a.y + __ldg(a.out_rows + t);
+            y_old = *yp;
+        }
 #pragma unroll 4
         for (int32_t k = kb + lane; k < ke; k += G) {
             const int32_t c = ld_stream_i1(a.col + k, pol);
@@ -192,7 +197,7 @@ __global__ void __launch_bounds__(256) tail_kernel(TailArgs a) {
         }
     }
     for (int off = G >> 1; off > 0; off >>= 1) acc += __shfl_xor_sync(0xffffffffu, acc, off, G);
-    if (lane == 0 && t >= 0) a.y[__ldg(a.out_rows + t)] += acc;
+    if (lane == 0 && active) *yp = y_old + acc;
 }
 
 // ------------------------------------------------------------ pack kernel --
