@@ -101,6 +101,8 @@ static void plan_chunks(hec_matrix_s* m, const HostHec& h, bool pipelined, std::
     order->assign(tr, 0);
     blk->clear();
     m->chunk_blk.assign(C + 1, 0);
+    int epl = 2;  // target entries per lane
+    if (const char* e = std::getenv("HEC_TAIL_EPL")) epl = std::max(1, std::min(16, std::atoi(e)));
     int32_t t0 = 0;
     for (int c = 0; c < C; ++c) {
         int32_t t1 = t0;
@@ -108,7 +110,7 @@ static void plan_chunks(hec_matrix_s* m, const HostHec& h, bool pipelined, std::
         for (int32_t sb = t0; sb < t1; sb += kTailSuperRows) {
             const int32_t se = std::min(t1, sb + kTailSuperRows);
             int32_t cnt[6] = {0, 0, 0, 0, 0, 0}, pos[6];
-            for (int32_t t = sb; t < se; ++t) cnt[tail_lg_for(tp[t + 1] - tp[t])]++;
+            for (int32_t t = sb; t < se; ++t) cnt[tail_lg_for(tp[t + 1] - tp[t], epl)]++;
             pos[0] = sb;
             for (int g = 1; g < 6; ++g) pos[g] = pos[g - 1] + cnt[g - 1];
             for (int g = 0; g < 6; ++g) {
@@ -116,7 +118,7 @@ static void plan_chunks(hec_matrix_s* m, const HostHec& h, bool pipelined, std::
                 for (int32_t f = pos[g]; f < pos[g] + cnt[g]; f += per_blk)
                     blk->push_back(make_int4(f, std::min(per_blk, pos[g] + cnt[g] - f), g, 0));
             }
-            for (int32_t t = sb; t < se; ++t) (*order)[pos[tail_lg_for(tp[t + 1] - tp[t])]++] = t;
+            for (int32_t t = sb; t < se; ++t) (*order)[pos[tail_lg_for(tp[t + 1] - tp[t], epl)]++] = t;
         }
         m->chunk_blk[c + 1] = (int64_t)blk->size();
         t0 = t1;

@@ -66,10 +66,11 @@ hec_status convert(const CsrView& A, int32_t width, int32_t stride_unit, HostHec
 // one warp (see plan_chunks in api.cpp), so a unit owns <= 256 rows.
 constexpr int kTailSuperRows = 4096;   // tail rows regrouped by length within blocks of this many
 
-// Lanes per tail row: the smallest power of two >= ceil(L/2), capped at 32.
-inline int tail_lg_for(int32_t L) {
+// Lanes per tail row: the smallest power of two >= ceil(L / epl), capped at
+// 32, where epl = target entries per lane.
+inline int tail_lg_for(int32_t L, int epl) {
     int lg = 0;
-    while (lg < 5 && (2 << lg) < L) ++lg;
+    while (lg < 5 && (epl << lg) < L) ++lg;
     return lg;
 }
 
