@@ -101,7 +101,10 @@ static void plan_chunks(hec_matrix_s* m, const HostHec& h, bool pipelined, std::
     order->assign(tr, 0);
     blk->clear();
     m->chunk_blk.assign(C + 1, 0);
-    int epl = 2;  // target entries per lane
+    // target entries per lane: more entries per lane = more loads in flight per
+    // row and fewer rows in flight -- better for big tails (measured r11:
+    // power-law 2^23 tail 8 > 4 > 2 > 1), worse for tiny ones (SPE10)
+    int epl = h.tail_col.size() >= ((size_t)1 << 22) ? 8 : 2;
     if (const char* e = std::getenv("HEC_TAIL_EPL")) epl = std::max(1, std::min(16, std::atoi(e)));
     int32_t t0 = 0;
     for (int c = 0; c < C; ++c) {

@@ -189,7 +189,7 @@ __global__ void __launch_bounds__(256) tail_kernel(TailArgs a) {
             yp = a.y + __ldg(a.out_rows + t);
             y_old = *yp;
         }
-#pragma unroll 4
+#pragma unroll 8
         for (int32_t k = kb + lane; k < ke; k += G) {
             const int32_t c = ld_stream_i1(a.col + k, pol);
             const double v = ld_stream_d1(a.val + k, pol);
