@@ -17,7 +17,6 @@
 #include <cuda_runtime.h>
 
 #include <cstdint>
-#include <cstdio>
 #include <cstdlib>
 #include <cstring>
 #include <utility>
@@ -162,82 +161,6 @@ __global__ void __launch_bounds__(256) ell_kernel(EllArgs a) {
     }
 }
 
-// Tuning variant of the plain (no halo, no row map) ELL kernel, selected by
-// HEC_ELL_X="rpt,pf,block": rpt = row pairs per thread (1 or 2; with 2 a warp
-// covers a 128-row tile, lane l owning pairs 2l and 64+2l), pf = 1 adds an
-// L2::256B prefetch-size hint to the matrix streams, block = threads per CTA.
-template <bool PF>
-__device__ __forceinline__ int2 ld_s_i2(const int32_t* p, uint64_t pol) {
-    int2 r;
-    if (PF)
-        asm volatile("ld.global.nc.L1::no_allocate.L2::cache_hint.L2::256B.v2.s32 {%0, %1}, [%2], %3;"
-                     : "=r"(r.x), "=r"(r.y) : "l"(p), "l"(pol));
-    else
-        asm volatile("ld.global.nc.L1::no_allocate.L2::cache_hint.v2.s32 {%0, %1}, [%2], %3;"
-                     : "=r"(r.x), "=r"(r.y) : "l"(p), "l"(pol));
-    return r;
-}
-
-template <bool PF>
-__device__ __forceinline__ double2 ld_s_d2(const double* p, uint64_t pol) {
-    double2 r;
-    if (PF)
-        asm volatile("ld.global.nc.L1::no_allocate.L2::cache_hint.L2::256B.v2.f64 {%0, %1}, [%2], %3;"
-                     : "=d"(r.x), "=d"(r.y) : "l"(p), "l"(pol));
-    else
-        asm volatile("ld.global.nc.L1::no_allocate.L2::cache_hint.v2.f64 {%0, %1}, [%2], %3;"
-                     : "=d"(r.x), "=d"(r.y) : "l"(p), "l"(pol));
-    return r;
-}
-
-template <int W, int RPT, bool PF>
-__global__ void __launch_bounds__(256) ell_kernel_x(EllArgs a) {
-    const uint64_t pol = policy_evict_first();
-    const int64_t s = a.stride;
-    const int lane = threadIdx.x & 31;
-    const int64_t rows_per_unit = RPT == 2 ? 128 : 64;  // rows per warp per iteration
-    const int64_t n_units = ((int64_t)a.n_rows + rows_per_unit - 1) / rows_per_unit;
-    const int64_t wid = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
-    const int64_t nw = ((int64_t)gridDim.x * blockDim.x) >> 5;
-    for (int64_t u = wid; u < n_units; u += nw) {
-        int64_t i0[RPT];
-#pragma unroll
-        for (int q = 0; q < RPT; ++q) i0[q] = u * rows_per_unit + 64 * q + 2 * lane;
-        int2 c[RPT][W];
-        double2 v[RPT][W];
-#pragma unroll
-        for (int q = 0; q < RPT; ++q)
-#pragma unroll
-            for (int j = 0; j < W; ++j)
-                c[q][j] = i0[q] < a.avail ? ld_s_i2<PF>(a.col + j * s + i0[q], pol) : make_int2(-1, -1);
-#pragma unroll
-        for (int q = 0; q < RPT; ++q)
-#pragma unroll
-            for (int j = 0; j < W; ++j)
-                v[q][j] = i0[q] < a.avail ? ld_s_d2<PF>(a.val + j * s + i0[q], pol) : make_double2(0.0, 0.0);
-#pragma unroll
-        for (int q = 0; q < RPT; ++q) {
-            double acc0 = 0.0, acc1 = 0.0;
-#pragma unroll
-            for (int j = 0; j < W; ++j) {
-                const double x0 = c[q][j].x >= 0 ? __ldg(a.x + c[q][j].x) : 0.0;
-                const double x1 = c[q][j].y >= 0 ? __ldg(a.x + c[q][j].y) : 0.0;
-                acc0 = fma(v[q][j].x, x0, acc0);
-                acc1 = fma(v[q][j].y, x1, acc1);
-            }
-            if (i0[q] < a.n_rows) {
-                double* yp = a.y + a.row_off + i0[q];
-                if (i0[q] + 1 < a.n_rows && ((reinterpret_cast<uintptr_t>(yp) & 15) == 0)) {
-                    st_stream_d2(yp, acc0, acc1);
-                } else {
-                    st_stream_d1(yp, acc0);
-                    if (i0[q] + 1 < a.n_rows) st_stream_d1(yp + 1, acc1);
-                }
-            }
-        }
-    }
-}
-
 // ------------------------------------------------------------ tail kernel --
 // The CSR part (Alg. 1 lines 5-7) for the rows that spill.  Rows
 // are regrouped by length inside super-blocks of consecutive tail rows
@@ -298,25 +221,8 @@ static int num_sms() {
     return g_num_sms;
 }
 
-// L2 residency of x: with HEC_X_PERSIST=1 the kernels are launched with an
-// access-policy window marking x "persisting" in L2 (set-aside sized once per
-// process from cudaDevAttrMaxPersistingL2CacheSize), so the matrix streams
-// cannot evict the vector the gathers reuse.  Tuning experiment.
-static int x_persist() {
-    static int v = -1;
-    if (v < 0) {
-        const char* e = std::getenv("HEC_X_PERSIST");
-        v = (e && std::atoi(e) != 0) ? 1 : 0;
-        if (v) {
-            int dev = 0, maxp = 0;
-            cudaGetDevice(&dev);
-            cudaDeviceGetAttribute(&maxp, cudaDevAttrMaxPersistingL2CacheSize, dev);
-            if (maxp <= 0 || cudaDeviceSetLimit(cudaLimitPersistingL2CacheSize, (size_t)maxp) != cudaSuccess) v = 0;
-        }
-    }
-    return v;
-}
-
+// Kernel launch through cudaLaunchKernelEx.  (An L2 persisting access-policy
+// window on x was measured, r09: slower for every config; not used.)
 template <typename... KArgs, typename... Args>
 static cudaError_t launch_k(void (*kernel)(KArgs...), dim3 g, dim3 b, cudaStream_t s, const void* x,
                             size_t x_bytes, Args&&... args) {
@@ -324,23 +230,10 @@ static cudaError_t launch_k(void (*kernel)(KArgs...), dim3 g, dim3 b, cudaStream
     cfg.gridDim = g;
     cfg.blockDim = b;
     cfg.stream = s;
-    cudaLaunchAttribute attr[1];
-    cfg.attrs = attr;
+    cfg.attrs = nullptr;
     cfg.numAttrs = 0;
-    if (x && x_bytes && x_persist()) {
-        int dev = 0, maxw = 0, maxp = 0;
-        cudaGetDevice(&dev);
-        cudaDeviceGetAttribute(&maxw, cudaDevAttrMaxAccessPolicyWindowSize, dev);
-        cudaDeviceGetAttribute(&maxp, cudaDevAttrMaxPersistingL2CacheSize, dev);
-        const size_t nb = x_bytes < (size_t)maxw ? x_bytes : (size_t)maxw;
-        attr[0].id = cudaLaunchAttributeAccessPolicyWindow;
-        attr[0].val.accessPolicyWindow.base_ptr = const_cast<void*>(x);
-        attr[0].val.accessPolicyWindow.num_bytes = nb;
-        attr[0].val.accessPolicyWindow.hitRatio = nb <= (size_t)maxp ? 1.0f : (float)maxp / (float)nb;
-        attr[0].val.accessPolicyWindow.hitProp = cudaAccessPropertyPersisting;
-        attr[0].val.accessPolicyWindow.missProp = cudaAccessPropertyStreaming;
-        cfg.numAttrs = 1;
-    }
+    (void)x;
+    (void)x_bytes;
     return cudaLaunchKernelEx(&cfg, kernel, std::forward<Args>(args)...);
 }
 
@@ -375,33 +268,8 @@ static int ell_variant() {
     return v;
 }
 
-template <int W>
-static cudaError_t launch_ell_x(const EllArgs& a, cudaStream_t s, int rpt, int pf, int block) {
-    const int64_t rows_per_unit = rpt == 2 ? 128 : 64;
-    const int64_t n_units = ((int64_t)a.n_rows + rows_per_unit - 1) / rows_per_unit;
-    int64_t blocks = (n_units * 32 + block - 1) / block;
-    if (blocks < 1) blocks = 1;
-    const dim3 g((unsigned)blocks), b(block);
-    if (rpt == 2) {
-        if (pf) ell_kernel_x<W, 2, true><<<g, b, 0, s>>>(a);
-        else ell_kernel_x<W, 2, false><<<g, b, 0, s>>>(a);
-    } else {
-        if (pf) ell_kernel_x<W, 1, true><<<g, b, 0, s>>>(a);
-        else ell_kernel_x<W, 1, false><<<g, b, 0, s>>>(a);
-    }
-    return cudaGetLastError();
-}
-
 cudaError_t launch_ell(const EllArgs& a, cudaStream_t s) {
     if (a.n_rows <= 0) return cudaSuccess;
-    if (const char* e = std::getenv("HEC_ELL_X")) {
-        int rpt = 1, pf = 0, block = 256;
-        std::sscanf(e, "%d,%d,%d", &rpt, &pf, &block);
-        if (!a.x_halo && !a.rowmap && (block == 128 || block == 256)) {
-            if (a.width == 7) return launch_ell_x<7>(a, s, rpt, pf, block);
-            if (a.width == 9) return launch_ell_x<9>(a, s, rpt, pf, block);
-        }
-    }
     if (ell_variant() == 1) {
         cudaError_t e = launch_ell_tma(a, s, num_sms());
         if (e != cudaErrorNotSupported) return e;
