@@ -82,6 +82,18 @@ __device__ __forceinline__ double ld_stream_d1(const double* ptr, uint64_t pol) 
     return r;
 }
 
+__device__ __forceinline__ int32_t ld_l1_i1(const int32_t* ptr, uint64_t pol) {
+    int32_t r;
+    asm("ld.global.nc.L2::cache_hint.s32 %0, [%1], %2;" : "=r"(r) : "l"(ptr), "l"(pol));
+    return r;
+}
+
+__device__ __forceinline__ double ld_l1_d1(const double* ptr, uint64_t pol) {
+    double r;
+    asm("ld.global.nc.L2::cache_hint.f64 %0, [%1], %2;" : "=d"(r) : "l"(ptr), "l"(pol));
+    return r;
+}
+
 __device__ __forceinline__ void st_stream_d2(double* ptr, double a, double b) {
     asm volatile("st.global.cs.v2.f64 [%0], {%1, %2};" ::"l"(ptr), "d"(a), "d"(b) : "memory");
 }
@@ -191,8 +203,10 @@ __global__ void __launch_bounds__(256) tail_kernel(TailArgs a) {
         }
 #pragma unroll 8
         for (int32_t k = kb + lane; k < ke; k += G) {
-            const int32_t c = ld_stream_i1(a.col + k, pol);
-            const double v = ld_stream_d1(a.val + k, pol);
+            // L1-allocating: the G lanes of a row revisit each 32-byte sector
+            // on consecutive iterations (k += G), which then hit in L1
+            const int32_t c = ld_l1_i1(a.col + k, pol);
+            const double v = ld_l1_d1(a.val + k, pol);
             acc = fma(v, gather_x<HALO>(a.x, a.x_halo, a.n_loc, c), acc);
         }
     }
