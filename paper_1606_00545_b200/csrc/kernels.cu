@@ -256,7 +256,13 @@ static cudaError_t launch_ell_t(const EllArgs& a, cudaStream_t s) {
     const int64_t n_pairs = ((int64_t)a.n_rows + 1) >> 1;
     const int threads = 256;
     int64_t blocks = (n_pairs + threads - 1) / threads;
-    const int64_t cap = (int64_t)num_sms() * 8 * 64;  // grid-stride beyond 64 waves
+    static int64_t blocks_per_sm = -1;  // grid cap = blocks_per_sm * #SMs (grid-stride beyond)
+    if (blocks_per_sm < 0) {
+        const char* e = std::getenv("HEC_ELL_BPS");
+        blocks_per_sm = e ? std::atoi(e) : 8 * 64;
+        if (blocks_per_sm <= 0) blocks_per_sm = 8 * 64;
+    }
+    const int64_t cap = (int64_t)num_sms() * blocks_per_sm;
     if (blocks > cap) blocks = cap;
     if (blocks < 1) blocks = 1;
     const dim3 g((unsigned)blocks), b(threads);
