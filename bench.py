@@ -79,6 +79,21 @@ def ncu_traffic(config: str):
         return None
 
 
+class L2Flusher:
+    """Between timed steps: write a 4x-L2 buffer (evicts everything), then read
+    another one so the dirty lines are written back before the next timed
+    step instead of inside it."""
+
+    def __init__(self, device):
+        import torch
+        self.w = torch.empty(4 * L2_BYTES // 8, dtype=torch.float64, device=device)
+        self.r = torch.zeros(4 * L2_BYTES // 8, dtype=torch.float64, device=device)
+
+    def __call__(self):
+        self.w.zero_()
+        self.r.sum()
+
+
 # -------------------------------------------------------------- clocks ----
 class ClockSampler:
     """Samples SM clocks and throttle reasons via NVML during the timed region."""
@@ -232,7 +247,7 @@ def run_single(args):
     # L2 policy: inputs far larger than L2 need no flush; otherwise write a
     # 4x-L2 scratch buffer before every step, outside that step's event pair
     flush = alg < 4 * L2_BYTES
-    scratch = torch.empty(4 * L2_BYTES // 8, dtype=torch.float64, device=f"cuda:{dev}") if flush else None
+    flusher = L2Flusher(f"cuda:{dev}") if flush else None
     ev = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)) for _ in range(K)]
     sampler = ClockSampler(dev) if not args.profile else None
     torch.cuda.synchronize()
@@ -242,7 +257,7 @@ def run_single(args):
     with torch.cuda.stream(stream):
         for k in range(K):
             if flush:
-                scratch.zero_()
+                flusher()
             ev[k][0].record(stream)
             M.spmv(x, y, stream)
             ev[k][1].record(stream)
@@ -292,7 +307,7 @@ def run_single(args):
                        "ell_width": inf.ell_width, "ell_stride": inf.ell_stride, "tail_rows": inf.tail_rows,
                        "tail_nnz": inf.tail_nnz, "parallelism": "1 GPU",
                        "l2": (f"inputs {alg / 1e9:.2f} GB > 4x {L2_BYTES / 2**20:.0f} MiB L2, no flush" if not flush
-                              else f"L2 flushed ({4 * L2_BYTES / 2**20:.0f} MiB write) before every step, outside the timed pair"),
+                              else f"L2 flushed ({4 * L2_BYTES / 2**20:.0f} MiB write + read) before every step, outside the timed pair"),
                        "checksum": A.checksum(), "setup_s": {"generate": round(t_gen, 2), "convert_upload": round(t_conv, 2)}},
             "gbs": round(alg / (ms_step * 1e-3) / 1e9, 1),
             "roofline": roof, "gpu_launches": K * launches_per_step,
@@ -325,7 +340,7 @@ def run_multi(args):
     stream = torch.cuda.Stream()
     # L2 policy: flush between steps unless this rank's working set is far larger than L2
     flush = D.info.algorithmic_bytes < 4 * L2_BYTES
-    scratch = torch.empty(4 * L2_BYTES // 8, dtype=torch.float64, device="cuda") if flush else None
+    flusher = L2Flusher("cuda") if flush else None
     with torch.cuda.stream(stream):
         for _ in range(args.warmup):
             D.spmv(x, y, stream)
@@ -340,7 +355,7 @@ def run_multi(args):
     with torch.cuda.stream(stream):
         for k in range(K):
             if flush:
-                scratch.zero_()  # outside the timed pair: evicts this rank's matrix from L2
+                flusher()  # outside the timed pair: evicts this rank's matrix from L2
             ev[k][0].record(stream)
             D.spmv(x, y, stream)
             ev[k][1].record(stream)
@@ -398,7 +413,7 @@ def run_multi(args):
                 "scaling": "strong", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
                 "config": {"workload": args.config, "n_rows": A.n_rows, "nnz": A.nnz,
                            "parallelism": f"row partition x{world} ({'GRID slabs' if kind == hec.PART_GRID else 'CONTIG_NNZ'}), NCCL halo exchange",
-                           "l2": ("L2 flushed (512 MiB write) before every step, outside the timed pair" if flush
+                           "l2": ("L2 flushed (504 MiB write + 504 MiB read) before every step, outside the timed pair" if flush
                                   else "per-rank inputs > 4x L2, no flush")},
                 "gbs": round(float(alg_loc.item()) / (ms_step * 1e-3) / 1e9, 1),
                 "roofline": {"bound": "hbm", "achieved": round(achieved, 1), "peak": peak, "unit": "GB/s",

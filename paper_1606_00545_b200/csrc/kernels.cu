@@ -256,13 +256,9 @@ static cudaError_t launch_ell_t(const EllArgs& a, cudaStream_t s) {
     const int64_t n_pairs = ((int64_t)a.n_rows + 1) >> 1;
     const int threads = 256;
     int64_t blocks = (n_pairs + threads - 1) / threads;
-    static int64_t blocks_per_sm = -1;  // grid cap = blocks_per_sm * #SMs (grid-stride beyond)
-    if (blocks_per_sm < 0) {
-        const char* e = std::getenv("HEC_ELL_BPS");
-        blocks_per_sm = e ? std::atoi(e) : 8 * 64;
-        if (blocks_per_sm <= 0) blocks_per_sm = 8 * 64;
-    }
-    const int64_t cap = (int64_t)num_sms() * blocks_per_sm;
+    // one row pair per thread, grid-stride only beyond 64 full waves (a
+    // persistent grid of 5-40 blocks/SM was measured slower, r15)
+    const int64_t cap = (int64_t)num_sms() * 8 * 64;
     if (blocks > cap) blocks = cap;
     if (blocks < 1) blocks = 1;
     const dim3 g((unsigned)blocks), b(threads);
