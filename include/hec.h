@@ -145,6 +145,50 @@ hec_status hec_spmv_host(hec_matrix A, const double* x_host, double* y_host, voi
 /* Number of kernels one hec_spmv launches on this matrix (1 or 2). */
 int32_t hec_spmv_launches(hec_matrix A);
 
+/* Eq. (2) (PAPER §2.3): y = alpha A x + beta y, fused into the
+ * SpMV epilogue (the ELL kernel writes alpha*ell + beta*y_old, the CSR-tail
+ * kernel adds alpha*tail).  beta == 0: y is not read (may hold NaN/garbage).
+ * x, y: device, must not overlap.  Asynchronous on `stream`. */
+hec_status hec_spmv_axpby(hec_matrix A, double alpha, const double* x, double beta, double* y,
+                          void* stream);
+
+/* ------------------------------------------------------ vector operations ---- */
+/* PAPER §2.3 Eqs. (3)-(6), on device vectors of length n
+ * (asynchronous on `stream` unless stated):
+ *   hec_axpby : y = alpha x + beta y   (Eq. 3)
+ *   hec_axpbyz: z = alpha x + beta y   (Eq. 4; z may alias x or y)
+ *   hec_dot   : *result = <x, y>       (Eq. 5; host result, synchronises)
+ *   hec_norm2 : *result = ||x||_2      (Eq. 6; host result, synchronises)
+ * Reductions use a fixed grid and a fixed summation order: deterministic. */
+hec_status hec_axpby(int64_t n, double alpha, const double* x, double beta, double* y, void* stream);
+hec_status hec_axpbyz(int64_t n, double alpha, const double* x, double beta, const double* y, double* z,
+                      void* stream);
+hec_status hec_dot(int64_t n, const double* x, const double* y, double* result, void* stream);
+hec_status hec_norm2(int64_t n, const double* x, double* result, void* stream);
+
+/* ------------------------------------------------------- Krylov solvers ---- */
+/* The consumers of the SpMV in the paper (§2.8): BiCGSTAB exactly as
+ * Alg. 4 with M = I (unpreconditioned; preconditioners are out of scope) and
+ * shadow residual r0 = b - A x0, and CG ("implemented") for SPD A.
+ * b: device rhs; x: device, initial guess on entry, iterate on return.
+ * Stops when ||s||_2 or ||r||_2 <= tol ||r0||_2 (Alg. 4's two tests; CG: ||r||),
+ * after max_it iterations, or on breakdown (rho = 0 -> breakdown = 1;
+ * omega = 0 -> breakdown = 2; (r0, v) = 0, where Alg. 4's alpha is undefined
+ * -> breakdown = 3, reading A20).  Scalars stay on the device; the host reads two
+ * norms per iteration for the tests.  Synchronises `stream` before returning. */
+typedef struct {
+    int32_t iterations;
+    int32_t converged;
+    int32_t breakdown;
+    int32_t reserved;
+    double rel_residual;  /* recurrence ||r_k||_2 / ||r_0||_2 at exit */
+} hec_solve_info;
+
+hec_status hec_bicgstab(hec_matrix A, const double* b, double* x, double tol, int32_t max_it, void* stream,
+                        hec_solve_info* info);
+hec_status hec_cg(hec_matrix A, const double* b, double* x, double tol, int32_t max_it, void* stream,
+                  hec_solve_info* info);
+
 void hec_free(hec_matrix A);
 
 /* ---------------------------------------------------------- partitions ---- */
@@ -253,6 +297,15 @@ typedef struct {
 } hec_dist_info;
 
 hec_status hec_dist_get_info(hec_dist D, hec_dist_info* out);
+
+/* COLLECTIVE distributed solvers: every rank passes its segments of b and x
+ * (n_loc each); SpMVs are hec_spmv_dist and the dot products are all-reduced
+ * with ncclAllReduce over this rank set (replacing the paper's CPU summation
+ * of per-GPU partial results).  Not available on local-emulation handles. */
+hec_status hec_bicgstab_dist(hec_dist D, const double* b_local, double* x_local, double tol, int32_t max_it,
+                             void* stream, hec_solve_info* info);
+hec_status hec_cg_dist(hec_dist D, const double* b_local, double* x_local, double tol, int32_t max_it,
+                       void* stream, hec_solve_info* info);
 void hec_dist_free(hec_dist D);
 
 #ifdef __cplusplus

@@ -198,7 +198,7 @@ hec_status make_matrix(HostHec&& h, int32_t device, cudaStream_t s, const int32_
 // Chunk c of the handle (rows [chunk_row[c], chunk_row[c+1]), r0 a multiple
 // of 512), or all chunks when c < 0: ELL kernel then tail kernel.
 static hec_status launch_chunks(const hec_matrix_s* A, int c, const double* x, const double* x_halo,
-                                double* y, cudaStream_t s) {
+                                double* y, cudaStream_t s, double alpha = 1.0, double beta = 0.0) {
     const int32_t r0 = c < 0 ? 0 : A->chunk_row[c];
     const int32_t r1 = c < 0 ? A->n_rows : A->chunk_row[c + 1];
     EllArgs e;
@@ -214,6 +214,8 @@ static hec_status launch_chunks(const hec_matrix_s* A, int c, const double* x, c
     e.y = A->d_rowmap ? y : y + r0;
     e.rowmap = A->d_rowmap ? A->d_rowmap + r0 : nullptr;
     e.row_off = A->row_off;
+    e.alpha = alpha;
+    e.beta = beta;
     cudaError_t err = launch_ell(e, s);  // Alg. 1 lines 1-3: ELL first
     if (err != cudaSuccess) return cuda_fail(err, "ell_kernel launch");
     const int64_t b0 = c < 0 ? 0 : A->chunk_blk[c];
@@ -231,6 +233,7 @@ static hec_status launch_chunks(const hec_matrix_s* A, int c, const double* x, c
         t.x_halo = x_halo;
         t.n_loc = e.n_loc;
         t.y = y;
+        t.alpha = alpha;
         err = launch_tail(t, s);
         if (err != cudaSuccess) return cuda_fail(err, "tail_kernel launch");
     }
@@ -240,6 +243,11 @@ static hec_status launch_chunks(const hec_matrix_s* A, int c, const double* x, c
 hec_status launch_spmv(const hec_matrix_s* A, const double* x, const double* x_halo, double* y,
                        cudaStream_t s) {
     return launch_chunks(A, -1, x, x_halo, y, s);
+}
+
+hec_status launch_spmv_axpby(const hec_matrix_s* A, double alpha, const double* x, double beta, double* y,
+                             cudaStream_t s) {
+    return launch_chunks(A, -1, x, nullptr, y, s, alpha, beta);
 }
 
 }  // namespace hec
@@ -349,6 +357,14 @@ hec_status hec_spmv(hec_matrix A, const double* x, double* y, void* stream) {
     if (A->n_rows == 0) return HEC_OK;
     DeviceGuard g(A->device);
     return launch_spmv(A, x, nullptr, y, (cudaStream_t)stream);
+}
+
+hec_status hec_spmv_axpby(hec_matrix A, double alpha, const double* x, double beta, double* y, void* stream) {
+    hec_status st = check_xy(A, x, y);
+    if (st != HEC_OK) return st;
+    if (A->n_rows == 0) return HEC_OK;
+    DeviceGuard g(A->device);
+    return launch_spmv_axpby(A, alpha, x, beta, y, (cudaStream_t)stream);
 }
 
 hec_status hec_spmv_host(hec_matrix A, const double* x_host, double* y_host, void* stream) {

@@ -208,25 +208,21 @@ hec_status hec_dist_create_local(const hec_csr* A, hec_plan P, const hec_opts* o
     return HEC_OK;
 }
 
-hec_status hec_spmv_dist(hec_dist D, const double* x_local, double* y_local, void* stream) {
-    if (!D) return fail(HEC_ERR_ARG, "NULL handle");
-    if (D->local) return fail(HEC_ERR_STATE, "local-emulation handle: use hec_spmv_dist_local");
-    const int32_t n_loc = D->r1 - D->r0;
-    if (n_loc > 0 && (!x_local || !y_local)) return fail(HEC_ERR_ARG, "NULL x_local/y_local");
-    if (x_local && y_local && x_local < y_local + n_loc && y_local < x_local + n_loc)
-        return fail(HEC_ERR_ARG, "x_local and y_local overlap");
-    cudaStream_t s = (cudaStream_t)stream;
-    int prev = 0;
-    cudaGetDevice(&prev);
-    if (prev != D->device) cudaSetDevice(D->device);
-    hec_status st = HEC_OK;
+}  // extern "C"
+
+namespace hec {
+
+// The distributed product on `s` (device already current).  The caller's
+// stream waits for the exchange before the boundary rows AND before returning
+// control of `s`, so every later NCCL call issued on `s` (e.g. the Krylov
+// all-reduces) is ordered after this exchange on every rank.
+hec_status dist_spmv_launch(hec_dist_s* D, const double* x_local, double* y_local, cudaStream_t s) {
     const bool ex = has_exchange(D) && D->comm;
     if (ex) {
         // comm stream: pack + grouped send/recv, overlapped with the interior SpMV
-        cudaError_t e = cudaEventRecord(D->ev_start, s);
-        if (e == cudaSuccess) e = cudaStreamWaitEvent(D->comm_stream, D->ev_start, 0);
-        if (e == cudaSuccess) e = launch_pack(D->d_send_idx, D->n_send, x_local, D->d_sendbuf, D->comm_stream);
-        if (e != cudaSuccess) { cudaSetDevice(prev); return cuda_fail(e, "halo pack"); }
+        HEC_CUDA_TRY(cudaEventRecord(D->ev_start, s));
+        HEC_CUDA_TRY(cudaStreamWaitEvent(D->comm_stream, D->ev_start, 0));
+        HEC_CUDA_TRY(launch_pack(D->d_send_idx, D->n_send, x_local, D->d_sendbuf, D->comm_stream));
         ncclResult_t r = ncclGroupStart();
         for (int32_t q = 0; q < D->n_parts && r == ncclSuccess; ++q) {
             const int32_t sc = D->send_off[q + 1] - D->send_off[q];
@@ -236,21 +232,35 @@ hec_status hec_spmv_dist(hec_dist D, const double* x_local, double* y_local, voi
                 r = ncclRecv(D->d_x_halo + D->recv_off[q], rc, ncclDouble, q, D->comm, D->comm_stream);
         }
         ncclResult_t r2 = ncclGroupEnd();
-        if (r != ncclSuccess || r2 != ncclSuccess) {
-            cudaSetDevice(prev);
-            return nccl_fail(r != ncclSuccess ? r : r2, "halo send/recv");
-        }
-        e = cudaEventRecord(D->ev_halo, D->comm_stream);
-        if (e != cudaSuccess) { cudaSetDevice(prev); return cuda_fail(e, "halo event"); }
+        if (r != ncclSuccess || r2 != ncclSuccess) return nccl_fail(r != ncclSuccess ? r : r2, "halo send/recv");
+        HEC_CUDA_TRY(cudaEventRecord(D->ev_halo, D->comm_stream));
     }
-    st = launch_spmv(D->interior, x_local, nullptr, y_local, s);          // interior rows
-    if (st == HEC_OK && D->n_boundary > 0) {
-        if (ex) {
-            cudaError_t e = cudaStreamWaitEvent(s, D->ev_halo, 0);
-            if (e != cudaSuccess) { cudaSetDevice(prev); return cuda_fail(e, "wait halo"); }
-        }
-        st = launch_spmv(D->boundary, x_local, D->d_x_halo, y_local, s);  // boundary rows
-    }
+    hec_status st = launch_spmv(D->interior, x_local, nullptr, y_local, s);  // interior rows
+    if (st != HEC_OK) return st;
+    if (ex) HEC_CUDA_TRY(cudaStreamWaitEvent(s, D->ev_halo, 0));
+    if (D->n_boundary > 0) st = launch_spmv(D->boundary, x_local, D->d_x_halo, y_local, s);  // boundary rows
+    return st;
+}
+
+int64_t dist_n_local(hec_dist_s* D) { return (int64_t)D->r1 - D->r0; }
+
+ncclComm_t dist_comm(hec_dist_s* D) { return D->comm; }
+
+}  // namespace hec
+
+extern "C" {
+
+hec_status hec_spmv_dist(hec_dist D, const double* x_local, double* y_local, void* stream) {
+    if (!D) return fail(HEC_ERR_ARG, "NULL handle");
+    if (D->local) return fail(HEC_ERR_STATE, "local-emulation handle: use hec_spmv_dist_local");
+    const int32_t n_loc = D->r1 - D->r0;
+    if (n_loc > 0 && (!x_local || !y_local)) return fail(HEC_ERR_ARG, "NULL x_local/y_local");
+    if (x_local && y_local && x_local < y_local + n_loc && y_local < x_local + n_loc)
+        return fail(HEC_ERR_ARG, "x_local and y_local overlap");
+    int prev = 0;
+    cudaGetDevice(&prev);
+    if (prev != D->device) cudaSetDevice(D->device);
+    hec_status st = dist_spmv_launch(D, x_local, y_local, (cudaStream_t)stream);
     if (prev != D->device) cudaSetDevice(prev);
     return st;
 }

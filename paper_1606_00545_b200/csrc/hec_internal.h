@@ -146,6 +146,8 @@ hec_status make_matrix(HostHec&& h, int32_t device, cudaStream_t s, const int32_
 // Launch the HEC product (ELL kernel then tail kernel) for one handle.
 hec_status launch_spmv(const hec_matrix_s* A, const double* x, const double* x_halo, double* y,
                        cudaStream_t s);
+hec_status launch_spmv_axpby(const hec_matrix_s* A, double alpha, const double* x, double beta, double* y,
+                             cudaStream_t s);
 }  // namespace hec
 
 // ---------------------------------------------------------------- kernels --
@@ -163,6 +165,7 @@ struct EllArgs {
     double* y;
     const int32_t* rowmap;
     int32_t row_off;
+    double alpha = 1.0, beta = 0.0;  // Eq. (2): y = alpha A x + beta y
 };
 struct TailArgs {
     const int4* blk;            // block descriptors {first, count, lg, 0}
@@ -175,6 +178,7 @@ struct TailArgs {
     const double* x_halo;
     int32_t n_loc;
     double* y;
+    double alpha = 1.0;  // the tail adds alpha * (its part of A x)
 };
 cudaError_t launch_ell(const EllArgs& a, cudaStream_t s);
 cudaError_t launch_tail(const TailArgs& a, cudaStream_t s);

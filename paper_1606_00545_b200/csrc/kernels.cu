@@ -158,16 +158,35 @@ __global__ void __launch_bounds__(256) ell_kernel(EllArgs a) {
                 acc1 = fma(v.y, x1, acc1);
             }
         }
+        // Eq. (2) epilogue y = alpha A x + beta y (alpha = 1, beta = 0 for hec_spmv:
+        // exact, and y is then never read)
+        const bool two = i0 + 1 < a.n_rows;
         if (ROWMAP) {
-            st_stream_d1(a.y + a.rowmap[i0], acc0);
-            if (i0 + 1 < a.n_rows) st_stream_d1(a.y + a.rowmap[i0 + 1], acc1);
+            double* y0 = a.y + a.rowmap[i0];
+            double* y1 = two ? a.y + a.rowmap[i0 + 1] : nullptr;
+            if (a.beta != 0.0) {
+                acc0 = a.alpha * acc0 + a.beta * *y0;
+                if (two) acc1 = a.alpha * acc1 + a.beta * *y1;
+            } else {
+                acc0 *= a.alpha;
+                acc1 *= a.alpha;
+            }
+            st_stream_d1(y0, acc0);
+            if (two) st_stream_d1(y1, acc1);
         } else {
             double* yp = a.y + a.row_off + i0;
-            if (i0 + 1 < a.n_rows && ((reinterpret_cast<uintptr_t>(yp) & 15) == 0)) {
+            if (a.beta != 0.0) {
+                acc0 = a.alpha * acc0 + a.beta * yp[0];
+                if (two) acc1 = a.alpha * acc1 + a.beta * yp[1];
+            } else {
+                acc0 *= a.alpha;
+                acc1 *= a.alpha;
+            }
+            if (two && ((reinterpret_cast<uintptr_t>(yp) & 15) == 0)) {
                 st_stream_d2(yp, acc0, acc1);
             } else {
                 st_stream_d1(yp, acc0);
-                if (i0 + 1 < a.n_rows) st_stream_d1(yp + 1, acc1);
+                if (two) st_stream_d1(yp + 1, acc1);
             }
         }
     }
@@ -211,7 +230,7 @@ __global__ void __launch_bounds__(256) tail_kernel(TailArgs a) {
         }
     }
     for (int off = G >> 1; off > 0; off >>= 1) acc += __shfl_xor_sync(0xffffffffu, acc, off, G);
-    if (lane == 0 && active) *yp = y_old + acc;
+    if (lane == 0 && active) *yp = y_old + a.alpha * acc;
 }
 
 // ------------------------------------------------------------ pack kernel --
@@ -286,7 +305,7 @@ static int ell_variant() {
 
 cudaError_t launch_ell(const EllArgs& a, cudaStream_t s) {
     if (a.n_rows <= 0) return cudaSuccess;
-    if (ell_variant() == 1) {
+    if (ell_variant() == 1 && a.alpha == 1.0 && a.beta == 0.0) {
         cudaError_t e = launch_ell_tma(a, s, num_sms());
         if (e != cudaErrorNotSupported) return e;
         cudaGetLastError();  // clear the sticky-free "not supported" status

@@ -80,7 +80,14 @@ EXPORTED = [
     "hec_plan_export", "hec_plan_part_hec", "hec_plan_free", "hec_nccl_unique_id",
     "hec_dist_create", "hec_dist_create_local", "hec_spmv_dist", "hec_spmv_dist_local",
     "hec_dist_get_info", "hec_dist_free",
+    "hec_spmv_axpby", "hec_axpby", "hec_axpbyz", "hec_dot", "hec_norm2", "hec_bicgstab", "hec_cg",
+    "hec_bicgstab_dist", "hec_cg_dist",
 ]
+
+
+class SolveInfoT(ctypes.Structure):
+    _fields_ = [("iterations", i32), ("converged", i32), ("breakdown", i32), ("reserved", i32),
+                ("rel_residual", dbl)]
 
 
 def lib_path() -> str:
@@ -152,6 +159,19 @@ def load(build: bool = True):
     L.hec_dist_get_info.argtypes = [vp, ctypes.POINTER(DistInfoT)]
     L.hec_dist_free.restype = None
     L.hec_dist_free.argtypes = [vp]
+    L.hec_spmv_axpby.restype = st
+    L.hec_spmv_axpby.argtypes = [vp, dbl, vp, dbl, vp, vp]
+    L.hec_axpby.restype = st
+    L.hec_axpby.argtypes = [i64, dbl, vp, dbl, vp, vp]
+    L.hec_axpbyz.restype = st
+    L.hec_axpbyz.argtypes = [i64, dbl, vp, dbl, vp, vp, vp]
+    L.hec_dot.restype = st
+    L.hec_dot.argtypes = [i64, vp, vp, ctypes.POINTER(dbl), vp]
+    L.hec_norm2.restype = st
+    L.hec_norm2.argtypes = [i64, vp, ctypes.POINTER(dbl), vp]
+    for f in (L.hec_bicgstab, L.hec_cg, L.hec_bicgstab_dist, L.hec_cg_dist):
+        f.restype = st
+        f.argtypes = [vp, vp, vp, dbl, i32, vp, ctypes.POINTER(SolveInfoT)]
     _lib = L
     return L
 
@@ -276,6 +296,26 @@ class Matrix:
         yp = y.data_ptr() if hasattr(y, "data_ptr") else _p(y)
         _check(_lib.hec_spmv_host(self._h, xp, yp, _stream_ptr(stream)))
         return y
+
+    def spmv_axpby(self, alpha: float, x, beta: float, y, stream=None):
+        """Eq. (2): y = alpha A x + beta y on the device."""
+        _check(_lib.hec_spmv_axpby(self._h, float(alpha), _dptr(x, self.n_cols, "x"), float(beta),
+                                   _dptr(y, self.n_rows, "y"), _stream_ptr(stream)))
+        return y
+
+    def bicgstab(self, b, x, tol: float = 1e-8, max_it: int = 1000, stream=None) -> SolveInfoT:
+        """Alg. 4 (unpreconditioned) on the device; x holds x0 on entry."""
+        inf = SolveInfoT()
+        _check(_lib.hec_bicgstab(self._h, _dptr(b, self.n_rows, "b"), _dptr(x, self.n_cols, "x"), float(tol),
+                                 int(max_it), _stream_ptr(stream), ctypes.byref(inf)))
+        return inf
+
+    def cg(self, b, x, tol: float = 1e-8, max_it: int = 1000, stream=None) -> SolveInfoT:
+        """Conjugate gradients (SPD A) on the device; x holds x0 on entry."""
+        inf = SolveInfoT()
+        _check(_lib.hec_cg(self._h, _dptr(b, self.n_rows, "b"), _dptr(x, self.n_cols, "x"), float(tol),
+                           int(max_it), _stream_ptr(stream), ctypes.byref(inf)))
+        return inf
 
     @property
     def launches(self) -> int:
@@ -417,6 +457,18 @@ class Dist:
                                   _dptr(y_local, self.n_loc, "y_local"), _stream_ptr(stream)))
         return y_local
 
+    def bicgstab(self, b_local, x_local, tol: float = 1e-8, max_it: int = 1000, stream=None) -> SolveInfoT:
+        inf = SolveInfoT()
+        _check(_lib.hec_bicgstab_dist(self._h, _dptr(b_local, self.n_loc, "b"), _dptr(x_local, self.n_loc, "x"),
+                                      float(tol), int(max_it), _stream_ptr(stream), ctypes.byref(inf)))
+        return inf
+
+    def cg(self, b_local, x_local, tol: float = 1e-8, max_it: int = 1000, stream=None) -> SolveInfoT:
+        inf = SolveInfoT()
+        _check(_lib.hec_cg_dist(self._h, _dptr(b_local, self.n_loc, "b"), _dptr(x_local, self.n_loc, "x"),
+                                float(tol), int(max_it), _stream_ptr(stream), ctypes.byref(inf)))
+        return inf
+
     def free(self):
         if self._h and self._h.value:
             _lib.hec_dist_free(self._h)
@@ -452,6 +504,40 @@ class LocalDistGroup:
     def free(self):
         for r in self.ranks:
             r.free()
+
+
+def axpby(alpha: float, x, beta: float, y, stream=None):
+    """Eq. (3): y = alpha x + beta y (device vectors)."""
+    load()
+    _check(_lib.hec_axpby(y.numel(), float(alpha), _dptr(x, y.numel(), "x"), float(beta),
+                          _dptr(y, y.numel(), "y"), _stream_ptr(stream)))
+    return y
+
+
+def axpbyz(alpha: float, x, beta: float, y, z, stream=None):
+    """Eq. (4): z = alpha x + beta y (device vectors)."""
+    load()
+    n = z.numel()
+    _check(_lib.hec_axpbyz(n, float(alpha), _dptr(x, n, "x"), float(beta), _dptr(y, n, "y"),
+                           _dptr(z, n, "z"), _stream_ptr(stream)))
+    return z
+
+
+def dot(x, y, stream=None) -> float:
+    """Eq. (5): <x, y> (device vectors, host result)."""
+    load()
+    r = ctypes.c_double()
+    _check(_lib.hec_dot(x.numel(), _dptr(x, x.numel(), "x"), _dptr(y, x.numel(), "y"), ctypes.byref(r),
+                        _stream_ptr(stream)))
+    return r.value
+
+
+def norm2(x, stream=None) -> float:
+    """Eq. (6): ||x||_2 (device vector, host result)."""
+    load()
+    r = ctypes.c_double()
+    _check(_lib.hec_norm2(x.numel(), _dptr(x, x.numel(), "x"), ctypes.byref(r), _stream_ptr(stream)))
+    return r.value
 
 
 def exchange_halo_host(plan: Plan, rank: int, x_local: np.ndarray, group=None) -> np.ndarray:
