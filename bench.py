@@ -45,6 +45,8 @@ def parse():
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--profile", action="store_true", help="short run for ncu (no clocks/e2e/cpu)")
+    ap.add_argument("--solver", choices=["cg", "bicgstab"], default=None,
+                    help="measure Krylov iterations/s instead of the SpMV (NEXT-1)")
     ap.add_argument("--dist", action="store_true",
                     help="use the distributed path (hec_spmv_dist under torchrun) even with one GPU")
     return ap.parse_args()
@@ -430,8 +432,66 @@ def run_multi(args):
     return 0
 
 
+def run_solver(args):
+    """NEXT-1 measurement (not the headline): a fixed number of Krylov
+    iterations (BiCGSTAB = Alg. 4 with M = I, or CG) on the workload, one GPU.
+    Reports iterations/s and the bytes the iteration must move (SpMVs +
+    vector passes) against the HBM peak; the oracle's serial iteration rate on
+    the same matrix (bounded: a few iterations) beside it."""
+    import torch
+    import paper_1606_00545_b200 as hec
+    torch.cuda.set_device(0)
+    A = hecgen.CONFIGS[args.config]()
+    b_h = hecgen.vector(A.n_rows, "uniform", seed=7)
+    M = hec.from_csr(A)
+    b = torch.from_numpy(b_h).cuda()
+    x = torch.zeros(A.n_rows, dtype=torch.float64, device="cuda")
+    solve = M.cg if args.solver == "cg" else M.bicgstab
+    solve(b, x, 0.0, max(1, args.warmup))                      # warm-up iterations
+    torch.cuda.synchronize()
+    K = args.steps
+    x.zero_()
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    e0.record()
+    info = solve(b, x, 0.0, K)                                   # tol 0: exactly K iterations
+    e1.record()
+    torch.cuda.synchronize()
+    ms = e0.elapsed_time(e1)
+    n, alg = A.n_rows, algorithmic_bytes(A.nnz, A.n_rows, A.n_cols)
+    # per iteration: CG = 1 SpMV + dot(p,q) 2n + x,r update 6n + p update 3n (doubles)
+    #                BiCGSTAB = 2 SpMV + p 4n + dot 2n + s 3n + 2 dots 3n + x,r 7n
+    per_it = alg + 8 * n * 11 if args.solver == "cg" else 2 * alg + 8 * n * 19
+    it_s = info.iterations / (ms * 1e-3)
+    peak, peak_src = measured_peak()
+    cpu = None
+    if not args.no_cpu_baseline:
+        from oracle import krylov_ref as KR
+        t0 = time.perf_counter()
+        its = 2
+        (KR.cg if args.solver == "cg" else KR.bicgstab)(A, b_h, np.zeros(n), 0.0, its)
+        dt = time.perf_counter() - t0
+        cpu = {"value": round(its / dt, 4), "unit": "iterations/s", "cores": 1, "kind": "oracle",
+               "sample": f"{its} iterations of oracle/krylov_ref.{args.solver} on {A.name} (serial O1 SpMV, "
+                         f"plain-Python dots), {dt:.1f} s"}
+    line = {"metric": f"fp64 {args.solver} iterations/s (HEC SpMV consumer, NEXT-1)", "value": round(it_s, 2),
+            "unit": "iterations/s", "n_gpus": 1, "steps": info.iterations, "warmup": args.warmup,
+            "ms_per_step": round(ms / max(1, info.iterations), 5), "higher_is_better": True, "scaling": "strong",
+            "vs_baseline": None, "dtype": "f64", "data": "synthetic",
+            "config": {"workload": args.config, "n_rows": n, "nnz": A.nnz, "solver": args.solver,
+                       "tol": 0.0, "rel_residual_at_end": info.rel_residual},
+            "roofline": {"bound": "hbm", "achieved": round(per_it * it_s / 1e9, 1), "peak": peak, "unit": "GB/s",
+                         "frac": round(per_it * it_s / 1e9 / peak, 4), "traffic": None,
+                         "kernel": "whole iteration (SpMV + fused vector passes)",
+                         "algorithmic_bytes_per_iteration": per_it, "peak_source": peak_src},
+            "cpu_baseline": cpu}
+    print(json.dumps(line), flush=True)
+    return 0
+
+
 def main():
     args = parse()
+    if args.solver:
+        return run_solver(args)
     if args.impl == "reference":
         return run_reference(args)
     world = int(os.environ.get("WORLD_SIZE", "1"))
