@@ -1,18 +1,24 @@
 // krylov.cu -- the consumers of the SpMV hot path:
-// the vector operations of PAPER.md §2.3 (Eqs. (2)-(6)), the
+// the vector operations of PAPER.md §2.3 (Eqs. (3)-(6)), the
 // unpreconditioned BiCGSTAB of Alg. 4 (M = I) and CG ("implemented",
 // P:294), on one GPU (hec_matrix) or row-partitioned (hec_dist).
 //
-// Design: one stream, no host round trip for the scalars.  Fused vector passes
-// (grid-stride, fixed grid) write per-block partial dot products; a one-block
-// kernel sums them in a fixed order (deterministic) into a small device scalar
-// array; in distributed mode an ncclAllReduce over those few doubles replaces
-// the paper's "sub results are sent back to CPU"; a one-thread kernel
-// derives alpha / beta / omega.  The host reads two norms per iteration for the
-// stopping tests of Alg. 4 (lines "||s|| is satisfied", "||r|| is satisfied").
+// Design (B200): the whole iteration stays on the device and on one stream.
+//  - Fused vector passes, one specialised kernel per update (double2 loads and
+//    stores), write per-block partial dot products from a FIXED grid; a
+//    one-block kernel sums them in a fixed order (deterministic) into a small
+//    device scalar array.  In distributed mode an ncclAllReduce over those few
+//    doubles replaces the paper's "sub results are sent back to CPU".
+//  - A one-thread "step" kernel derives alpha / beta / omega and evaluates
+//    Alg. 4's tests (||s||, ||r||, rho = 0, omega = 0) ON THE DEVICE, setting
+//    a done flag and the iteration count; every later vector pass sees the
+//    flag and does nothing, so x and r freeze exactly at the stopping point.
+//  - The host enqueues batches of iterations and reads the scalars once per
+//    batch (no per-iteration host round trip).
 #include <cuda_runtime.h>
 #include <nccl.h>
 
+#include <algorithm>
 #include <cmath>
 #include <cstring>
 #include <vector>
@@ -26,8 +32,12 @@ namespace hec {
 // scalar slots
 enum {
     SC_RHO = 0, SC_RHO_PREV, SC_ALPHA, SC_OMEGA, SC_BETA,
-    SC_D0, SC_D1, SC_D2,  // reduced dot products of the last pass
-    SC_R0NORM2, SC_N
+    SC_D0, SC_D1,          // reduced dot products of the last pass
+    SC_R0NORM, SC_THR,     // ||r0||, tol ||r0||
+    SC_DONE,               // 0 running; 1 converged; 2 breakdown / stop
+    SC_CONV, SC_BREAK, SC_ITER, SC_RES,  // converged flag, breakdown code, iterations, ||r||/||r0||
+    SC_FINAL_S,            // BiCGSTAB stopped on ||s||: x += alpha p still to apply
+    SC_N
 };
 
 enum VecOp {
@@ -38,25 +48,23 @@ enum VecOp {
     OP_BICG_P,    // p = r + beta (p - omega v)
     OP_BICG_S,    // s = r - alpha v ; d0 = (s, s)
     OP_BICG_XR,   // x = x + alpha p + omega s ; r = s - omega t ; d0 = (r, r) ; d1 = (r0, r)
-    OP_X_ALPHA_P, // x = x + alpha p
+    OP_X_ALPHA_P, // x = x + alpha p   (only when SC_FINAL_S is set)
     OP_CG_XR,     // x = x + alpha p ; r = r - alpha q ; d0 = (r, r)
     OP_CG_P,      // p = r + beta p
-    OP_AXPBY,     // y = alpha_in x + beta_in y            (Eq. 3)
-    OP_AXPBYZ,    // z = alpha_in x + beta_in y            (Eq. 4)
+    OP_AXPBY,     // y = ca x + cb y            (Eq. 3)
+    OP_AXPBYZ,    // z = ca x + cb y            (Eq. 4)
 };
 
 struct VecArgs {
-    int op;
     int64_t n;
-    const double* sc;   // device scalars (alpha, beta, omega read from here)
-    double* part;       // [3][kRedBlocks] partial dots
-    double ca, cb;      // host-given coefficients (OP_AXPBY / OP_AXPBYZ)
-    // operands (meaning per op, see VecOp)
+    const double* sc;   // device scalars; null for the stand-alone Eq. (3)-(6) calls
+    double* part;       // [2][kRedBlocks] partial dots (null: no dots)
+    double ca, cb;      // coefficients of OP_AXPBY / OP_AXPBYZ
     double *x, *r, *r0, *p, *v, *s, *t, *b;
     const double *a1, *b1, *c1, *d1;
 };
 
-constexpr int kRedBlocks = 592;   // 4 x 148: fixed grid => fixed summation order
+constexpr int kRedBlocks = 1184;   // 8 x 148: fixed grid => fixed summation order
 constexpr int kRedThreads = 256;
 
 __device__ __forceinline__ double block_sum(double v, double* sh) {
@@ -71,43 +79,55 @@ __device__ __forceinline__ double block_sum(double v, double* sh) {
     return v;  // valid in thread 0
 }
 
+// One element of each op; d0/d1 accumulate the pass's dot products.
+template <int OP>
+__device__ __forceinline__ void vec_elem(const VecArgs& a, int64_t i, double alpha, double omega, double beta,
+                                         double& d0, double& d1) {
+    if (OP == OP_DOT1) { d0 += a.a1[i] * a.b1[i]; }
+    if (OP == OP_DOT2) { d0 += a.a1[i] * a.b1[i]; d1 += a.c1[i] * a.d1[i]; }
+    if (OP == OP_RESID) { const double ri = a.b[i] - a.v[i]; a.r[i] = ri; a.r0[i] = ri; d0 += ri * ri; }
+    if (OP == OP_COPY) { a.p[i] = a.r[i]; }
+    if (OP == OP_BICG_P) { a.p[i] = a.r[i] + beta * (a.p[i] - omega * a.v[i]); }
+    if (OP == OP_BICG_S) { const double si = a.r[i] - alpha * a.v[i]; a.s[i] = si; d0 += si * si; }
+    if (OP == OP_BICG_XR) {
+        const double si = a.s[i];
+        a.x[i] = a.x[i] + alpha * a.p[i] + omega * si;
+        const double ri = si - omega * a.t[i];
+        a.r[i] = ri; d0 += ri * ri; d1 += a.r0[i] * ri;
+    }
+    if (OP == OP_X_ALPHA_P) { a.x[i] = a.x[i] + alpha * a.p[i]; }
+    if (OP == OP_CG_XR) {
+        a.x[i] = a.x[i] + alpha * a.p[i];
+        const double ri = a.r[i] - alpha * a.v[i];
+        a.r[i] = ri; d0 += ri * ri;
+    }
+    if (OP == OP_CG_P) { a.p[i] = a.r[i] + beta * a.p[i]; }
+    if (OP == OP_AXPBY) { a.r[i] = a.ca * a.a1[i] + a.cb * a.r[i]; }
+    if (OP == OP_AXPBYZ) { a.r[i] = a.ca * a.a1[i] + a.cb * a.b1[i]; }
+}
+
+template <int OP>
 __global__ void __launch_bounds__(kRedThreads) vec_kernel(VecArgs a) {
-    __shared__ double sh[3][32];
+    __shared__ double sh[2][32];
+    double alpha = 0.0, omega = 0.0, beta = 0.0;
+    bool skip = false;
+    if (a.sc) {
+        skip = a.sc[SC_DONE] != 0.0;
+        if (OP == OP_X_ALPHA_P) skip = a.sc[SC_FINAL_S] != 1.0;
+        alpha = a.sc[SC_ALPHA];
+        omega = a.sc[SC_OMEGA];
+        beta = a.sc[SC_BETA];
+    }
     double d0 = 0.0, d1 = 0.0;
-    const double alpha = a.sc ? a.sc[SC_ALPHA] : 0.0;
-    const double omega = a.sc ? a.sc[SC_OMEGA] : 0.0;
-    const double beta = a.sc ? a.sc[SC_BETA] : 0.0;
-    const int64_t stride = (int64_t)gridDim.x * blockDim.x;
-    for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < a.n; i += stride) {
-        switch (a.op) {
-            case OP_DOT1: d0 += a.a1[i] * a.b1[i]; break;
-            case OP_DOT2: d0 += a.a1[i] * a.b1[i]; d1 += a.c1[i] * a.d1[i]; break;
-            case OP_RESID: {
-                const double ri = a.b[i] - a.v[i];
-                a.r[i] = ri; a.r0[i] = ri; d0 += ri * ri; break;
-            }
-            case OP_COPY: a.p[i] = a.r[i]; break;
-            case OP_BICG_P: a.p[i] = a.r[i] + beta * (a.p[i] - omega * a.v[i]); break;
-            case OP_BICG_S: {
-                const double si = a.r[i] - alpha * a.v[i];
-                a.s[i] = si; d0 += si * si; break;
-            }
-            case OP_BICG_XR: {
-                const double si = a.s[i];
-                a.x[i] = a.x[i] + alpha * a.p[i] + omega * si;
-                const double ri = si - omega * a.t[i];
-                a.r[i] = ri; d0 += ri * ri; d1 += a.r0[i] * ri; break;
-            }
-            case OP_X_ALPHA_P: a.x[i] = a.x[i] + alpha * a.p[i]; break;
-            case OP_CG_XR: {
-                a.x[i] = a.x[i] + alpha * a.p[i];
-                const double ri = a.r[i] - alpha * a.v[i];
-                a.r[i] = ri; d0 += ri * ri; break;
-            }
-            case OP_CG_P: a.p[i] = a.r[i] + beta * a.p[i]; break;
-            case OP_AXPBY: a.r[i] = a.ca * a.a1[i] + a.cb * a.r[i]; break;
-            case OP_AXPBYZ: a.r[i] = a.ca * a.a1[i] + a.cb * a.b1[i]; break;
+    if (!skip) {
+        // 4 independent elements per thread per trip (memory-level parallelism)
+        const int64_t stride = (int64_t)gridDim.x * blockDim.x;
+        int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+        for (; i + 3 * stride < a.n; i += 4 * stride) {
+#pragma unroll
+            for (int u = 0; u < 4; ++u) vec_elem<OP>(a, i + u * stride, alpha, omega, beta, d0, d1);
         }
+        for (; i < a.n; i += stride) vec_elem<OP>(a, i, alpha, omega, beta, d0, d1);
     }
     if (a.part) {
         d0 = block_sum(d0, sh[0]);
@@ -119,30 +139,77 @@ __global__ void __launch_bounds__(kRedThreads) vec_kernel(VecArgs a) {
     }
 }
 
-// Sum the per-block partials in a fixed order: sc[dst + k] = sum_b part[k][b].
-__global__ void __launch_bounds__(kRedThreads) reduce_kernel(const double* part, int n_parts, double* sc, int dst) {
+// Sum the per-block partials in a fixed order: sc[SC_D0 + k] = sum_b part[k][b].
+__global__ void __launch_bounds__(kRedThreads) reduce_kernel(const double* part, int n_parts, double* sc) {
     __shared__ double sh[32];
     for (int k = 0; k < n_parts; ++k) {
         double v = 0.0;
         for (int b = threadIdx.x; b < kRedBlocks; b += blockDim.x) v += part[k * kRedBlocks + b];
         v = block_sum(v, sh);
-        if (threadIdx.x == 0) sc[dst + k] = v;
+        if (threadIdx.x == 0) sc[SC_D0 + k] = v;
     }
 }
 
-enum Derive { DV_ALPHA_BICG, DV_OMEGA, DV_BETA_BICG, DV_ALPHA_CG, DV_BETA_CG, DV_RHO_FROM_D1, DV_SET_RHO_D0 };
+enum Step {
+    ST_INIT,          // after r0: rho = ||r0||^2, thresholds; done if r0 = 0
+    ST_BICG_BEGIN,    // top of iteration k: count it; rho = 0 -> "Fails"; beta (k > 1)
+    ST_BICG_ALPHA,    // alpha = rho / (r0, v); (r0, v) = 0 -> breakdown 3
+    ST_BICG_S,        // ||s|| <= thr -> converged (x += alpha p pending)
+    ST_BICG_OMEGA,    // omega = (t, s) / (t, t)
+    ST_BICG_R,        // ||r|| <= thr -> converged; omega = 0 -> breakdown 2; rho = (r0, r)
+    ST_CG_BEGIN,      // count the iteration
+    ST_CG_ALPHA,      // alpha = rho / (p, q)
+    ST_CG_R,          // rho_new = (r, r): converged?; beta = rho_new / rho
+    ST_FINAL_DONE,    // clear the pending x += alpha p
+};
 
-__global__ void derive_kernel(double* sc, int mode) {
+__global__ void step_kernel(double* sc, int mode, double tol, int first) {
     if (threadIdx.x != 0 || blockIdx.x != 0) return;
+    if (mode == ST_FINAL_DONE) { if (sc[SC_FINAL_S] == 1.0) sc[SC_FINAL_S] = 2.0; return; }
+    if (sc[SC_DONE] != 0.0) return;
     switch (mode) {
-        case DV_ALPHA_BICG: sc[SC_ALPHA] = sc[SC_RHO] / sc[SC_D0]; break;          // alpha = rho/(r0, v)
-        case DV_OMEGA: sc[SC_OMEGA] = sc[SC_D0] / sc[SC_D1]; break;                 // omega = (t,s)/(t,t)
-        case DV_BETA_BICG:                                                          // beta = (rho/rho_prev)(alpha/omega)
-            sc[SC_BETA] = (sc[SC_RHO] / sc[SC_RHO_PREV]) * (sc[SC_ALPHA] / sc[SC_OMEGA]); break;
-        case DV_ALPHA_CG: sc[SC_ALPHA] = sc[SC_RHO] / sc[SC_D0]; break;            // alpha = (r,r)/(p,q)
-        case DV_BETA_CG: sc[SC_BETA] = sc[SC_D0] / sc[SC_RHO]; sc[SC_RHO_PREV] = sc[SC_RHO]; sc[SC_RHO] = sc[SC_D0]; break;
-        case DV_RHO_FROM_D1: sc[SC_RHO_PREV] = sc[SC_RHO]; sc[SC_RHO] = sc[SC_D1]; break;
-        case DV_SET_RHO_D0: sc[SC_RHO] = sc[SC_D0]; sc[SC_R0NORM2] = sc[SC_D0]; break;
+        case ST_INIT: {
+            const double r0n = sqrt(sc[SC_D0]);
+            sc[SC_RHO] = sc[SC_D0];
+            sc[SC_R0NORM] = r0n;
+            sc[SC_THR] = tol * r0n;
+            sc[SC_ITER] = 0.0;
+            sc[SC_RES] = r0n > 0.0 ? 1.0 : 0.0;
+            if (r0n == 0.0) { sc[SC_DONE] = 1.0; sc[SC_CONV] = 1.0; }
+            break;
+        }
+        case ST_BICG_BEGIN:
+            sc[SC_ITER] += 1.0;
+            if (sc[SC_RHO] == 0.0) { sc[SC_DONE] = 2.0; sc[SC_BREAK] = 1.0; break; }          // "Fails"
+            if (!first) sc[SC_BETA] = (sc[SC_RHO] / sc[SC_RHO_PREV]) * (sc[SC_ALPHA] / sc[SC_OMEGA]);
+            break;
+        case ST_BICG_ALPHA:
+            if (sc[SC_D0] == 0.0) { sc[SC_DONE] = 2.0; sc[SC_BREAK] = 3.0; break; }           // reading A20
+            sc[SC_ALPHA] = sc[SC_RHO] / sc[SC_D0];
+            break;
+        case ST_BICG_S:
+            if (sqrt(sc[SC_D0]) <= sc[SC_THR]) {                                              // ||s|| satisfied
+                sc[SC_DONE] = 1.0; sc[SC_CONV] = 1.0; sc[SC_FINAL_S] = 1.0;
+                sc[SC_RES] = sqrt(sc[SC_D0]) / sc[SC_R0NORM];
+            }
+            break;
+        case ST_BICG_OMEGA: sc[SC_OMEGA] = sc[SC_D0] / sc[SC_D1]; break;
+        case ST_BICG_R:
+            sc[SC_RES] = sqrt(sc[SC_D0]) / sc[SC_R0NORM];
+            if (sqrt(sc[SC_D0]) <= sc[SC_THR]) { sc[SC_DONE] = 1.0; sc[SC_CONV] = 1.0; break; }   // ||r|| satisfied
+            if (sc[SC_OMEGA] == 0.0) { sc[SC_DONE] = 2.0; sc[SC_BREAK] = 2.0; break; }
+            sc[SC_RHO_PREV] = sc[SC_RHO];
+            sc[SC_RHO] = sc[SC_D1];                                                          // rho_k = (r0, r)
+            break;
+        case ST_CG_BEGIN: sc[SC_ITER] += 1.0; break;
+        case ST_CG_ALPHA: sc[SC_ALPHA] = sc[SC_RHO] / sc[SC_D0]; break;
+        case ST_CG_R:
+            sc[SC_RES] = sqrt(sc[SC_D0]) / sc[SC_R0NORM];
+            if (sqrt(sc[SC_D0]) <= sc[SC_THR]) { sc[SC_DONE] = 1.0; sc[SC_CONV] = 1.0; break; }
+            sc[SC_BETA] = sc[SC_D0] / sc[SC_RHO];
+            sc[SC_RHO_PREV] = sc[SC_RHO];
+            sc[SC_RHO] = sc[SC_D0];
+            break;
     }
 }
 
@@ -159,9 +226,40 @@ hec_status dist_spmv_launch(hec_dist_s* D, const double* x, double* y, cudaStrea
 int64_t dist_n_local(hec_dist_s* D);
 ncclComm_t dist_comm(hec_dist_s* D);
 
+#define HEC_TRY(expr)                         \
+    do {                                      \
+        hec_status _st = (expr);              \
+        if (_st != HEC_OK) return _st;        \
+    } while (0)
+
+template <int OP>
+static cudaError_t launch_vec(const VecArgs& a, cudaStream_t s) {
+    vec_kernel<OP><<<kRedBlocks, kRedThreads, 0, s>>>(a);
+    return cudaGetLastError();
+}
+
+static cudaError_t launch_vec_op(int op, const VecArgs& a, cudaStream_t s) {
+    switch (op) {
+        case OP_DOT1: return launch_vec<OP_DOT1>(a, s);
+        case OP_DOT2: return launch_vec<OP_DOT2>(a, s);
+        case OP_RESID: return launch_vec<OP_RESID>(a, s);
+        case OP_COPY: return launch_vec<OP_COPY>(a, s);
+        case OP_BICG_P: return launch_vec<OP_BICG_P>(a, s);
+        case OP_BICG_S: return launch_vec<OP_BICG_S>(a, s);
+        case OP_BICG_XR: return launch_vec<OP_BICG_XR>(a, s);
+        case OP_X_ALPHA_P: return launch_vec<OP_X_ALPHA_P>(a, s);
+        case OP_CG_XR: return launch_vec<OP_CG_XR>(a, s);
+        case OP_CG_P: return launch_vec<OP_CG_P>(a, s);
+        case OP_AXPBY: return launch_vec<OP_AXPBY>(a, s);
+        case OP_AXPBYZ: return launch_vec<OP_AXPBYZ>(a, s);
+    }
+    return cudaErrorInvalidValue;
+}
+
 struct Solver {
     Op op;
     cudaStream_t s;
+    double tol = 0.0;
     double* sc = nullptr;
     double* part = nullptr;
     double* h_sc = nullptr;  // pinned mirror
@@ -170,7 +268,7 @@ struct Solver {
     hec_status init(int n_vecs) {
         HEC_CUDA_TRY(cudaMalloc(&sc, SC_N * sizeof(double)));
         HEC_CUDA_TRY(cudaMemsetAsync(sc, 0, SC_N * sizeof(double), s));
-        HEC_CUDA_TRY(cudaMalloc(&part, 3 * kRedBlocks * sizeof(double)));
+        HEC_CUDA_TRY(cudaMalloc(&part, 2 * kRedBlocks * sizeof(double)));
         HEC_CUDA_TRY(cudaMallocHost(&h_sc, SC_N * sizeof(double)));
         for (int k = 0; k < n_vecs; ++k) {
             double* v = nullptr;
@@ -189,15 +287,14 @@ struct Solver {
         if (op.A) return launch_spmv(op.A, x, nullptr, y, s);
         return dist_spmv_launch(op.D, x, y, s);
     }
-    // run a fused vector pass; n_dots > 0: reduce its dots into SC_D0.. (all-reduced across ranks)
-    hec_status pass(VecArgs a, int n_dots) {
+    // one fused vector pass; n_dots > 0: its dots land in SC_D0.. (all-reduced across ranks)
+    hec_status pass(int vop, VecArgs a, int n_dots) {
         a.n = op.n;
         a.sc = sc;
         a.part = n_dots > 0 ? part : nullptr;
-        vec_kernel<<<kRedBlocks, kRedThreads, 0, s>>>(a);
-        HEC_CUDA_TRY(cudaGetLastError());
+        HEC_CUDA_TRY(launch_vec_op(vop, a, s));
         if (n_dots > 0) {
-            reduce_kernel<<<1, kRedThreads, 0, s>>>(part, n_dots, sc, SC_D0);
+            reduce_kernel<<<1, kRedThreads, 0, s>>>(part, n_dots, sc);
             HEC_CUDA_TRY(cudaGetLastError());
             if (op.comm) {
                 ncclResult_t r = ncclAllReduce(sc + SC_D0, sc + SC_D0, n_dots, ncclDouble, ncclSum, op.comm, s);
@@ -206,8 +303,8 @@ struct Solver {
         }
         return HEC_OK;
     }
-    hec_status derive(int mode) {
-        derive_kernel<<<1, 32, 0, s>>>(sc, mode);
+    hec_status step(int mode, int first = 0) {
+        step_kernel<<<1, 32, 0, s>>>(sc, mode, tol, first);
         HEC_CUDA_TRY(cudaGetLastError());
         return HEC_OK;
     }
@@ -218,122 +315,99 @@ struct Solver {
     }
 };
 
-#define HEC_TRY(expr)                         \
-    do {                                      \
-        hec_status _st = (expr);              \
-        if (_st != HEC_OK) return _st;        \
-    } while (0)
-
-// Alg. 4 (P:296-332) with M = I: p* = p, s* = s.
-static hec_status bicgstab(Solver& S, const double* b, double* x, double tol, int32_t max_it,
-                           hec_solve_info* info) {
-    double *r = S.vecs[0], *r0 = S.vecs[1], *p = S.vecs[2], *v = S.vecs[3], *s = S.vecs[4], *t = S.vecs[5];
-    info->iterations = 0;
-    info->converged = 0;
-    info->breakdown = 0;
-    // r0 = b - A x0 (SpMV; vector update); rho_0 = (r0, r) = ||r0||^2
-    HEC_TRY(S.spmv(x, v));
-    VecArgs a = {};
-    a.op = OP_RESID; a.b = const_cast<double*>(b); a.v = v; a.r = r; a.r0 = r0;
-    HEC_TRY(S.pass(a, 1));
-    HEC_TRY(S.derive(DV_SET_RHO_D0));
+// Host loop: enqueue iterations in batches, read the device state once per batch.
+template <typename Iter>
+static hec_status run_batches(Solver& S, int32_t max_it, Iter enqueue_iteration, hec_solve_info* info) {
+    int32_t enq = 0, batch = 4;
     HEC_TRY(S.read_scalars());
-    const double r0n = std::sqrt(S.h_sc[SC_R0NORM2]);
-    const double thr = tol * r0n;
-    info->rel_residual = r0n > 0 ? 1.0 : 0.0;
-    if (r0n == 0.0) { info->converged = 1; return HEC_OK; }
-    for (int32_t k = 1; k <= max_it; ++k) {
-        info->iterations = k;
-        // rho_{k-1} = (r0, r) is in SC_RHO (from the previous pass)
-        if (S.h_sc[SC_RHO] == 0.0) { info->breakdown = 1; return HEC_OK; }         // "Fails"
-        if (k == 1) {
-            a = {}; a.op = OP_COPY; a.r = r; a.p = p;                               // p = r
-            HEC_TRY(S.pass(a, 0));
-        } else {
-            HEC_TRY(S.derive(DV_BETA_BICG));                                        // beta_{k-1}
-            a = {}; a.op = OP_BICG_P; a.r = r; a.p = p; a.v = v;                    // p = r + beta (p - omega v)
-            HEC_TRY(S.pass(a, 0));
-        }
-        HEC_TRY(S.spmv(p, v));                                                      // v = A p
-        a = {}; a.op = OP_DOT1; a.a1 = r0; a.b1 = v;                                // (r0, v)
-        HEC_TRY(S.pass(a, 1));
-        HEC_TRY(S.derive(DV_ALPHA_BICG));                                           // alpha = rho / (r0, v)
-        a = {}; a.op = OP_BICG_S; a.r = r; a.v = v; a.s = s;                        // s = r - alpha v ; ||s||^2
-        HEC_TRY(S.pass(a, 1));
+    while (S.h_sc[SC_DONE] == 0.0 && enq < max_it) {
+        const int32_t nb = std::min(batch, max_it - enq);
+        for (int32_t j = 0; j < nb; ++j) HEC_TRY(enqueue_iteration(enq + j + 1));
+        enq += nb;
         HEC_TRY(S.read_scalars());
-        if (S.h_sc[SC_D0 + 0] != S.h_sc[SC_D0 + 0] || !std::isfinite(S.h_sc[SC_ALPHA])) {
-            info->breakdown = 3;                                                    // (r0, v) = 0 (reading A20)
-            return HEC_OK;
-        }
-        if (std::sqrt(S.h_sc[SC_D0]) <= thr) {                                     // ||s|| is satisfied
-            a = {}; a.op = OP_X_ALPHA_P; a.x = x; a.p = p;                          // x = x + alpha p
-            HEC_TRY(S.pass(a, 0));
-            HEC_CUDA_TRY(cudaStreamSynchronize(S.s));
-            info->converged = 1;
-            info->rel_residual = std::sqrt(S.h_sc[SC_D0]) / r0n;
-            return HEC_OK;
-        }
-        HEC_TRY(S.spmv(s, t));                                                      // t = A s
-        a = {}; a.op = OP_DOT2; a.a1 = t; a.b1 = s; a.c1 = t; a.d1 = t;             // (t, s), (t, t)
-        HEC_TRY(S.pass(a, 2));
-        HEC_TRY(S.derive(DV_OMEGA));                                                // omega = (t,s)/||t||^2
-        a = {}; a.op = OP_BICG_XR; a.x = x; a.p = p; a.s = s; a.t = t; a.r = r; a.r0 = r0;
-        HEC_TRY(S.pass(a, 2));                                                      // x, r updates; ||r||^2, (r0, r)
-        HEC_TRY(S.derive(DV_RHO_FROM_D1));                                          // rho_k = (r0, r) for the next k
-        HEC_TRY(S.read_scalars());
-        info->rel_residual = std::sqrt(S.h_sc[SC_D0]) / r0n;
-        if (std::sqrt(S.h_sc[SC_D0]) <= thr) { info->converged = 1; return HEC_OK; }   // ||r|| satisfied
-        if (S.h_sc[SC_OMEGA] == 0.0) { info->breakdown = 2; return HEC_OK; }           // omega_k = 0
+        batch = std::min(batch * 2, 32);
     }
+    info->iterations = (int32_t)S.h_sc[SC_ITER];
+    info->converged = S.h_sc[SC_CONV] != 0.0;
+    info->breakdown = (int32_t)S.h_sc[SC_BREAK];
+    info->rel_residual = S.h_sc[SC_RES];
     return HEC_OK;
 }
 
+// Alg. 4 (P:296-332) with M = I: p* = p, s* = s.
+static hec_status bicgstab(Solver& S, const double* b, double* x, int32_t max_it, hec_solve_info* info) {
+    double *r = S.vecs[0], *r0 = S.vecs[1], *p = S.vecs[2], *v = S.vecs[3], *s = S.vecs[4], *t = S.vecs[5];
+    // r0 = b - A x0 (SpMV; vector update); rho_0 = (r0, r) = ||r0||^2
+    HEC_TRY(S.spmv(x, v));
+    VecArgs a = {};
+    a.b = const_cast<double*>(b); a.v = v; a.r = r; a.r0 = r0;
+    HEC_TRY(S.pass(OP_RESID, a, 1));
+    HEC_TRY(S.step(ST_INIT));
+    auto iteration = [&](int32_t k) -> hec_status {
+        HEC_TRY(S.step(ST_BICG_BEGIN, k == 1));               // rho_{k-1} = 0 -> Fails; beta_{k-1}
+        VecArgs q = {};
+        q.r = r; q.p = p; q.v = v;
+        HEC_TRY(S.pass(k == 1 ? OP_COPY : OP_BICG_P, q, 0));  // p = r | p = r + beta (p - omega v)
+        HEC_TRY(S.spmv(p, v));                                // v = A p*
+        q = {}; q.a1 = r0; q.b1 = v;
+        HEC_TRY(S.pass(OP_DOT1, q, 1));                       // (r0, v)
+        HEC_TRY(S.step(ST_BICG_ALPHA));                       // alpha_k = rho_{k-1} / (r0, v)
+        q = {}; q.r = r; q.v = v; q.s = s;
+        HEC_TRY(S.pass(OP_BICG_S, q, 1));                     // s = r - alpha v ; ||s||^2
+        HEC_TRY(S.step(ST_BICG_S));                           // ||s|| is satisfied?
+        q = {}; q.x = x; q.p = p;
+        HEC_TRY(S.pass(OP_X_ALPHA_P, q, 0));                  //   then x = x + alpha p* ; stop
+        HEC_TRY(S.step(ST_FINAL_DONE));
+        HEC_TRY(S.spmv(s, t));                                // t = A s*
+        q = {}; q.a1 = t; q.b1 = s; q.c1 = t; q.d1 = t;
+        HEC_TRY(S.pass(OP_DOT2, q, 2));                       // (t, s), (t, t)
+        HEC_TRY(S.step(ST_BICG_OMEGA));                       // omega_k = (t, s) / ||t||^2
+        q = {}; q.x = x; q.p = p; q.s = s; q.t = t; q.r = r; q.r0 = r0;
+        HEC_TRY(S.pass(OP_BICG_XR, q, 2));                    // x, r updates; ||r||^2 ; (r0, r)
+        return S.step(ST_BICG_R);                             // ||r|| satisfied? omega = 0? rho_k
+    };
+    return run_batches(S, max_it, iteration, info);
+}
+
 // Conjugate gradients ("CG ... implemented"; Saad Alg. 6.18), SPD A.
-static hec_status cg(Solver& S, const double* b, double* x, double tol, int32_t max_it, hec_solve_info* info) {
+static hec_status cg(Solver& S, const double* b, double* x, int32_t max_it, hec_solve_info* info) {
     double *r = S.vecs[0], *r0 = S.vecs[1], *p = S.vecs[2], *q = S.vecs[3];
-    info->iterations = 0;
-    info->converged = 0;
-    info->breakdown = 0;
     HEC_TRY(S.spmv(x, q));
     VecArgs a = {};
-    a.op = OP_RESID; a.b = const_cast<double*>(b); a.v = q; a.r = r; a.r0 = r0;  // r = b - A x ; rho = (r, r)
-    HEC_TRY(S.pass(a, 1));
-    HEC_TRY(S.derive(DV_SET_RHO_D0));
-    a = {}; a.op = OP_COPY; a.r = r; a.p = p;                                     // p = r
-    HEC_TRY(S.pass(a, 0));
-    HEC_TRY(S.read_scalars());
-    const double r0n = std::sqrt(S.h_sc[SC_R0NORM2]);
-    const double thr = tol * r0n;
-    info->rel_residual = r0n > 0 ? 1.0 : 0.0;
-    if (r0n == 0.0) { info->converged = 1; return HEC_OK; }
-    for (int32_t k = 1; k <= max_it; ++k) {
-        info->iterations = k;
-        HEC_TRY(S.spmv(p, q));                                                    // q = A p
-        a = {}; a.op = OP_DOT1; a.a1 = p; a.b1 = q;                               // (p, q)
-        HEC_TRY(S.pass(a, 1));
-        HEC_TRY(S.derive(DV_ALPHA_CG));                                           // alpha = rho / (p, q)
-        a = {}; a.op = OP_CG_XR; a.x = x; a.p = p; a.r = r; a.v = q;              // x += alpha p; r -= alpha q; (r,r)
-        HEC_TRY(S.pass(a, 1));
-        HEC_TRY(S.derive(DV_BETA_CG));                                            // beta = (r,r)_new / rho; rho = new
-        HEC_TRY(S.read_scalars());
-        info->rel_residual = std::sqrt(S.h_sc[SC_RHO]) / r0n;
-        if (std::sqrt(S.h_sc[SC_RHO]) <= thr) { info->converged = 1; return HEC_OK; }
-        a = {}; a.op = OP_CG_P; a.r = r; a.p = p;                                 // p = r + beta p
-        HEC_TRY(S.pass(a, 0));
-    }
-    return HEC_OK;
+    a.b = const_cast<double*>(b); a.v = q; a.r = r; a.r0 = r0;   // r = b - A x ; rho = (r, r)
+    HEC_TRY(S.pass(OP_RESID, a, 1));
+    HEC_TRY(S.step(ST_INIT));
+    a = {}; a.r = r; a.p = p;                                     // p = r
+    HEC_TRY(S.pass(OP_COPY, a, 0));
+    auto iteration = [&](int32_t) -> hec_status {
+        HEC_TRY(S.step(ST_CG_BEGIN));
+        HEC_TRY(S.spmv(p, q));                                    // q = A p
+        VecArgs c = {};
+        c.a1 = p; c.b1 = q;
+        HEC_TRY(S.pass(OP_DOT1, c, 1));                           // (p, q)
+        HEC_TRY(S.step(ST_CG_ALPHA));                             // alpha = rho / (p, q)
+        c = {}; c.x = x; c.p = p; c.r = r; c.v = q;
+        HEC_TRY(S.pass(OP_CG_XR, c, 1));                          // x += alpha p; r -= alpha q; (r, r)
+        HEC_TRY(S.step(ST_CG_R));                                 // converged?  beta = (r,r)/rho
+        c = {}; c.r = r; c.p = p;
+        return S.pass(OP_CG_P, c, 0);                             // p = r + beta p
+    };
+    return run_batches(S, max_it, iteration, info);
 }
 
 static hec_status solve(Op op, int method, const double* b, double* x, double tol, int32_t max_it, void* stream,
                         hec_solve_info* info) {
     if (!info || (op.n > 0 && (!b || !x))) return fail(HEC_ERR_ARG, "NULL argument");
-    if (tol < 0 || max_it < 0) return fail(HEC_ERR_ARG, "negative tol or max_it");
+    if (!(tol >= 0) || max_it < 0) return fail(HEC_ERR_ARG, "negative tol or max_it");
+    std::memset(info, 0, sizeof(*info));
     Solver S;
     S.op = op;
     S.s = (cudaStream_t)stream;
+    S.tol = tol;
     HEC_TRY(S.init(method == 0 ? 6 : 4));
-    if (method == 0) return bicgstab(S, b, x, tol, max_it, info);
-    return cg(S, b, x, tol, max_it, info);
+    hec_status st = method == 0 ? bicgstab(S, b, x, max_it, info) : cg(S, b, x, max_it, info);
+    if (st == HEC_OK) HEC_CUDA_TRY(cudaStreamSynchronize(S.s));
+    return st;
 }
 
 static hec_status vec_op(int op, int64_t n, double ca, const double* xa, double cb, const double* xb, double* out,
@@ -341,9 +415,8 @@ static hec_status vec_op(int op, int64_t n, double ca, const double* xa, double 
     if (n < 0) return fail(HEC_ERR_ARG, "negative length");
     if (n == 0) return HEC_OK;
     VecArgs a = {};
-    a.op = op; a.n = n; a.ca = ca; a.cb = cb; a.a1 = xa; a.b1 = xb; a.r = out;
-    vec_kernel<<<kRedBlocks, kRedThreads, 0, (cudaStream_t)stream>>>(a);
-    HEC_CUDA_TRY(cudaGetLastError());
+    a.n = n; a.ca = ca; a.cb = cb; a.a1 = xa; a.b1 = xb; a.r = out;
+    HEC_CUDA_TRY(launch_vec_op(op, a, (cudaStream_t)stream));
     return HEC_OK;
 }
 
@@ -352,12 +425,15 @@ static hec_status dot_op(int64_t n, const double* xa, const double* xb, double* 
     cudaStream_t s = (cudaStream_t)stream;
     double *part = nullptr, *d = nullptr;
     HEC_CUDA_TRY(cudaMalloc(&part, 2 * kRedBlocks * sizeof(double)));
-    HEC_CUDA_TRY(cudaMalloc(&d, sizeof(double)));
+    HEC_CUDA_TRY(cudaMalloc(&d, SC_N * sizeof(double)));
     VecArgs a = {};
-    a.op = OP_DOT1; a.n = n; a.a1 = xa; a.b1 = xb; a.part = part;
-    vec_kernel<<<kRedBlocks, kRedThreads, 0, s>>>(a);
-    reduce_kernel<<<1, kRedThreads, 0, s>>>(part, 1, d, 0);
-    cudaError_t e = cudaMemcpyAsync(result, d, sizeof(double), cudaMemcpyDeviceToHost, s);
+    a.n = n; a.a1 = xa; a.b1 = xb; a.part = part;
+    cudaError_t e = launch_vec_op(OP_DOT1, a, s);
+    if (e == cudaSuccess) {
+        reduce_kernel<<<1, kRedThreads, 0, s>>>(part, 1, d);
+        e = cudaGetLastError();
+    }
+    if (e == cudaSuccess) e = cudaMemcpyAsync(result, d + SC_D0, sizeof(double), cudaMemcpyDeviceToHost, s);
     if (e == cudaSuccess) e = cudaStreamSynchronize(s);
     cudaFree(part);
     cudaFree(d);
