@@ -4,8 +4,8 @@
 // P:294), on one GPU (hec_matrix) or row-partitioned (hec_dist).
 //
 // Design (B200): the whole iteration stays on the device and on one stream.
-//  - Fused vector passes, one specialised kernel per update (double2 loads and
-//    stores), write per-block partial dot products from a FIXED grid; a
+//  - Fused vector passes, one specialised kernel per update (4 independent
+//    elements per thread per trip), write per-block partial dot products from a FIXED grid; a
 //    one-block kernel sums them in a fixed order (deterministic) into a small
 //    device scalar array.  In distributed mode an ncclAllReduce over those few
 //    doubles replaces the paper's "sub results are sent back to CPU".
