@@ -45,6 +45,8 @@ def parse():
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--profile", action="store_true", help="short run for ncu (no clocks/e2e/cpu)")
+    ap.add_argument("--formats", default=None,
+                    help="'all' or comma-separated configs: per-format SpMV table (NEXT-2, Table 3 analog)")
     ap.add_argument("--solver", choices=["cg", "bicgstab"], default=None,
                     help="measure Krylov iterations/s instead of the SpMV (NEXT-1)")
     ap.add_argument("--dist", action="store_true",
@@ -488,8 +490,84 @@ def run_solver(args):
     return 0
 
 
+def run_formats(args):
+    """NEXT-2: the paper's Table 3 experiment (SpMV speedup per format)
+    on B200 with the synthetic workloads: ELL (w = max row length, no
+    remainder), HYB (ELL + COO remainder, Bell & Garland), HEC with the paper's
+    literal boundary 20 (CAP policy), and HEC with the default BG3 width.  The
+    speedup is the paper's: serial CPU time (the oracle O1, one core) / GPU
+    time.  One JSON line per (workload, format); cold L2 below 4x L2."""
+    import torch
+    import oracle
+    import paper_1606_00545_b200 as hec
+    torch.cuda.set_device(0)
+    configs = args.formats.split(",") if args.formats != "all" else \
+        ["poisson2d_64", "spe10", "poisson3d_128", "poisson3d_150", "poisson3d_256", "powerlaw_8M"]
+    flusher = L2Flusher("cuda:0")
+    free_bytes = torch.cuda.mem_get_info()[0]
+    for cfg in configs:
+        A = hecgen.CONFIGS[cfg]()
+        x_h = hecgen.vector(A.n_cols, "uniform", seed=1606)
+        x = torch.from_numpy(x_h).cuda()
+        y = torch.empty(A.n_rows, dtype=torch.float64, device="cuda")
+        alg = algorithmic_bytes(A.nnz, A.n_rows, A.n_cols)
+        # serial CPU time of the same product (the paper's speedup denominator)
+        reps, t_cpu = 0, 0.0
+        while t_cpu < 1.0 and reps < 50:
+            t0 = time.perf_counter()
+            oracle.csr_spmv(A, x_h)
+            t_cpu += time.perf_counter() - t0
+            reps += 1
+        cpu_ms = t_cpu / reps * 1e3
+        max_len = int(np.diff(A.row_ptr).max())
+        variants = [("ELL", hec.opts(hec.WIDTH_CAP, max_len), False),
+                    ("HYB", hec.opts(), True),
+                    ("HEC-20", hec.opts(hec.WIDTH_CAP, 20), False),
+                    ("HEC", hec.opts(), False)]
+        for name, o, hyb in variants:
+            w = min(o.cap, max_len) if o.width_policy == hec.WIDTH_CAP else None
+            need = 12 * (w or 0) * A.n_rows
+            rec = {"metric": "fp64 SpMV GFLOP/s per format (Table 3 analog)", "workload": cfg, "format": name,
+                   "n_rows": A.n_rows, "nnz": A.nnz, "cpu_serial_ms": round(cpu_ms, 3)}
+            if need > 0.8 * free_bytes:
+                rec["skipped"] = f"ELL width {w} needs {need / 1e9:.0f} GB of slots"
+                print(json.dumps(rec), flush=True)
+                continue
+            M = hec.Matrix(A, o, 0, hyb=hyb)
+            cold = alg < 4 * L2_BYTES
+            for _ in range(5):
+                M.spmv(x, y)
+            ev = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)) for _ in range(30)]
+            for a, b in ev:
+                if cold:
+                    flusher()
+                a.record()
+                M.spmv(x, y)
+                b.record()
+            torch.cuda.synchronize()
+            ms = statistics.median(a.elapsed_time(b) for a, b in ev)
+            yv = y.cpu().numpy()
+            r0 = A.n_rows // 3
+            ok = bool(np.all(np.abs(yv[r0:r0 + 2000] - oracle.csr_spmv(A, x_h, r0, min(A.n_rows, r0 + 2000)))
+                             <= oracle.tolerance(A, x_h, r0, min(A.n_rows, r0 + 2000))))
+            inf = M.info
+            rec.update({"gpu_ms": round(ms, 5), "gflops": round(2 * A.nnz / (ms * 1e-3) / 1e9, 2),
+                        "alg_gbs": round(alg / (ms * 1e-3) / 1e9, 1), "speedup_vs_serial": round(cpu_ms / ms, 1),
+                        "ell_width": inf.ell_width, "tail_rows": inf.tail_rows, "tail_nnz": inf.tail_nnz,
+                        "stored_bytes": 12 * inf.ell_width * inf.ell_stride + 12 * inf.tail_nnz +
+                        (4 * inf.tail_nnz if hyb else 8 * inf.tail_rows), "l2": "cold" if cold else "inputs > 4x L2",
+                        "parity_sample_ok": ok})
+            print(json.dumps(rec), flush=True)
+            M.free()
+        del x, y
+        torch.cuda.empty_cache()
+    return 0
+
+
 def main():
     args = parse()
+    if args.formats:
+        return run_formats(args)
     if args.solver:
         return run_solver(args)
     if args.impl == "reference":

@@ -128,6 +128,14 @@ typedef struct {
  * hec_export (conversion checks without a GPU) but not for compute. */
 hec_status hec_from_csr(const hec_csr* A, const hec_opts* o, int32_t device, void* stream,
                         hec_matrix* out);
+/* Comparison variant (the paper's Table 3 formats): the
+ * same ELL part, but the remainder kept in COO as in Bell & Garland's HYB
+ * ("HYB (Hybrid of ELL and COO)") and added with fp64 atomics.  The
+ * product is correct within the usual tolerance but the addition order of a
+ * row's COO pieces is not fixed.  hec_spmv / hec_spmv_axpby / hec_spmv_host
+ * accept the handle; hec_export returns the remainder as CSR.  device >= 0. */
+hec_status hec_from_csr_hyb(const hec_csr* A, const hec_opts* o, int32_t device, void* stream,
+                            hec_matrix* out);
 hec_status hec_info(hec_matrix A, hec_matrix_info* out);
 hec_status hec_export(hec_matrix A, hec_host_arrays* out);
 

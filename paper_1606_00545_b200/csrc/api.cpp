@@ -30,7 +30,7 @@ static void release(hec_matrix_s* m) {
         cudaGetDevice(&cur);
         cudaSetDevice(m->device);
         void* ptrs[] = {m->d_ell_col, m->d_ell_val, m->d_tail_out, m->d_tail_blk,
-                        m->d_tail_ptr, m->d_tail_col, m->d_tail_val, m->d_rowmap, m->d_stage_x,
+                        m->d_tail_ptr, m->d_tail_col, m->d_tail_val, m->d_rowmap, m->d_coo_row, m->d_stage_x,
                         m->d_stage_y};
         for (void* p : ptrs)
             if (p) cudaFree(p);
@@ -129,7 +129,7 @@ static void plan_chunks(hec_matrix_s* m, const HostHec& h, bool pipelined, std::
 }
 
 hec_status make_matrix(HostHec&& h, int32_t device, cudaStream_t s, const int32_t* rowmap,
-                       int32_t n_rowmap, int32_t row_off, int32_t n_loc, hec_matrix* out) {
+                       int32_t n_rowmap, int32_t row_off, int32_t n_loc, hec_matrix* out, bool coo_tail) {
     std::unique_ptr<hec_matrix_s, void (*)(hec_matrix_s*)> m(new (std::nothrow) hec_matrix_s(),
                                                              release);
     if (!m) return fail(HEC_ERR_NOMEM, "host allocation failed");
@@ -155,12 +155,28 @@ hec_status make_matrix(HostHec&& h, int32_t device, cudaStream_t s, const int32_
         return fail(HEC_ERR_NODEV, "no CUDA device available");
     if (device >= n_dev) return fail(HEC_ERR_ARG, "device ordinal out of range");
     DeviceGuard g(device);
+    m->tail_coo = coo_tail;
     std::vector<int32_t> order;
     std::vector<int4> blk;
-    plan_chunks(m.get(), h, n_loc < 0 && !rowmap, &order, &blk);
+    plan_chunks(m.get(), h, n_loc < 0 && !rowmap && !coo_tail, &order, &blk);
     int64_t bytes = 0;
     hec_status st;
     if ((st = dmalloc_copy(&m->d_ell_col, h.ell_col.data(), h.ell_col.size(), s, &bytes))) return st;
+    if (coo_tail) {  // HYB comparison variant: remainder as row-sorted COO triplets
+        std::vector<int32_t> rows(h.tail_col.size());
+        for (size_t t = 0; t < h.tail_rows.size(); ++t)
+            for (int32_t k = h.tail_ptr[t]; k < h.tail_ptr[t + 1]; ++k)
+                rows[k] = rowmap ? rowmap[h.tail_rows[t]] : row_off + h.tail_rows[t];
+        m->h_tail_ptr = h.tail_ptr;
+        if ((st = dmalloc_copy(&m->d_ell_val, h.ell_val.data(), h.ell_val.size(), s, &bytes))) return st;
+        if ((st = dmalloc_copy(&m->d_coo_row, rows.data(), rows.size(), s, &bytes))) return st;
+        if ((st = dmalloc_copy(&m->d_tail_col, h.tail_col.data(), h.tail_col.size(), s, &bytes))) return st;
+        if ((st = dmalloc_copy(&m->d_tail_val, h.tail_val.data(), h.tail_val.size(), s, &bytes))) return st;
+        HEC_CUDA_TRY(cudaStreamSynchronize(s));
+        m->device_bytes = bytes;
+        *out = m.release();
+        return HEC_OK;
+    }
     if ((st = dmalloc_copy(&m->d_ell_val, h.ell_val.data(), h.ell_val.size(), s, &bytes))) return st;
     if (!h.tail_rows.empty()) {
         // Device copy of the CSR tail in the kernel's order (rows regrouped
@@ -218,6 +234,18 @@ static hec_status launch_chunks(const hec_matrix_s* A, int c, const double* x, c
     e.beta = beta;
     cudaError_t err = launch_ell(e, s);  // Alg. 1 lines 1-3: ELL first
     if (err != cudaSuccess) return cuda_fail(err, "ell_kernel launch");
+    if (A->tail_coo) {                   // HYB comparison variant: COO remainder
+        CooArgs k;
+        k.nnz = A->tail_nnz;
+        k.row = A->d_coo_row;
+        k.col = A->d_tail_col;
+        k.val = A->d_tail_val;
+        k.x = x;
+        k.y = y;
+        k.alpha = alpha;
+        err = launch_coo(k, s);
+        return err == cudaSuccess ? HEC_OK : cuda_fail(err, "coo_kernel launch");
+    }
     const int64_t b0 = c < 0 ? 0 : A->chunk_blk[c];
     const int64_t b1 = c < 0 ? A->chunk_blk[A->n_chunks] : A->chunk_blk[c + 1];
     if (A->tail_rows > 0 && b1 > b0) {  // Alg. 1 lines 5-7: then the CSR part
@@ -276,6 +304,26 @@ hec_status hec_from_csr(const hec_csr* A, const hec_opts* o, int32_t device, voi
     return make_matrix(std::move(h), device, (cudaStream_t)stream, nullptr, 0, 0, -1, out);
 }
 
+hec_status hec_from_csr_hyb(const hec_csr* A, const hec_opts* o, int32_t device, void* stream,
+                            hec_matrix* out) {
+    if (!out) return fail(HEC_ERR_ARG, "NULL out");
+    *out = nullptr;
+    if (device < 0) return fail(HEC_ERR_NODEV, "the HYB comparison variant is device-only");
+    CsrView v;
+    hec_status st = validate_csr(A, &v);
+    if (st != HEC_OK) return st;
+    const hec_opts op = normalise_opts(o);
+    if ((st = check_opts(op)) != HEC_OK) return st;
+    HostHec h;
+    try {
+        st = convert(v, choose_width(v, op), op.stride_unit, &h);
+    } catch (...) {
+        return fail(HEC_ERR_NOMEM, "host allocation failed in hec_from_csr_hyb");
+    }
+    if (st != HEC_OK) return st;
+    return make_matrix(std::move(h), device, (cudaStream_t)stream, nullptr, 0, 0, -1, out, true);
+}
+
 hec_status hec_info(hec_matrix A, hec_matrix_info* o) {
     if (!A || !o) return fail(HEC_ERR_ARG, "NULL argument");
     o->n_rows = A->n_rows;
@@ -312,6 +360,12 @@ hec_status hec_export(hec_matrix A, hec_host_arrays* o) {
     if (o->ell_val && slots) HEC_CUDA_TRY(cudaMemcpy(o->ell_val, A->d_ell_val, slots * sizeof(double), cudaMemcpyDeviceToHost));
     if (!A->tail_rows) {
         if (o->tail_ptr) o->tail_ptr[0] = 0;
+        return HEC_OK;
+    }
+    if (A->tail_coo) {  // HYB: remainder kept in the original (row-sorted) order
+        if (o->tail_ptr) std::memcpy(o->tail_ptr, A->h_tail_ptr.data(), A->h_tail_ptr.size() * sizeof(int32_t));
+        if (o->tail_col) HEC_CUDA_TRY(cudaMemcpy(o->tail_col, A->d_tail_col, A->tail_nnz * sizeof(int32_t), cudaMemcpyDeviceToHost));
+        if (o->tail_val) HEC_CUDA_TRY(cudaMemcpy(o->tail_val, A->d_tail_val, A->tail_nnz * sizeof(double), cudaMemcpyDeviceToHost));
         return HEC_OK;
     }
     // the device tail is stored in kernel order (see make_matrix): undo it

@@ -110,6 +110,9 @@ struct hec_matrix_s {
     int32_t n_rows = 0, n_cols = 0, width = 0, stride = 0;
     int64_t nnz = 0, ell_nnz = 0, tail_nnz = 0;
     int32_t tail_rows = 0;
+    bool tail_coo = false;             // HYB comparison variant: the remainder in COO
+    int32_t* d_coo_row = nullptr;      // HYB: output row of every remainder entry
+    std::vector<int32_t> h_tail_ptr;   // HYB: tail_ptr kept on the host for hec_export
     hec::HostHec host;                 // full copy only for host-only handles
     std::vector<int32_t> h_tail_rows;  // local tail row ids (always kept; small)
     // device arrays
@@ -142,7 +145,8 @@ struct hec_matrix_s {
 namespace hec {
 // Build a device (or host-only) matrix handle from a host HEC.
 hec_status make_matrix(HostHec&& h, int32_t device, cudaStream_t s, const int32_t* rowmap,
-                       int32_t n_rowmap, int32_t row_off, int32_t n_loc, hec_matrix* out);
+                       int32_t n_rowmap, int32_t row_off, int32_t n_loc, hec_matrix* out,
+                       bool coo_tail = false);
 // Launch the HEC product (ELL kernel then tail kernel) for one handle.
 hec_status launch_spmv(const hec_matrix_s* A, const double* x, const double* x_halo, double* y,
                        cudaStream_t s);
@@ -180,6 +184,16 @@ struct TailArgs {
     double* y;
     double alpha = 1.0;  // the tail adds alpha * (its part of A x)
 };
+struct CooArgs {               // HYB remainder: row-sorted (row, col, val) triplets
+    int64_t nnz;
+    const int32_t* row;        // output rows
+    const int32_t* col;
+    const double* val;
+    const double* x;
+    double* y;
+    double alpha;
+};
+cudaError_t launch_coo(const CooArgs& a, cudaStream_t s);
 cudaError_t launch_ell(const EllArgs& a, cudaStream_t s);
 cudaError_t launch_tail(const TailArgs& a, cudaStream_t s);
 cudaError_t launch_ell_tma(const EllArgs& a, cudaStream_t s, int num_sms);

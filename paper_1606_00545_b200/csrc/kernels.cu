@@ -233,6 +233,68 @@ __global__ void __launch_bounds__(256) tail_kernel(TailArgs a) {
     if (lane == 0 && active) *yp = y_old + a.alpha * acc;
 }
 
+// ------------------------------------------------------- HYB: COO kernel --
+// Comparison variant: the Bell-Garland HYB remainder in
+// COO instead of CSR.  Lane l of a warp owns 8 consecutive row-sorted
+// entries (vector loads), sums each run of equal rows, and adds every run into
+// y with an fp64 atomic (rows may span lanes and warps; the addition order of
+// those partial sums is not fixed -- parity is within tolerance, exact only in
+// the integer regime).
+__global__ void __launch_bounds__(256) coo_kernel(CooArgs a) {
+    const int64_t k0 = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) * 8;
+    if (k0 >= a.nnz) return;
+    const int n = a.nnz - k0 < 8 ? (int)(a.nnz - k0) : 8;
+    int32_t row[8], col[8];
+    double val[8];
+    if (n == 8) {  // k0 is a multiple of 8: 32-byte aligned int4 / double2 loads
+        const int4 r0 = __ldg(reinterpret_cast<const int4*>(a.row + k0));
+        const int4 r1 = __ldg(reinterpret_cast<const int4*>(a.row + k0) + 1);
+        const int4 c0 = __ldg(reinterpret_cast<const int4*>(a.col + k0));
+        const int4 c1 = __ldg(reinterpret_cast<const int4*>(a.col + k0) + 1);
+        row[0] = r0.x; row[1] = r0.y; row[2] = r0.z; row[3] = r0.w;
+        row[4] = r1.x; row[5] = r1.y; row[6] = r1.z; row[7] = r1.w;
+        col[0] = c0.x; col[1] = c0.y; col[2] = c0.z; col[3] = c0.w;
+        col[4] = c1.x; col[5] = c1.y; col[6] = c1.z; col[7] = c1.w;
+#pragma unroll
+        for (int j = 0; j < 4; ++j) {
+            const double2 v = __ldg(reinterpret_cast<const double2*>(a.val + k0) + j);
+            val[2 * j] = v.x;
+            val[2 * j + 1] = v.y;
+        }
+    } else {
+        for (int j = 0; j < 8; ++j) {
+            row[j] = j < n ? __ldg(a.row + k0 + j) : -1;
+            col[j] = j < n ? __ldg(a.col + k0 + j) : 0;
+            val[j] = j < n ? __ldg(a.val + k0 + j) : 0.0;
+        }
+    }
+    double xg[8];
+#pragma unroll
+    for (int j = 0; j < 8; ++j) xg[j] = j < n ? __ldg(a.x + col[j]) : 0.0;
+    double acc = 0.0;
+    int32_t cur = row[0];
+#pragma unroll
+    for (int j = 0; j < 8; ++j) {
+        if (j < n) {
+            if (row[j] != cur) {
+                atomicAdd(a.y + cur, a.alpha * acc);
+                acc = 0.0;
+                cur = row[j];
+            }
+            acc = fma(val[j], xg[j], acc);
+        }
+    }
+    atomicAdd(a.y + cur, a.alpha * acc);
+}
+
+cudaError_t launch_coo(const CooArgs& a, cudaStream_t s) {
+    if (a.nnz <= 0) return cudaSuccess;
+    const int64_t threads = (a.nnz + 7) / 8;
+    const int64_t blocks = (threads + 255) / 256;
+    coo_kernel<<<(unsigned)blocks, 256, 0, s>>>(a);
+    return cudaGetLastError();
+}
+
 // ------------------------------------------------------------ pack kernel --
 __global__ void __launch_bounds__(256) pack_kernel(const int32_t* __restrict__ idx, int32_t n,
                                                    const double* __restrict__ x,

@@ -81,7 +81,7 @@ EXPORTED = [
     "hec_dist_create", "hec_dist_create_local", "hec_spmv_dist", "hec_spmv_dist_local",
     "hec_dist_get_info", "hec_dist_free",
     "hec_spmv_axpby", "hec_axpby", "hec_axpbyz", "hec_dot", "hec_norm2", "hec_bicgstab", "hec_cg",
-    "hec_bicgstab_dist", "hec_cg_dist",
+    "hec_bicgstab_dist", "hec_cg_dist", "hec_from_csr_hyb",
 ]
 
 
@@ -113,8 +113,9 @@ def load(build: bool = True):
     L.hec_version.restype = ctypes.c_char_p
     L.hec_opts_default.restype = None
     L.hec_opts_default.argtypes = [ctypes.POINTER(OptsT)]
-    L.hec_from_csr.restype = st
-    L.hec_from_csr.argtypes = [ctypes.POINTER(CsrT), ctypes.POINTER(OptsT), i32, vp, ctypes.POINTER(vp)]
+    for f in (L.hec_from_csr, L.hec_from_csr_hyb):
+        f.restype = st
+        f.argtypes = [ctypes.POINTER(CsrT), ctypes.POINTER(OptsT), i32, vp, ctypes.POINTER(vp)]
     L.hec_info.restype = st
     L.hec_info.argtypes = [vp, ctypes.POINTER(MatrixInfoT)]
     L.hec_export.restype = st
@@ -242,7 +243,7 @@ class Matrix:
     (for conversion checks without a GPU; compute refuses it)."""
 
     def __init__(self, A=None, options: OptsT | None = None, device: int = 0, stream=None,
-                 _handle: int | None = None):
+                 _handle: int | None = None, hyb: bool = False):
         L = load()
         self._h = vp()
         if _handle is not None:
@@ -251,7 +252,8 @@ class Matrix:
             args = _CsrArgs(A)
             o = options if options is not None else opts()
             s = _stream_ptr(stream) if device >= 0 else 0
-            _check(L.hec_from_csr(args.ref(), ctypes.byref(o), device, s, ctypes.byref(self._h)))
+            make = L.hec_from_csr_hyb if hyb else L.hec_from_csr
+            _check(make(args.ref(), ctypes.byref(o), device, s, ctypes.byref(self._h)))
         self.info = self._info()
 
     def _info(self) -> MatrixInfoT:
@@ -335,6 +337,11 @@ class Matrix:
 
 def from_csr(A, options: OptsT | None = None, device: int = 0, stream=None) -> Matrix:
     return Matrix(A, options, device, stream)
+
+
+def from_csr_hyb(A, options: OptsT | None = None, device: int = 0, stream=None) -> Matrix:
+    """ELL + COO (Bell-Garland HYB) comparison variant (NEXT-2)."""
+    return Matrix(A, options, device, stream, hyb=True)
 
 
 # -------------------------------------------------------------------- plan --

@@ -226,3 +226,31 @@ def test_aliasing_rejected_and_stream_order():
     s.synchronize()
     ref = oracle.csr_spmv(A, 2.0 * np.ones(256)) + 1.0
     assert y.cpu().numpy().tobytes() == ref.tobytes()
+
+
+@pytest.mark.parametrize("maker", [lambda: hecgen.powerlaw(1 << 16, seed=8), lambda: hecgen.spe10(60, 220, 85),
+                                   lambda: hecgen.random_csr(500, 300, 0.05, seed=4)])
+def test_hyb_comparison_variant_parity(maker):
+    # NEXT-2: ELL + COO remainder (Bell-Garland HYB).  Atomic order is not fixed:
+    # parity within tolerance; bitwise only on integer data.
+    A = maker()
+    x = hecgen.vector(A.n_cols, "uniform", seed=5)
+    M = hec.from_csr_hyb(A)
+    y, _ = gpu_spmv(A, x, M=M)
+    assert_parity(A, x, y)
+    e, r = M.export(), hec.from_csr(A, device=-1).export()
+    for f in ("ell_col", "ell_val", "tail_rows", "tail_ptr", "tail_col", "tail_val"):
+        assert getattr(e, f).tobytes() == getattr(r, f).tobytes()
+
+
+def test_hyb_integer_bitwise_and_axpby():
+    A = hecgen.powerlaw(1 << 15, integer_values=True, seed=9)
+    x = hecgen.vector(A.n_cols, "int", seed=3)
+    M = hec.from_csr_hyb(A)
+    y, _ = gpu_spmv(A, x, M=M)
+    assert y.tobytes() == oracle.csr_spmv(A, x).tobytes()
+    y0 = hecgen.vector(A.n_rows, "int", seed=4)
+    yd = torch.from_numpy(y0.copy()).cuda()
+    M.spmv_axpby(2.0, torch.from_numpy(x).cuda(), -1.0, yd)
+    torch.cuda.synchronize()
+    assert yd.cpu().numpy().tobytes() == (2.0 * oracle.csr_spmv(A, x) - y0).tobytes()
