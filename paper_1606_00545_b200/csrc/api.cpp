@@ -30,8 +30,7 @@ static void release(hec_matrix_s* m) {
         cudaGetDevice(&cur);
         cudaSetDevice(m->device);
         void* ptrs[] = {m->d_ell_col, m->d_ell_val, m->d_tail_out, m->d_tail_blk,
-                        m->d_tail_ptr, m->d_tail_col, m->d_tail_val, m->d_rowmap, m->d_coo_row,
-                        m->d_grow, m->d_gk0, m->d_carry, m->d_headsum, m->d_stage_x,
+                        m->d_tail_ptr, m->d_tail_col, m->d_tail_val, m->d_rowmap, m->d_coo_row, m->d_stage_x,
                         m->d_stage_y};
         for (void* p : ptrs)
             if (p) cudaFree(p);
@@ -179,40 +178,7 @@ hec_status make_matrix(HostHec&& h, int32_t device, cudaStream_t s, const int32_
         return HEC_OK;
     }
     if ((st = dmalloc_copy(&m->d_ell_val, h.ell_val.data(), h.ell_val.size(), s, &bytes))) return st;
-    const char* tail_env = std::getenv("HEC_TAIL");
-    m->tail_grouped = !h.tail_rows.empty() && tail_env && std::strcmp(tail_env, "group") == 0;
-    if (m->tail_grouped) {
-        // Grouped CSR tail: original row order; groups of 8 consecutive entries
-        // restarting at every chunk's first tail entry (rows never cross chunks).
-        const int32_t tr = (int32_t)h.tail_rows.size();
-        const int32_t* tp = h.tail_ptr.data();
-        std::vector<int32_t> grow, gk0, tout(tr);
-        m->chunk_grp.assign(m->n_chunks + 1, 0);
-        int32_t t0 = 0;
-        for (int c = 0; c < m->n_chunks; ++c) {
-            int32_t t1 = t0;
-            while (t1 < tr && h.tail_rows[t1] < m->chunk_row[c + 1]) ++t1;
-            for (int32_t k = tp[t0]; k < tp[t1]; k += 8) {
-                gk0.push_back(k);
-                grow.push_back((int32_t)(std::upper_bound(tp + t0, tp + t1 + 1, k) - tp) - 1);
-            }
-            m->chunk_grp[c + 1] = (int64_t)gk0.size();
-            t0 = t1;
-        }
-        gk0.push_back(tp[tr]);
-        for (int32_t t = 0; t < tr; ++t) tout[t] = rowmap ? rowmap[h.tail_rows[t]] : row_off + h.tail_rows[t];
-        const size_t G = grow.size();
-        if ((st = dmalloc_copy(&m->d_tail_out, tout.data(), tout.size(), s, &bytes))) return st;
-        if ((st = dmalloc_copy(&m->d_grow, grow.data(), G, s, &bytes))) return st;
-        if ((st = dmalloc_copy(&m->d_gk0, gk0.data(), gk0.size(), s, &bytes))) return st;
-        if ((st = dmalloc_copy(&m->d_carry, (const double*)nullptr, G, s, &bytes))) return st;
-        if ((st = dmalloc_copy(&m->d_headsum, (const double*)nullptr, G, s, &bytes))) return st;
-        if ((st = dmalloc_copy(&m->d_tail_ptr, h.tail_ptr.data(), h.tail_ptr.size(), s, &bytes))) return st;
-        if ((st = dmalloc_copy(&m->d_tail_col, h.tail_col.data(), h.tail_col.size(), s, &bytes))) return st;
-        if ((st = dmalloc_copy(&m->d_tail_val, h.tail_val.data(), h.tail_val.size(), s, &bytes))) return st;
-        m->h_tail_ptr = h.tail_ptr;
-        HEC_CUDA_TRY(cudaStreamSynchronize(s));
-    } else if (!h.tail_rows.empty()) {
+    if (!h.tail_rows.empty()) {
         // Device copy of the CSR tail in the kernel's order (rows regrouped
         // inside super-blocks, plan_chunks): a block's rows and their entries
         // are contiguous, and the kernel needs no indirection.  hec_export
@@ -279,27 +245,6 @@ static hec_status launch_chunks(const hec_matrix_s* A, int c, const double* x, c
         k.alpha = alpha;
         err = launch_coo(k, s);
         return err == cudaSuccess ? HEC_OK : cuda_fail(err, "coo_kernel launch");
-    }
-    if (A->tail_grouped) {               // grouped CSR tail (+ deterministic fix-up)
-        TailGrpArgs t;
-        t.g_begin = c < 0 ? 0 : A->chunk_grp[c];
-        t.g_end = c < 0 ? A->chunk_grp[A->n_chunks] : A->chunk_grp[c + 1];
-        t.grow = A->d_grow;
-        t.gk0 = A->d_gk0;
-        t.ptr = A->d_tail_ptr;
-        t.n_tail = A->tail_rows;
-        t.col = A->d_tail_col;
-        t.val = A->d_tail_val;
-        t.out_rows = A->d_tail_out;
-        t.x = x;
-        t.x_halo = x_halo;
-        t.n_loc = e.n_loc;
-        t.y = y;
-        t.carry = A->d_carry;
-        t.headsum = A->d_headsum;
-        t.alpha = alpha;
-        err = launch_tail_grouped(t, s);
-        return err == cudaSuccess ? HEC_OK : cuda_fail(err, "tail_group_kernel launch");
     }
     const int64_t b0 = c < 0 ? 0 : A->chunk_blk[c];
     const int64_t b1 = c < 0 ? A->chunk_blk[A->n_chunks] : A->chunk_blk[c + 1];
@@ -417,7 +362,7 @@ hec_status hec_export(hec_matrix A, hec_host_arrays* o) {
         if (o->tail_ptr) o->tail_ptr[0] = 0;
         return HEC_OK;
     }
-    if (A->tail_coo || A->tail_grouped) {  // remainder kept in the original (row-sorted) order
+    if (A->tail_coo) {  // HYB: remainder kept in the original (row-sorted) order
         if (o->tail_ptr) std::memcpy(o->tail_ptr, A->h_tail_ptr.data(), A->h_tail_ptr.size() * sizeof(int32_t));
         if (o->tail_col) HEC_CUDA_TRY(cudaMemcpy(o->tail_col, A->d_tail_col, A->tail_nnz * sizeof(int32_t), cudaMemcpyDeviceToHost));
         if (o->tail_val) HEC_CUDA_TRY(cudaMemcpy(o->tail_val, A->d_tail_val, A->tail_nnz * sizeof(double), cudaMemcpyDeviceToHost));
@@ -559,7 +504,7 @@ hec_status hec_spmv_host(hec_matrix A, const double* x_host, double* y_host, voi
 
 int32_t hec_spmv_launches(hec_matrix A) {
     if (!A || A->n_rows == 0) return 0;
-    return 1 + (A->tail_rows > 0 ? (A->tail_grouped ? 2 : 1) : 0);
+    return 1 + (A->tail_rows > 0 ? 1 : 0);
 }
 
 void hec_free(hec_matrix A) { release(A); }

@@ -136,13 +136,6 @@ struct hec_matrix_s {
     std::vector<int32_t> chunk_row;    // [n_chunks+1], multiples of 512
     std::vector<int32_t> chunk_xend;   // [n_chunks]: x[0 : xend) needed by rows < chunk_row[c+1]
     std::vector<int64_t> chunk_blk;    // [n_chunks+1]: tail-kernel blocks of each chunk
-    // grouped CSR tail (tail entries in original order, 8-entry groups)
-    bool tail_grouped = false;
-    int32_t* d_grow = nullptr;         // [G]: tail row containing each group's first entry
-    int32_t* d_gk0 = nullptr;          // [G+1]: first entry of each group (+ terminal)
-    double* d_carry = nullptr;         // [G]: partial of the row left open at the group's end
-    double* d_headsum = nullptr;       // [G]: partial of a spanning row that ends in the group
-    std::vector<int64_t> chunk_grp;    // [n_chunks+1]: groups of each chunk
     cudaStream_t s_h2d = nullptr, s_d2h = nullptr;
     std::vector<cudaEvent_t> ev_x, ev_y;
     cudaEvent_t ev_start = nullptr;
@@ -201,24 +194,6 @@ struct CooArgs {               // HYB remainder: row-sorted (row, col, val) trip
     double alpha;
 };
 cudaError_t launch_coo(const CooArgs& a, cudaStream_t s);
-struct TailGrpArgs {           // grouped CSR tail: thread = 8 consecutive tail entries
-    int64_t g_begin, g_end;
-    const int32_t* grow;
-    const int32_t* gk0;
-    const int32_t* ptr;        // tail_ptr (original order)
-    int32_t n_tail;            // tail rows
-    const int32_t* col;
-    const double* val;
-    const int32_t* out_rows;   // output row of each tail row
-    const double* x;
-    const double* x_halo;
-    int32_t n_loc;
-    double* y;
-    double* carry;
-    double* headsum;
-    double alpha;
-};
-cudaError_t launch_tail_grouped(const TailGrpArgs& a, cudaStream_t s);
 cudaError_t launch_ell(const EllArgs& a, cudaStream_t s);
 cudaError_t launch_tail(const TailArgs& a, cudaStream_t s);
 cudaError_t launch_ell_tma(const EllArgs& a, cudaStream_t s, int num_sms);

@@ -233,106 +233,6 @@ __global__ void __launch_bounds__(256) tail_kernel(TailArgs a) {
     if (lane == 0 && active) *yp = y_old + a.alpha * acc;
 }
 
-// ------------------------------------------------- grouped CSR-tail kernel --
-// The CSR remainder (Alg. 1 lines 5-7) with the tail in its original row
-// order, cut into groups of 8 consecutive entries: one thread per group reads
-// its entries with vector loads (when 8-aligned), keeps 8 x gathers in flight,
-// and walks them against the prefetched ends of the (at most 8) rows they
-// touch.  A row that starts and ends inside the group is added into y by this
-// thread alone.  A row spanning groups leaves partial sums: `carry[g]` (the
-// row open at the group's end) and `headsum[g]` (its last piece, in the group
-// where it ends); tail_fix_kernel then adds headsum + carries of the earlier
-// groups in a fixed order.  Every row has one writer: deterministic, no atomics.
-template <bool HALO>
-__global__ void __launch_bounds__(256) tail_group_kernel(TailGrpArgs a) {
-    const int64_t g = a.g_begin + (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
-    if (g >= a.g_end) return;
-    const int32_t k0 = __ldg(a.gk0 + g), n = __ldg(a.gk0 + g + 1) - k0;
-    const int32_t r = __ldg(a.grow + g);
-    int32_t end[8];
-#pragma unroll
-    for (int j = 0; j < 8; ++j) end[j] = r + 1 + j <= a.n_tail ? __ldg(a.ptr + r + 1 + j) : 0x7fffffff;
-    const bool started_before = __ldg(a.ptr + r) < k0;
-    int32_t col[8];
-    double val[8];
-    if (n == 8 && (k0 & 7) == 0) {
-        const int4 c0 = __ldg(reinterpret_cast<const int4*>(a.col + k0));
-        const int4 c1 = __ldg(reinterpret_cast<const int4*>(a.col + k0) + 1);
-        col[0] = c0.x; col[1] = c0.y; col[2] = c0.z; col[3] = c0.w;
-        col[4] = c1.x; col[5] = c1.y; col[6] = c1.z; col[7] = c1.w;
-#pragma unroll
-        for (int j = 0; j < 4; ++j) {
-            const double2 v = __ldg(reinterpret_cast<const double2*>(a.val + k0) + j);
-            val[2 * j] = v.x;
-            val[2 * j + 1] = v.y;
-        }
-    } else {
-#pragma unroll
-        for (int j = 0; j < 8; ++j) {
-            col[j] = j < n ? __ldg(a.col + k0 + j) : -1;
-            val[j] = j < n ? __ldg(a.val + k0 + j) : 0.0;
-        }
-    }
-    double xg[8];
-#pragma unroll
-    for (int j = 0; j < 8; ++j) xg[j] = col[j] >= 0 ? gather_x<HALO>(a.x, a.x_halo, a.n_loc, col[j]) : 0.0;
-    double acc = 0.0, head = 0.0;
-    bool head_ends = false;
-    int cur = 0;  // row r + cur
-#pragma unroll
-    for (int j = 0; j < 8; ++j) {
-        if (j < n) {
-            acc = fma(val[j], xg[j], acc);
-            int32_t e = end[0];
-#pragma unroll
-            for (int q = 1; q < 8; ++q) e = (cur == q) ? end[q] : e;
-            if (k0 + j + 1 == e) {  // row r + cur ends at this entry
-                if (cur == 0 && started_before) {
-                    head = acc;          // last piece of a spanning row: the fix-up adds the rest
-                    head_ends = true;
-                } else {
-                    double* yp = a.y + __ldg(a.out_rows + r + cur);
-                    *yp = *yp + a.alpha * acc;
-                }
-                acc = 0.0;
-                ++cur;
-            }
-        }
-    }
-    a.carry[g] = acc;  // open row at the group's end (0 when the last entry closed a row)
-    if (head_ends) a.headsum[g] = head;
-}
-
-// For every group where a spanning row ends: y[row] += alpha (headsum + carries
-// of the earlier groups of that row), summed backwards in a fixed order.
-__global__ void __launch_bounds__(256) tail_fix_kernel(TailGrpArgs a) {
-    const int64_t g = a.g_begin + (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
-    if (g >= a.g_end) return;
-    const int32_t k0 = __ldg(a.gk0 + g), k1 = __ldg(a.gk0 + g + 1);
-    const int32_t r = __ldg(a.grow + g);
-    const int32_t rs = __ldg(a.ptr + r), re = __ldg(a.ptr + r + 1);
-    if (!(rs < k0 && re <= k1)) return;  // the group's first row neither spans into it nor ends in it
-    double s = a.headsum[g];
-    for (int64_t h = g - 1; h >= a.g_begin; --h) {
-        s += a.carry[h];
-        if (__ldg(a.gk0 + h) <= rs) break;  // group h holds the row's first entry
-    }
-    double* yp = a.y + __ldg(a.out_rows + r);
-    *yp = *yp + a.alpha * s;
-}
-
-cudaError_t launch_tail_grouped(const TailGrpArgs& a, cudaStream_t s) {
-    const int64_t groups = a.g_end - a.g_begin;
-    if (groups <= 0) return cudaSuccess;
-    const unsigned blocks = (unsigned)((groups + 255) / 256);
-    if (a.x_halo) tail_group_kernel<true><<<blocks, 256, 0, s>>>(a);
-    else tail_group_kernel<false><<<blocks, 256, 0, s>>>(a);
-    cudaError_t e = cudaGetLastError();
-    if (e != cudaSuccess) return e;
-    tail_fix_kernel<<<blocks, 256, 0, s>>>(a);
-    return cudaGetLastError();
-}
-
 // ------------------------------------------------------- HYB: COO kernel --
 // Comparison variant: the Bell-Garland HYB remainder in
 // COO instead of CSR.  Lane l of a warp owns 8 consecutive row-sorted
