@@ -114,8 +114,8 @@ __device__ __forceinline__ double gather_x(const double* __restrict__ x,
 
 // ------------------------------------------------------------- ELL kernel --
 // W > 0: width known at compile time (fully unrolled); W == 0: runtime width.
-template <int W, bool HALO, bool ROWMAP>
-__global__ void __launch_bounds__(256) ell_kernel(EllArgs a) {
+template <int W, bool HALO, bool ROWMAP, int MINB = 1>
+__global__ void __launch_bounds__(256, MINB) ell_kernel(EllArgs a) {
     const uint64_t pol = policy_evict_first();
     const int32_t width = W > 0 ? W : a.width;
     const int64_t s = a.stride;
@@ -190,6 +190,9 @@ __global__ void __launch_bounds__(256) ell_kernel(EllArgs a) {
             }
         }
     }
+    // programmatic dependent launch: the tail kernel may start its loads now
+    // (it waits for this grid's completion before it touches y)
+    asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
 }
 
 // ------------------------------------------------------------ tail kernel --
@@ -210,16 +213,13 @@ __global__ void __launch_bounds__(256) tail_kernel(TailArgs a) {
     const int G = 1 << lg;
     const int lane = threadIdx.x & (G - 1);
     const int grp = threadIdx.x >> lg;
-    double acc = 0.0, y_old = 0.0;
+    double acc = 0.0;
     double* yp = nullptr;
     const bool active = grp < d.y;
     if (active) {
         const int32_t t = d.x + grp;  // device position: the block's rows are contiguous
         const int32_t kb = __ldg(a.ptr + t), ke = __ldg(a.ptr + t + 1);
-        if (lane == 0) {  // the ELL result this row adds to (written by the previous kernel)
-            yp = a.y + __ldg(a.out_rows + t);
-            y_old = *yp;
-        }
+        if (lane == 0) yp = a.y + __ldg(a.out_rows + t);
 #pragma unroll 8
         for (int32_t k = kb + lane; k < ke; k += G) {
             // L1-allocating: the G lanes of a row revisit each 32-byte sector
@@ -230,7 +230,11 @@ __global__ void __launch_bounds__(256) tail_kernel(TailArgs a) {
         }
     }
     for (int off = G >> 1; off > 0; off >>= 1) acc += __shfl_xor_sync(0xffffffffu, acc, off, G);
-    if (lane == 0 && active) *yp = y_old + a.alpha * acc;
+    // y holds the ELL result: with programmatic dependent launch this kernel may
+    // have started before ell_kernel finished, so wait for it here (a no-op
+    // when launched normally)
+    asm volatile("griddepcontrol.wait;" ::: "memory");
+    if (lane == 0 && active) *yp = *yp + a.alpha * acc;
 }
 
 // ------------------------------------------------------- HYB: COO kernel --
@@ -318,18 +322,38 @@ static int num_sms() {
 
 // Kernel launch through cudaLaunchKernelEx.  (An L2 persisting access-policy
 // window on x was measured, r09: slower for every config; not used.)
+// pdl = programmatic dependent launch: the kernel may start while the previous
+// kernel on the stream drains (it must griddepcontrol.wait before consuming).
 template <typename... KArgs, typename... Args>
-static cudaError_t launch_k(void (*kernel)(KArgs...), dim3 g, dim3 b, cudaStream_t s, const void* x,
-                            size_t x_bytes, Args&&... args) {
+static cudaError_t launch_k(void (*kernel)(KArgs...), dim3 g, dim3 b, cudaStream_t s, bool pdl, Args&&... args) {
     cudaLaunchConfig_t cfg = {};
     cfg.gridDim = g;
     cfg.blockDim = b;
     cfg.stream = s;
-    cfg.attrs = nullptr;
-    cfg.numAttrs = 0;
-    (void)x;
-    (void)x_bytes;
+    cudaLaunchAttribute attr[1];
+    attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+    attr[0].val.programmaticStreamSerializationAllowed = 1;
+    cfg.attrs = attr;
+    cfg.numAttrs = pdl ? 1 : 0;
     return cudaLaunchKernelEx(&cfg, kernel, std::forward<Args>(args)...);
+}
+
+static bool tail_pdl() {
+    static int v = -1;
+    if (v < 0) {
+        const char* e = std::getenv("HEC_PDL");
+        v = (e && std::atoi(e) != 0) ? 1 : 0;
+    }
+    return v == 1;
+}
+
+static int ell_minb() {
+    static int v = -1;
+    if (v < 0) {
+        const char* e = std::getenv("HEC_ELL_MINB");
+        v = e ? std::atoi(e) : 1;
+    }
+    return v;
 }
 
 template <bool HALO, bool ROWMAP>
@@ -343,14 +367,17 @@ static cudaError_t launch_ell_t(const EllArgs& a, cudaStream_t s) {
     if (blocks > cap) blocks = cap;
     if (blocks < 1) blocks = 1;
     const dim3 g((unsigned)blocks), b(threads);
-    const size_t xb = (size_t)a.n_loc * sizeof(double);
+    if (!HALO && !ROWMAP && ell_minb() == 6) {  // tuning experiment: >= 6 CTAs/SM (<= 40 registers)
+        if (a.width == 7) return launch_k(ell_kernel<7, false, false, 6>, g, b, s, false, a);
+        if (a.width == 9) return launch_k(ell_kernel<9, false, false, 6>, g, b, s, false, a);
+    }
     switch (a.width) {
 #define HEC_W(w) \
-    case w: return launch_k(ell_kernel<w, HALO, ROWMAP>, g, b, s, a.x, xb, a);
+    case w: return launch_k(ell_kernel<w, HALO, ROWMAP>, g, b, s, false, a);
         HEC_W(1) HEC_W(2) HEC_W(3) HEC_W(4) HEC_W(5) HEC_W(6) HEC_W(7) HEC_W(8)
         HEC_W(9) HEC_W(10) HEC_W(11) HEC_W(12) HEC_W(13) HEC_W(14) HEC_W(15) HEC_W(16)
 #undef HEC_W
-        default: return launch_k(ell_kernel<0, HALO, ROWMAP>, g, b, s, a.x, xb, a);
+        default: return launch_k(ell_kernel<0, HALO, ROWMAP>, g, b, s, false, a);
     }
 }
 
@@ -382,9 +409,9 @@ cudaError_t launch_tail(const TailArgs& a, cudaStream_t s) {
     const int64_t blocks = a.blk_end - a.blk_begin;
     if (blocks <= 0) return cudaSuccess;
     if (blocks > 0x7fffffff) return cudaErrorInvalidValue;
-    const size_t xb = (size_t)a.n_loc * sizeof(double);
-    if (a.x_halo) return launch_k(tail_kernel<true>, dim3((unsigned)blocks), dim3(256), s, a.x, xb, a);
-    return launch_k(tail_kernel<false>, dim3((unsigned)blocks), dim3(256), s, a.x, xb, a);
+    const bool pdl = tail_pdl();
+    if (a.x_halo) return launch_k(tail_kernel<true>, dim3((unsigned)blocks), dim3(256), s, pdl, a);
+    return launch_k(tail_kernel<false>, dim3((unsigned)blocks), dim3(256), s, pdl, a);
 }
 
 cudaError_t launch_pack(const int32_t* idx, int32_t n, const double* x, double* out,
