@@ -114,8 +114,10 @@ __device__ __forceinline__ double gather_x(const double* __restrict__ x,
 
 // ------------------------------------------------------------- ELL kernel --
 // W > 0: width known at compile time (fully unrolled); W == 0: runtime width.
-template <int W, bool HALO, bool ROWMAP, int MINB = 1>
-__global__ void __launch_bounds__(256, MINB) ell_kernel(EllArgs a) {
+// AXPBY: the Eq. (2) epilogue is compiled in only for hec_spmv_axpby (keeping
+// it out of the plain kernel keeps the load schedule of the hot path intact).
+template <int W, bool HALO, bool ROWMAP, bool AXPBY>
+__global__ void __launch_bounds__(256) ell_kernel(EllArgs a) {
     const uint64_t pol = policy_evict_first();
     const int32_t width = W > 0 ? W : a.width;
     const int64_t s = a.stride;
@@ -164,10 +166,10 @@ __global__ void __launch_bounds__(256, MINB) ell_kernel(EllArgs a) {
         if (ROWMAP) {
             double* y0 = a.y + a.rowmap[i0];
             double* y1 = two ? a.y + a.rowmap[i0 + 1] : nullptr;
-            if (a.beta != 0.0) {
+            if (AXPBY && a.beta != 0.0) {
                 acc0 = a.alpha * acc0 + a.beta * *y0;
                 if (two) acc1 = a.alpha * acc1 + a.beta * *y1;
-            } else {
+            } else if (AXPBY) {
                 acc0 *= a.alpha;
                 acc1 *= a.alpha;
             }
@@ -175,10 +177,10 @@ __global__ void __launch_bounds__(256, MINB) ell_kernel(EllArgs a) {
             if (two) st_stream_d1(y1, acc1);
         } else {
             double* yp = a.y + a.row_off + i0;
-            if (a.beta != 0.0) {
+            if (AXPBY && a.beta != 0.0) {
                 acc0 = a.alpha * acc0 + a.beta * yp[0];
                 if (two) acc1 = a.alpha * acc1 + a.beta * yp[1];
-            } else {
+            } else if (AXPBY) {
                 acc0 *= a.alpha;
                 acc1 *= a.alpha;
             }
@@ -347,37 +349,25 @@ static bool tail_pdl() {
     return v == 1;
 }
 
-static int ell_minb() {
-    static int v = -1;
-    if (v < 0) {
-        const char* e = std::getenv("HEC_ELL_MINB");
-        v = e ? std::atoi(e) : 1;
-    }
-    return v;
-}
-
-template <bool HALO, bool ROWMAP>
+template <bool HALO, bool ROWMAP, bool AXPBY>
 static cudaError_t launch_ell_t(const EllArgs& a, cudaStream_t s) {
     const int64_t n_pairs = ((int64_t)a.n_rows + 1) >> 1;
     const int threads = 256;
     int64_t blocks = (n_pairs + threads - 1) / threads;
     // one row pair per thread, grid-stride only beyond 64 full waves (a
-    // persistent grid of 5-40 blocks/SM was measured slower, r15)
+    // persistent grid of 5-40 blocks/SM was measured slower, r15; forcing
+    // >= 6 CTAs/SM by a 40-register cap too, pdl run)
     const int64_t cap = (int64_t)num_sms() * 8 * 64;
     if (blocks > cap) blocks = cap;
     if (blocks < 1) blocks = 1;
     const dim3 g((unsigned)blocks), b(threads);
-    if (!HALO && !ROWMAP && ell_minb() == 6) {  // tuning experiment: >= 6 CTAs/SM (<= 40 registers)
-        if (a.width == 7) return launch_k(ell_kernel<7, false, false, 6>, g, b, s, false, a);
-        if (a.width == 9) return launch_k(ell_kernel<9, false, false, 6>, g, b, s, false, a);
-    }
     switch (a.width) {
 #define HEC_W(w) \
-    case w: return launch_k(ell_kernel<w, HALO, ROWMAP>, g, b, s, false, a);
+    case w: return launch_k(ell_kernel<w, HALO, ROWMAP, AXPBY>, g, b, s, false, a);
         HEC_W(1) HEC_W(2) HEC_W(3) HEC_W(4) HEC_W(5) HEC_W(6) HEC_W(7) HEC_W(8)
         HEC_W(9) HEC_W(10) HEC_W(11) HEC_W(12) HEC_W(13) HEC_W(14) HEC_W(15) HEC_W(16)
 #undef HEC_W
-        default: return launch_k(ell_kernel<0, HALO, ROWMAP>, g, b, s, false, a);
+        default: return launch_k(ell_kernel<0, HALO, ROWMAP, AXPBY>, g, b, s, false, a);
     }
 }
 
@@ -401,8 +391,12 @@ cudaError_t launch_ell(const EllArgs& a, cudaStream_t s) {
     }
     const bool halo = a.x_halo != nullptr;
     const bool rowmap = a.rowmap != nullptr;
-    if (halo) return rowmap ? launch_ell_t<true, true>(a, s) : launch_ell_t<true, false>(a, s);
-    return rowmap ? launch_ell_t<false, true>(a, s) : launch_ell_t<false, false>(a, s);
+    if (a.alpha != 1.0 || a.beta != 0.0) {  // hec_spmv_axpby (single matrix: no halo, no row map)
+        if (halo || rowmap) return cudaErrorInvalidValue;
+        return launch_ell_t<false, false, true>(a, s);
+    }
+    if (halo) return rowmap ? launch_ell_t<true, true, false>(a, s) : launch_ell_t<true, false, false>(a, s);
+    return rowmap ? launch_ell_t<false, true, false>(a, s) : launch_ell_t<false, false, false>(a, s);
 }
 
 cudaError_t launch_tail(const TailArgs& a, cudaStream_t s) {
