@@ -118,6 +118,11 @@ __device__ __forceinline__ double gather_x(const double* __restrict__ x,
 // it out of the plain kernel keeps the load schedule of the hot path intact).
 template <int W, bool HALO, bool ROWMAP, bool AXPBY>
 __global__ void __launch_bounds__(256) ell_kernel(EllArgs a) {
+    // Programmatic dependent launch: the tail kernel may be scheduled once every
+    // CTA of this grid has started (it griddepcontrol.waits for this grid's
+    // completion before it touches y).  No memory clobber: nothing is ordered
+    // by it, and a clobber costs the hot loop 14 registers.
+    asm volatile("griddepcontrol.launch_dependents;");
     const uint64_t pol = policy_evict_first();
     const int32_t width = W > 0 ? W : a.width;
     const int64_t s = a.stride;
@@ -192,9 +197,6 @@ __global__ void __launch_bounds__(256) ell_kernel(EllArgs a) {
             }
         }
     }
-    // programmatic dependent launch: the tail kernel may start its loads now
-    // (it waits for this grid's completion before it touches y)
-    asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
 }
 
 // ------------------------------------------------------------ tail kernel --
