@@ -345,8 +345,10 @@ static cudaError_t launch_k(void (*kernel)(KArgs...), dim3 g, dim3 b, cudaStream
 static bool tail_pdl() {
     static int v = -1;
     if (v < 0) {
+        // default on (measured q3: SPE10 0.0279 -> 0.0237 ms, no change elsewhere);
+        // HEC_PDL=0 launches the tail kernel plainly
         const char* e = std::getenv("HEC_PDL");
-        v = (e && std::atoi(e) != 0) ? 1 : 0;
+        v = (e && std::atoi(e) == 0) ? 0 : 1;
     }
     return v == 1;
 }
