@@ -233,12 +233,20 @@ hec_status dist_spmv_launch(hec_dist_s* D, const double* x_local, double* y_loca
         }
         ncclResult_t r2 = ncclGroupEnd();
         if (r != ncclSuccess || r2 != ncclSuccess) return nccl_fail(r != ncclSuccess ? r : r2, "halo send/recv");
+        // boundary rows right behind the halo on the (high-priority) comm
+        // stream: they write rows of y disjoint from the interior's, so they
+        // need not wait for the interior kernel -- critical path
+        // max(interior, pack + exchange + boundary)
+        if (D->n_boundary > 0) {
+            hec_status st = launch_spmv(D->boundary, x_local, D->d_x_halo, y_local, D->comm_stream);
+            if (st != HEC_OK) return st;
+        }
         HEC_CUDA_TRY(cudaEventRecord(D->ev_halo, D->comm_stream));
     }
     hec_status st = launch_spmv(D->interior, x_local, nullptr, y_local, s);  // interior rows
     if (st != HEC_OK) return st;
     if (ex) HEC_CUDA_TRY(cudaStreamWaitEvent(s, D->ev_halo, 0));
-    if (D->n_boundary > 0) st = launch_spmv(D->boundary, x_local, D->d_x_halo, y_local, s);  // boundary rows
+    else if (D->n_boundary > 0) st = launch_spmv(D->boundary, x_local, D->d_x_halo, y_local, s);
     return st;
 }
 
