@@ -196,7 +196,9 @@ int hecgen_powerlaw_fill(int32_t n, int32_t band, double p_local, int integer_va
                 double u = hecgen_u01(seed, ST_COL, 2 * key);
                 uint64_t r = hecgen_ctr(seed, ST_COL, 2 * key + 1);
                 int64_t j;
-                if (u < p_local) {
+                /* after 16 L attempts the band is exhausted (p_local = 1 and L >
+                 * 2 band + 1): draw globally so the row always completes */
+                if (u < p_local && attempt < 16 * (uint64_t)L) {
                     int64_t delta = 1 + (int64_t)(r % (uint64_t)band);
                     if ((r >> 32) & 1) delta = -delta;
                     j = (int64_t)i + delta;

@@ -260,6 +260,19 @@ hec_status hec_plan_part_hec(hec_plan P, const hec_csr* A, int32_t part, int32_t
                              const hec_opts* o, int32_t device, void* stream, hec_matrix* out);
 void hec_plan_free(hec_plan P);
 
+/* Reordering for irregular matrices ("the rows of the matrix are
+ * switched first and all the nonzero entries are put along the diagonal as
+ * close as possible"; METIS is not available offline -- reading A21):
+ *   hec_reorder_rcm: deterministic reverse Cuthill-McKee ordering of the
+ *     pattern of A + A^T; perm[new] = old (caller-allocated, n entries).
+ *   hec_permute: B = P A P^T, i.e. B[i][j] = A[perm[i]][perm[j]], canonical
+ *     (rows re-sorted); caller allocates row_ptr_out[n+1], col_out[nnz],
+ *     val_out[nnz].  Vectors follow with x_new[i] = x[perm[i]].
+ * Square A only (HEC_ERR_DIM); perm must be a permutation (HEC_ERR_ARG). */
+hec_status hec_reorder_rcm(const hec_csr* A, int32_t* perm);
+hec_status hec_permute(const hec_csr* A, const int32_t* perm, int32_t* row_ptr_out, int32_t* col_out,
+                       double* val_out);
+
 /* -------------------------------------------------------- distributed ---- */
 
 typedef struct hec_dist_s* hec_dist;

@@ -81,7 +81,7 @@ EXPORTED = [
     "hec_dist_create", "hec_dist_create_local", "hec_spmv_dist", "hec_spmv_dist_local",
     "hec_dist_get_info", "hec_dist_free",
     "hec_spmv_axpby", "hec_axpby", "hec_axpbyz", "hec_dot", "hec_norm2", "hec_bicgstab", "hec_cg",
-    "hec_bicgstab_dist", "hec_cg_dist", "hec_from_csr_hyb",
+    "hec_bicgstab_dist", "hec_cg_dist", "hec_from_csr_hyb", "hec_reorder_rcm", "hec_permute",
 ]
 
 
@@ -170,6 +170,10 @@ def load(build: bool = True):
     L.hec_dot.argtypes = [i64, vp, vp, ctypes.POINTER(dbl), vp]
     L.hec_norm2.restype = st
     L.hec_norm2.argtypes = [i64, vp, ctypes.POINTER(dbl), vp]
+    L.hec_reorder_rcm.restype = st
+    L.hec_reorder_rcm.argtypes = [ctypes.POINTER(CsrT), vp]
+    L.hec_permute.restype = st
+    L.hec_permute.argtypes = [ctypes.POINTER(CsrT), vp, vp, vp, vp]
     for f in (L.hec_bicgstab, L.hec_cg, L.hec_bicgstab_dist, L.hec_cg_dist):
         f.restype = st
         f.argtypes = [vp, vp, vp, dbl, i32, vp, ctypes.POINTER(SolveInfoT)]
@@ -511,6 +515,27 @@ class LocalDistGroup:
     def free(self):
         for r in self.ranks:
             r.free()
+
+
+def reorder_rcm(A) -> np.ndarray:
+    """Reverse Cuthill-McKee ordering (perm[new] = old) of A's symmetrised pattern."""
+    load()
+    args = _CsrArgs(A)
+    perm = np.empty(A.n_rows, np.int32)
+    _check(_lib.hec_reorder_rcm(args.ref(), _p(perm)))
+    return perm
+
+
+def permute(A, perm: np.ndarray):
+    """B = P A P^T (B[i][j] = A[perm[i]][perm[j]]) as a canonical CSR of A's type."""
+    load()
+    args = _CsrArgs(A)
+    perm = np.ascontiguousarray(perm, dtype=np.int32)
+    rp = np.empty(A.n_rows + 1, np.int32)
+    col = np.empty(args.col.shape[0], np.int32)
+    val = np.empty(args.col.shape[0], np.float64)
+    _check(_lib.hec_permute(args.ref(), _p(perm), _p(rp), _p(col), _p(val)))
+    return type(A)(A.n_rows, A.n_cols, rp, col, val)
 
 
 def axpby(alpha: float, x, beta: float, y, stream=None):
