@@ -41,7 +41,7 @@ def test_path_graph_recovers_bandwidth_one():
 
 
 @pytest.mark.parametrize("maker", [lambda: hecgen.poisson2d(20, 15), lambda: hecgen.poisson3d(8, 7, 6),
-                                   lambda: hecgen.powerlaw(400, seed=2, band=8, p_local=1.0)])
+                                   lambda: hecgen.powerlaw(2000, lmin=3, lmax=8, alpha=2.0, band=6, p_local=1.0, seed=2)])
 def test_bandwidth_comparable_to_scipy(maker):
     S, _ = scramble(maker(), 3)
     ours = R.bandwidth(R.permute(S, R.rcm(S), hecgen.Csr))
