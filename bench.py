@@ -45,6 +45,10 @@ def parse():
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--profile", action="store_true", help="short run for ncu (no clocks/e2e/cpu)")
+    ap.add_argument("--scramble", type=int, default=None,
+                    help="apply a seeded random symmetric permutation to the workload (NEXT-4 experiment)")
+    ap.add_argument("--reorder", choices=["rcm"], default=None,
+                    help="reorder the workload with reverse Cuthill-McKee before converting (NEXT-4)")
     ap.add_argument("--formats", default=None,
                     help="'all' or comma-separated configs: per-format SpMV table (NEXT-2, Table 3 analog)")
     ap.add_argument("--solver", choices=["cg", "bicgstab"], default=None,
@@ -227,6 +231,26 @@ def run_single(args):
     torch.cuda.set_device(dev)
     t_setup = time.perf_counter()
     A = hecgen.CONFIGS[args.config]()
+    reorder_info = None
+    if args.scramble is not None or args.reorder:
+        # NEXT-4 experiment: a random symmetric permutation of the workload
+        # (input generation), then optionally the RCM reordering (setup)
+        def halo8(M):
+            P = hec.partition(M, 8, hec.PART_CONTIG_NNZ)
+            return int(sum(P.part_info(p).n_halo for p in range(8)))
+        reorder_info = {}
+        if args.scramble is not None:
+            perm = np.random.default_rng(args.scramble).permutation(A.n_rows).astype(np.int32)
+            A = hec.permute(A, perm)
+            A.name = f"{args.config}_scrambled{args.scramble}"
+            reorder_info["scrambled_seed"] = args.scramble
+        reorder_info["halo_entries_p8_before"] = halo8(A)
+        if args.reorder == "rcm":
+            t0 = time.perf_counter()
+            A = hec.permute(A, hec.reorder_rcm(A))
+            reorder_info["rcm_s"] = round(time.perf_counter() - t0, 2)
+            reorder_info["halo_entries_p8_after"] = halo8(A)
+        A.name = A.name or args.config
     t_gen = time.perf_counter() - t_setup
     x_h = hecgen.vector(A.n_cols, "uniform", seed=1606)
     stream = torch.cuda.Stream()
@@ -312,7 +336,8 @@ def run_single(args):
                        "tail_nnz": inf.tail_nnz, "parallelism": "1 GPU",
                        "l2": (f"inputs {alg / 1e9:.2f} GB > 4x {L2_BYTES / 2**20:.0f} MiB L2, no flush" if not flush
                               else f"L2 flushed ({4 * L2_BYTES / 2**20:.0f} MiB write + read) before every step, outside the timed pair"),
-                       "checksum": A.checksum(), "setup_s": {"generate": round(t_gen, 2), "convert_upload": round(t_conv, 2)}},
+                       "checksum": A.checksum(), "setup_s": {"generate": round(t_gen, 2), "convert_upload": round(t_conv, 2)},
+                       "reorder": reorder_info},
             "gbs": round(alg / (ms_step * 1e-3) / 1e9, 1),
             "roofline": roof, "gpu_launches": K * launches_per_step,
             "e2e": e2e, "cpu_baseline": cpu,
