@@ -122,4 +122,4 @@ def is_canonical(A) -> bool:
     return True
 
 
-from . import hec_ref, plan_ref, krylov_ref, reorder_ref  # noqa: E402,F401
+from . import hec_ref, plan_ref, krylov_ref, reorder_ref, jacobi_ref  # noqa: E402,F401
