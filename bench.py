@@ -53,6 +53,8 @@ def parse():
                     help="'all' or comma-separated configs: per-format SpMV table (NEXT-2, Table 3 analog)")
     ap.add_argument("--solver", choices=["cg", "bicgstab"], default=None,
                     help="measure Krylov iterations/s instead of the SpMV (NEXT-1)")
+    ap.add_argument("--jacobi", type=float, default=None, metavar="OMEGA",
+                    help="NEXT-3: time damped-Jacobi sweeps (hec_jacobi) with this omega")
     ap.add_argument("--dist", action="store_true",
                     help="use the distributed path (hec_spmv_dist under torchrun) even with one GPU")
     return ap.parse_args()
@@ -515,6 +517,77 @@ def run_solver(args):
     return 0
 
 
+def run_jacobi(args):
+    """NEXT-3 measurement (not the headline): damped-Jacobi sweeps x <- x +
+    omega D^-1 (b - A x) (hec_jacobi, the SpMV with its Jacobi epilogue),
+    ping-pong over K sweeps, per-sweep event pairs (cold L2 below 4x L2).
+    Algorithmic bytes per sweep = the SpMV's (12 nnz + 8 n_cols + 8 n_rows)
+    + b and d (16 n).  The plain SpMV on the same matrix is timed beside it."""
+    import torch
+    from oracle import jacobi_ref as JR
+    import paper_1606_00545_b200 as hec
+    torch.cuda.set_device(0)
+    A = hecgen.CONFIGS[args.config]()
+    n = A.n_rows
+    M = hec.from_csr(A)
+    b_h = hecgen.vector(n, "uniform", seed=7)
+    x_h = hecgen.vector(n, "uniform", seed=8)
+    b = torch.from_numpy(b_h).cuda()
+    d = torch.empty(n, dtype=torch.float64, device="cuda")
+    M.diag(d)
+    u, v = torch.from_numpy(x_h).cuda(), torch.empty(n, dtype=torch.float64, device="cuda")
+    alg = algorithmic_bytes(A.nnz, n, A.n_cols) + 16 * n
+    cold = alg < 4 * L2_BYTES
+    flusher = L2Flusher("cuda:0") if cold else None
+    # one checked sweep (sampled rows against the oracle), then warm-up
+    M.jacobi(d, b, u, v, args.jacobi)
+    r0 = n // 3
+    r1 = min(n, r0 + 4000)
+    d_s = JR.diag(A, r0, r1)
+    ref = JR.jacobi(A, d_s, b_h[r0:r1], x_h, args.jacobi, r0, r1)
+    tol = JR.tolerance(A, d_s, b_h[r0:r1], x_h, args.jacobi, r0, r1)
+    ok = bool(np.all(np.abs(v.cpu().numpy()[r0:r1] - ref) <= tol))
+    for _ in range(max(3, args.warmup)):
+        M.jacobi(d, b, u, v, args.jacobi)
+        u, v = v, u
+
+    def timed(fn, K):
+        ev = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)) for _ in range(K)]
+        for e0, e1 in ev:
+            if flusher:
+                flusher()
+            e0.record()
+            fn()
+            e1.record()
+        torch.cuda.synchronize()
+        return sum(e0.elapsed_time(e1) for e0, e1 in ev) / K
+
+    state = [u, v]
+
+    def sweep():
+        M.jacobi(d, b, state[0], state[1], args.jacobi)
+        state.reverse()
+    with ClockSampler(0) as clk:
+        ms = timed(sweep, args.steps)
+    y = torch.empty(n, dtype=torch.float64, device="cuda")
+    spmv_ms = timed(lambda: M.spmv(state[0], y), args.steps)
+    peak, peak_src = measured_peak()
+    gbs = alg / (ms * 1e-3) / 1e9
+    line = {"metric": "fp64 damped-Jacobi sweeps/s (HEC SpMV + fused epilogue, NEXT-3)",
+            "value": round(1e3 / ms, 2), "unit": "sweeps/s", "n_gpus": 1, "steps": args.steps,
+            "warmup": max(3, args.warmup), "ms_per_step": round(ms, 5), "higher_is_better": True,
+            "scaling": "strong", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
+            "config": {"workload": args.config, "n_rows": n, "nnz": A.nnz, "omega": args.jacobi,
+                       "l2": "flushed before every sweep" if cold else "inputs > 4x L2, no flush",
+                       "spmv_ms_same_matrix": round(spmv_ms, 5), "parity_sample_ok": ok},
+            "roofline": {"bound": "hbm", "achieved": round(gbs, 1), "peak": peak, "unit": "GB/s",
+                         "frac": round(gbs / peak, 4), "traffic": None, "kernel": "ell_kernel<EPI_JACOBI> (+ tail)",
+                         "algorithmic_bytes_per_sweep": alg, "peak_source": peak_src},
+            "gpu_launches": M.launches * args.steps, "clocks": clk.summary()}
+    print(json.dumps(line), flush=True)
+    return 0
+
+
 def run_formats(args):
     """NEXT-2: the paper's Table 3 experiment (SpMV speedup per format)
     on B200 with the synthetic workloads: ELL (w = max row length, no
@@ -595,6 +668,8 @@ def main():
         return run_formats(args)
     if args.solver:
         return run_solver(args)
+    if args.jacobi is not None:
+        return run_jacobi(args)
     if args.impl == "reference":
         return run_reference(args)
     world = int(os.environ.get("WORLD_SIZE", "1"))

@@ -160,6 +160,25 @@ int32_t hec_spmv_launches(hec_matrix A);
 hec_status hec_spmv_axpby(hec_matrix A, double alpha, const double* x, double beta, double* y,
                           void* stream);
 
+/* d[i] = A_ii: the stored diagonal entry of row i, +0.0 when the row stores
+ * none (A22).  A must be a square whole-matrix device handle
+ * (HEC_ERR_DIM otherwise; HEC_ERR_NODEV for a host-only handle).  d: device,
+ * n_rows doubles, fully overwritten.  Asynchronous on `stream`; setup-time. */
+hec_status hec_diag(hec_matrix A, double* d, void* stream);
+
+/* One damped-Jacobi sweep, the SpMV-based smoother of the paper's AMG ("damped
+ * Jacobi"; "developed based on the SpMV and vector operations", P:542;
+ * formula: DESIGN.md A22):
+ *     x_out = x + omega * D^{-1} (b - A x),   D = diag(d)
+ * fused into the SpMV epilogue (the ELL kernel writes x + omega((b - s_ell)/d),
+ * the CSR-tail kernel subtracts omega(s_tail/d)); no FMA contraction in the
+ * update.  A: square whole-matrix device handle (HEC_ERR_DIM).  d, b, x, x_out:
+ * device, n_rows doubles; x_out is fully overwritten and must not overlap x, b
+ * or d (HEC_ERR_ARG); rows with d_i = 0 give IEEE Inf/NaN.  Asynchronous on
+ * `stream`. */
+hec_status hec_jacobi(hec_matrix A, const double* d, const double* b, const double* x, double* x_out,
+                      double omega, void* stream);
+
 /* ------------------------------------------------------ vector operations ---- */
 /* PAPER §2.3 Eqs. (3)-(6), on device vectors of length n
  * (asynchronous on `stream` unless stated):

@@ -28,26 +28,32 @@ import numpy as np
 from . import csr_absmv, csr_spmv
 
 
-def diag(A) -> np.ndarray:
-    """d_i = A_ii if row i stores column i, else +0.0 (square A)."""
+def diag(A, r0: int = 0, r1: int | None = None) -> np.ndarray:
+    """d_i = A_ii if row i stores column i, else +0.0 (square A); rows [r0, r1)."""
     if A.n_rows != A.n_cols:
         raise ValueError("diag needs a square matrix")
-    d = np.zeros(A.n_rows, dtype=np.float64)
-    for i in range(A.n_rows):
+    r1 = A.n_rows if r1 is None else r1
+    d = np.zeros(r1 - r0, dtype=np.float64)
+    for i in range(r0, r1):
         for k in range(int(A.row_ptr[i]), int(A.row_ptr[i + 1])):
             if int(A.col[k]) == i:
-                d[i] = A.val[k]
+                d[i - r0] = A.val[k]
     return d
 
 
-def jacobi(A, d: np.ndarray, b: np.ndarray, x: np.ndarray, omega: float) -> np.ndarray:
-    """One damped-Jacobi sweep x + omega D^{-1} (b - A x)."""
-    r = b - csr_spmv(A, x)   # numpy elementwise: one rounding each
+def jacobi(A, d: np.ndarray, b: np.ndarray, x: np.ndarray, omega: float,
+           r0: int = 0, r1: int | None = None) -> np.ndarray:
+    """One damped-Jacobi sweep x + omega D^{-1} (b - A x), rows [r0, r1).
+    d and b hold rows [r0, r1); x is the whole vector."""
+    r1 = A.n_rows if r1 is None else r1
+    r = b - csr_spmv(A, x, r0, r1)   # numpy elementwise: one rounding each
     q = r / d
-    return x + omega * q
+    return x[r0:r1] + omega * q
 
 
-def tolerance(A, d: np.ndarray, b: np.ndarray, x: np.ndarray, omega: float) -> np.ndarray:
+def tolerance(A, d: np.ndarray, b: np.ndarray, x: np.ndarray, omega: float,
+              r0: int = 0, r1: int | None = None) -> np.ndarray:
+    r1 = A.n_rows if r1 is None else r1
     with np.errstate(divide="ignore", invalid="ignore"):
         g = np.abs(omega / d)
-    return 1e-12 * (np.abs(x) + g * (np.abs(b) + csr_absmv(A, x)))
+    return 1e-12 * (np.abs(x[r0:r1]) + g * (np.abs(b) + csr_absmv(A, x, r0, r1)))

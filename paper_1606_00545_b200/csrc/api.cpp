@@ -216,7 +216,8 @@ hec_status make_matrix(HostHec&& h, int32_t device, cudaStream_t s, const int32_
 // Chunk c of the handle (rows [chunk_row[c], chunk_row[c+1]), r0 a multiple
 // of 512), or all chunks when c < 0: ELL kernel then tail kernel.
 static hec_status launch_chunks(const hec_matrix_s* A, int c, const double* x, const double* x_halo,
-                                double* y, cudaStream_t s, double alpha = 1.0, double beta = 0.0) {
+                                double* y, cudaStream_t s, double alpha = 1.0, double beta = 0.0,
+                                const double* jd = nullptr, const double* jb = nullptr, double omega = 0.0) {
     const int32_t r0 = c < 0 ? 0 : A->chunk_row[c];
     const int32_t r1 = c < 0 ? A->n_rows : A->chunk_row[c + 1];
     EllArgs e;
@@ -234,6 +235,9 @@ static hec_status launch_chunks(const hec_matrix_s* A, int c, const double* x, c
     e.row_off = A->row_off;
     e.alpha = alpha;
     e.beta = beta;
+    e.diag = jd;  // Jacobi epilogue (whole matrix only: c < 0)
+    e.b = jb;
+    e.omega = omega;
     cudaError_t err = launch_ell(e, s);  // Alg. 1 lines 1-3: ELL first
     if (err != cudaSuccess) return cuda_fail(err, "ell_kernel launch");
     if (A->tail_coo) {                   // HYB comparison variant: COO remainder
@@ -245,6 +249,8 @@ static hec_status launch_chunks(const hec_matrix_s* A, int c, const double* x, c
         k.x = x;
         k.y = y;
         k.alpha = alpha;
+        k.diag = jd;
+        k.omega = omega;
         err = launch_coo(k, s);
         return err == cudaSuccess ? HEC_OK : cuda_fail(err, "coo_kernel launch");
     }
@@ -264,6 +270,8 @@ static hec_status launch_chunks(const hec_matrix_s* A, int c, const double* x, c
         t.n_loc = e.n_loc;
         t.y = y;
         t.alpha = alpha;
+        t.diag = jd;
+        t.omega = omega;
         err = launch_tail(t, s);
         if (err != cudaSuccess) return cuda_fail(err, "tail_kernel launch");
     }
@@ -421,6 +429,40 @@ hec_status hec_spmv_axpby(hec_matrix A, double alpha, const double* x, double be
     if (A->n_rows == 0) return HEC_OK;
     DeviceGuard g(A->device);
     return launch_spmv_axpby(A, alpha, x, beta, y, (cudaStream_t)stream);
+}
+
+static bool overlaps(const void* a, size_t na, const void* b, size_t nb) {
+    const char* pa = static_cast<const char*>(a);
+    const char* pb = static_cast<const char*>(b);
+    return a && b && na && nb && pa < pb + nb && pb < pa + na;
+}
+
+hec_status hec_diag(hec_matrix A, double* d, void* stream) {
+    if (!A) return fail(HEC_ERR_ARG, "NULL matrix");
+    if (A->device < 0) return fail(HEC_ERR_NODEV, "host-only matrix handle (device = -1); no CPU fallback");
+    if (A->n_rows != A->n_cols || A->n_loc >= 0 || A->d_rowmap || A->row_off)
+        return fail(HEC_ERR_DIM, "hec_diag needs a square whole-matrix handle");
+    if (A->n_rows == 0) return HEC_OK;
+    if (!d) return fail(HEC_ERR_ARG, "NULL d");
+    DeviceGuard g(A->device);
+    cudaError_t e = launch_diag(A, d, (cudaStream_t)stream);
+    return e == cudaSuccess ? HEC_OK : cuda_fail(e, "diag kernel launch");
+}
+
+hec_status hec_jacobi(hec_matrix A, const double* d, const double* b, const double* x, double* x_out,
+                      double omega, void* stream) {
+    if (!A) return fail(HEC_ERR_ARG, "NULL matrix");
+    if (A->device < 0) return fail(HEC_ERR_NODEV, "host-only matrix handle (device = -1); no CPU fallback");
+    if (A->n_rows != A->n_cols || A->n_loc >= 0 || A->d_rowmap || A->row_off)
+        return fail(HEC_ERR_DIM, "hec_jacobi needs a square whole-matrix handle");
+    const size_t n = (size_t)A->n_rows;
+    if (n == 0) return HEC_OK;
+    if (!d || !b || !x || !x_out) return fail(HEC_ERR_ARG, "NULL vector");
+    const size_t nb = n * sizeof(double);
+    if (overlaps(x_out, nb, x, nb) || overlaps(x_out, nb, b, nb) || overlaps(x_out, nb, d, nb))
+        return fail(HEC_ERR_ARG, "x_out overlaps x, b or d");
+    DeviceGuard g(A->device);
+    return launch_chunks(A, -1, x, nullptr, x_out, (cudaStream_t)stream, 1.0, 0.0, d, b, omega);
 }
 
 hec_status hec_spmv_host(hec_matrix A, const double* x_host, double* y_host, void* stream) {

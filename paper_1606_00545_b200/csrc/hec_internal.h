@@ -170,6 +170,11 @@ struct EllArgs {
     const int32_t* rowmap;
     int32_t row_off;
     double alpha = 1.0, beta = 0.0;  // Eq. (2): y = alpha A x + beta y
+    // damped-Jacobi epilogue (A22), when diag != null: y = x + omega ((b - A x) / diag),
+    // with x, b, diag indexed by the output row (square, single matrix)
+    const double* diag = nullptr;
+    const double* b = nullptr;
+    double omega = 0.0;
 };
 struct TailArgs {
     const int4* blk;            // block descriptors {first, count, lg, 0}
@@ -183,6 +188,8 @@ struct TailArgs {
     int32_t n_loc;
     double* y;
     double alpha = 1.0;  // the tail adds alpha * (its part of A x)
+    const double* diag = nullptr;  // Jacobi (A22): the tail adds -omega * (its part / diag[row])
+    double omega = 0.0;
 };
 struct CooArgs {               // HYB remainder: row-sorted (row, col, val) triplets
     int64_t nnz;
@@ -192,6 +199,8 @@ struct CooArgs {               // HYB remainder: row-sorted (row, col, val) trip
     const double* x;
     double* y;
     double alpha;
+    const double* diag = nullptr;  // Jacobi (A22): adds -omega * (part / diag[row])
+    double omega = 0.0;
 };
 cudaError_t launch_coo(const CooArgs& a, cudaStream_t s);
 cudaError_t launch_ell(const EllArgs& a, cudaStream_t s);
@@ -199,4 +208,6 @@ cudaError_t launch_tail(const TailArgs& a, cudaStream_t s);
 cudaError_t launch_ell_tma(const EllArgs& a, cudaStream_t s, int num_sms);
 cudaError_t launch_pack(const int32_t* idx, int32_t n, const double* x, double* out,
                         cudaStream_t s);
+// d[i] = A_ii of a square single-device handle: ELL scan, then the tail (CSR or COO)
+cudaError_t launch_diag(const hec_matrix_s* A, double* d, cudaStream_t s);
 }  // namespace hec

@@ -114,10 +114,22 @@ __device__ __forceinline__ double gather_x(const double* __restrict__ x,
 
 // ------------------------------------------------------------- ELL kernel --
 // W > 0: width known at compile time (fully unrolled); W == 0: runtime width.
-// AXPBY: the Eq. (2) epilogue is compiled in only for hec_spmv_axpby (keeping
-// it out of the plain kernel keeps the load schedule of the hot path intact).
-template <int W, bool HALO, bool ROWMAP, bool AXPBY>
+// EPI: the epilogue, compiled in only where it is used (keeping it out of the
+// plain kernel keeps the load schedule of the hot path intact):
+//   EPI_NONE    y = A x                         (hec_spmv)
+//   EPI_AXPBY   y = alpha A x + beta y          (Eq. (2), hec_spmv_axpby)
+//   EPI_JACOBI  y = x + omega ((b - A x) / d)   (damped Jacobi, A22, hec_jacobi)
+enum { EPI_NONE = 0, EPI_AXPBY = 1, EPI_JACOBI = 2 };
+
+// One damped-Jacobi row update, each operation rounded on its own (no FMA
+// contraction), in the oracle's order: r = b - s, q = r / d, x + omega q.
+__device__ __forceinline__ double jacobi_row(double x, double b, double d, double omega, double s) {
+    return __dadd_rn(x, __dmul_rn(omega, __ddiv_rn(__dsub_rn(b, s), d)));
+}
+
+template <int W, bool HALO, bool ROWMAP, int EPI>
 __global__ void __launch_bounds__(256) ell_kernel(EllArgs a) {
+    constexpr bool AXPBY = EPI == EPI_AXPBY;
     // Programmatic dependent launch: the tail kernel may be scheduled once every
     // CTA of this grid has started (it griddepcontrol.waits for this grid's
     // completion before it touches y).  No memory clobber: nothing is ordered
@@ -182,6 +194,12 @@ __global__ void __launch_bounds__(256) ell_kernel(EllArgs a) {
             if (two) st_stream_d1(y1, acc1);
         } else {
             double* yp = a.y + a.row_off + i0;
+            if (EPI == EPI_JACOBI) {  // square single matrix: x, b, d indexed like y
+                const int64_t g = a.row_off + i0;
+                acc0 = jacobi_row(__ldg(a.x + g), __ldg(a.b + g), __ldg(a.diag + g), a.omega, acc0);
+                if (two)
+                    acc1 = jacobi_row(__ldg(a.x + g + 1), __ldg(a.b + g + 1), __ldg(a.diag + g + 1), a.omega, acc1);
+            }
             if (AXPBY && a.beta != 0.0) {
                 acc0 = a.alpha * acc0 + a.beta * yp[0];
                 if (two) acc1 = a.alpha * acc1 + a.beta * yp[1];
@@ -209,7 +227,7 @@ __global__ void __launch_bounds__(256) ell_kernel(EllArgs a) {
 // ELL result (this kernel runs after ell_kernel on the same stream).
 // Blocks of one super-block run back to back, so its entries and the x window
 // they touch are reused in L2.  Fixed reduction order: deterministic.
-template <bool HALO>
+template <bool HALO, bool JACOBI>
 __global__ void __launch_bounds__(256) tail_kernel(TailArgs a) {
     const uint64_t pol = policy_evict_first();
     const int4 d = __ldg(a.blk + a.blk_begin + blockIdx.x);  // {first, count, lg, 0}
@@ -219,11 +237,15 @@ __global__ void __launch_bounds__(256) tail_kernel(TailArgs a) {
     const int grp = threadIdx.x >> lg;
     double acc = 0.0;
     double* yp = nullptr;
+    int32_t orow = 0;
     const bool active = grp < d.y;
     if (active) {
         const int32_t t = d.x + grp;  // device position: the block's rows are contiguous
         const int32_t kb = __ldg(a.ptr + t), ke = __ldg(a.ptr + t + 1);
-        if (lane == 0) yp = a.y + __ldg(a.out_rows + t);
+        if (lane == 0) {
+            orow = __ldg(a.out_rows + t);
+            yp = a.y + orow;
+        }
 #pragma unroll 8
         for (int32_t k = kb + lane; k < ke; k += G) {
             // L1-allocating: the G lanes of a row revisit each 32-byte sector
@@ -238,7 +260,12 @@ __global__ void __launch_bounds__(256) tail_kernel(TailArgs a) {
     // have started before ell_kernel finished, so wait for it here (a no-op
     // when launched normally)
     asm volatile("griddepcontrol.wait;" ::: "memory");
-    if (lane == 0 && active) *yp = *yp + a.alpha * acc;
+    if (lane == 0 && active) {
+        if (JACOBI)  // the ELL kernel wrote x + omega ((b - s_ell) / d): subtract omega (s_tail / d)
+            *yp = __dsub_rn(*yp, __dmul_rn(a.omega, __ddiv_rn(acc, __ldg(a.diag + orow))));
+        else
+            *yp = *yp + a.alpha * acc;
+    }
 }
 
 // ------------------------------------------------------- HYB: COO kernel --
@@ -248,6 +275,10 @@ __global__ void __launch_bounds__(256) tail_kernel(TailArgs a) {
 // y with an fp64 atomic (rows may span lanes and warps; the addition order of
 // those partial sums is not fixed -- parity is within tolerance, exact only in
 // the integer regime).
+__device__ __forceinline__ double coo_part(const CooArgs& a, int32_t row, double acc) {
+    return a.diag ? -__dmul_rn(a.omega, __ddiv_rn(acc, __ldg(a.diag + row))) : a.alpha * acc;
+}
+
 __global__ void __launch_bounds__(256) coo_kernel(CooArgs a) {
     const int64_t k0 = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) * 8;
     if (k0 >= a.nnz) return;
@@ -285,14 +316,14 @@ __global__ void __launch_bounds__(256) coo_kernel(CooArgs a) {
     for (int j = 0; j < 8; ++j) {
         if (j < n) {
             if (row[j] != cur) {
-                atomicAdd(a.y + cur, a.alpha * acc);
+                atomicAdd(a.y + cur, coo_part(a, cur, acc));
                 acc = 0.0;
                 cur = row[j];
             }
             acc = fma(val[j], xg[j], acc);
         }
     }
-    atomicAdd(a.y + cur, a.alpha * acc);
+    atomicAdd(a.y + cur, coo_part(a, cur, acc));
 }
 
 cudaError_t launch_coo(const CooArgs& a, cudaStream_t s) {
@@ -353,7 +384,7 @@ static bool tail_pdl() {
     return v == 1;
 }
 
-template <bool HALO, bool ROWMAP, bool AXPBY>
+template <bool HALO, bool ROWMAP, int EPI>
 static cudaError_t launch_ell_t(const EllArgs& a, cudaStream_t s) {
     const int64_t n_pairs = ((int64_t)a.n_rows + 1) >> 1;
     const int threads = 256;
@@ -367,11 +398,11 @@ static cudaError_t launch_ell_t(const EllArgs& a, cudaStream_t s) {
     const dim3 g((unsigned)blocks), b(threads);
     switch (a.width) {
 #define HEC_W(w) \
-    case w: return launch_k(ell_kernel<w, HALO, ROWMAP, AXPBY>, g, b, s, false, a);
+    case w: return launch_k(ell_kernel<w, HALO, ROWMAP, EPI>, g, b, s, false, a);
         HEC_W(1) HEC_W(2) HEC_W(3) HEC_W(4) HEC_W(5) HEC_W(6) HEC_W(7) HEC_W(8)
         HEC_W(9) HEC_W(10) HEC_W(11) HEC_W(12) HEC_W(13) HEC_W(14) HEC_W(15) HEC_W(16)
 #undef HEC_W
-        default: return launch_k(ell_kernel<0, HALO, ROWMAP, AXPBY>, g, b, s, false, a);
+        default: return launch_k(ell_kernel<0, HALO, ROWMAP, EPI>, g, b, s, false, a);
     }
 }
 
@@ -388,19 +419,23 @@ static int ell_variant() {
 
 cudaError_t launch_ell(const EllArgs& a, cudaStream_t s) {
     if (a.n_rows <= 0) return cudaSuccess;
-    if (ell_variant() == 1 && a.alpha == 1.0 && a.beta == 0.0) {
+    if (ell_variant() == 1 && a.alpha == 1.0 && a.beta == 0.0 && !a.diag) {
         cudaError_t e = launch_ell_tma(a, s, num_sms());
         if (e != cudaErrorNotSupported) return e;
         cudaGetLastError();  // clear the sticky-free "not supported" status
     }
     const bool halo = a.x_halo != nullptr;
     const bool rowmap = a.rowmap != nullptr;
+    if (a.diag) {  // hec_jacobi (single square matrix: no halo, no row map)
+        if (halo || rowmap) return cudaErrorInvalidValue;
+        return launch_ell_t<false, false, EPI_JACOBI>(a, s);
+    }
     if (a.alpha != 1.0 || a.beta != 0.0) {  // hec_spmv_axpby (single matrix: no halo, no row map)
         if (halo || rowmap) return cudaErrorInvalidValue;
-        return launch_ell_t<false, false, true>(a, s);
+        return launch_ell_t<false, false, EPI_AXPBY>(a, s);
     }
-    if (halo) return rowmap ? launch_ell_t<true, true, false>(a, s) : launch_ell_t<true, false, false>(a, s);
-    return rowmap ? launch_ell_t<false, true, false>(a, s) : launch_ell_t<false, false, false>(a, s);
+    if (halo) return rowmap ? launch_ell_t<true, true, EPI_NONE>(a, s) : launch_ell_t<true, false, EPI_NONE>(a, s);
+    return rowmap ? launch_ell_t<false, true, EPI_NONE>(a, s) : launch_ell_t<false, false, EPI_NONE>(a, s);
 }
 
 cudaError_t launch_tail(const TailArgs& a, cudaStream_t s) {
@@ -408,8 +443,12 @@ cudaError_t launch_tail(const TailArgs& a, cudaStream_t s) {
     if (blocks <= 0) return cudaSuccess;
     if (blocks > 0x7fffffff) return cudaErrorInvalidValue;
     const bool pdl = tail_pdl();
-    if (a.x_halo) return launch_k(tail_kernel<true>, dim3((unsigned)blocks), dim3(256), s, pdl, a);
-    return launch_k(tail_kernel<false>, dim3((unsigned)blocks), dim3(256), s, pdl, a);
+    if (a.diag) {
+        if (a.x_halo) return cudaErrorInvalidValue;
+        return launch_k(tail_kernel<false, true>, dim3((unsigned)blocks), dim3(256), s, pdl, a);
+    }
+    if (a.x_halo) return launch_k(tail_kernel<true, false>, dim3((unsigned)blocks), dim3(256), s, pdl, a);
+    return launch_k(tail_kernel<false, false>, dim3((unsigned)blocks), dim3(256), s, pdl, a);
 }
 
 cudaError_t launch_pack(const int32_t* idx, int32_t n, const double* x, double* out,
@@ -418,6 +457,54 @@ cudaError_t launch_pack(const int32_t* idx, int32_t n, const double* x, double* 
     int blocks = (n + 255) / 256;
     if (blocks > num_sms() * 8) blocks = num_sms() * 8;
     pack_kernel<<<blocks, 256, 0, s>>>(idx, n, x, out);
+    return cudaGetLastError();
+}
+
+// ------------------------------------------------------------ diagonal --
+// d[i] = A_ii (A22), setup-time: the ELL slots of row i, then (stream order)
+// the tail rows, which overwrite only where the diagonal spilled.
+__global__ void __launch_bounds__(256) diag_ell_kernel(const int32_t* __restrict__ col,
+                                                       const double* __restrict__ val, int64_t stride,
+                                                       int32_t width, int32_t n, double* __restrict__ d) {
+    for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x) {
+        double v = 0.0;
+        for (int32_t j = 0; j < width; ++j)
+            if (col[j * stride + i] == (int32_t)i) v = val[j * stride + i];
+        d[i] = v;
+    }
+}
+
+__global__ void __launch_bounds__(256) diag_tail_kernel(const int32_t* __restrict__ out_rows,
+                                                        const int32_t* __restrict__ ptr,
+                                                        const int32_t* __restrict__ col,
+                                                        const double* __restrict__ val, int32_t t_rows,
+                                                        double* __restrict__ d) {
+    for (int32_t t = blockIdx.x * blockDim.x + threadIdx.x; t < t_rows; t += gridDim.x * blockDim.x) {
+        const int32_t r = out_rows[t];
+        for (int32_t k = ptr[t]; k < ptr[t + 1]; ++k)
+            if (col[k] == r) d[r] = val[k];
+    }
+}
+
+__global__ void __launch_bounds__(256) diag_coo_kernel(const int32_t* __restrict__ row,
+                                                       const int32_t* __restrict__ col,
+                                                       const double* __restrict__ val, int64_t nnz,
+                                                       double* __restrict__ d) {
+    for (int64_t k = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; k < nnz; k += (int64_t)gridDim.x * blockDim.x)
+        if (row[k] == col[k]) d[row[k]] = val[k];
+}
+
+cudaError_t launch_diag(const hec_matrix_s* A, double* d, cudaStream_t s) {
+    if (A->n_rows <= 0) return cudaSuccess;
+    const int cap = num_sms() * 8;
+    auto grid = [cap](int64_t n) { int64_t g = (n + 255) / 256; return (unsigned)(g < 1 ? 1 : (g > cap ? cap : g)); };
+    diag_ell_kernel<<<grid(A->n_rows), 256, 0, s>>>(A->d_ell_col, A->d_ell_val, A->stride,
+                                                    A->d_ell_col ? A->width : 0, A->n_rows, d);
+    if (A->tail_rows > 0 && A->tail_coo)
+        diag_coo_kernel<<<grid(A->tail_nnz), 256, 0, s>>>(A->d_coo_row, A->d_tail_col, A->d_tail_val, A->tail_nnz, d);
+    else if (A->tail_rows > 0)
+        diag_tail_kernel<<<grid(A->tail_rows), 256, 0, s>>>(A->d_tail_out, A->d_tail_ptr, A->d_tail_col,
+                                                            A->d_tail_val, A->tail_rows, d);
     return cudaGetLastError();
 }
 

@@ -80,7 +80,7 @@ EXPORTED = [
     "hec_plan_export", "hec_plan_part_hec", "hec_plan_free", "hec_nccl_unique_id",
     "hec_dist_create", "hec_dist_create_local", "hec_spmv_dist", "hec_spmv_dist_local",
     "hec_dist_get_info", "hec_dist_free",
-    "hec_spmv_axpby", "hec_axpby", "hec_axpbyz", "hec_dot", "hec_norm2", "hec_bicgstab", "hec_cg",
+    "hec_spmv_axpby", "hec_diag", "hec_jacobi", "hec_axpby", "hec_axpbyz", "hec_dot", "hec_norm2", "hec_bicgstab", "hec_cg",
     "hec_bicgstab_dist", "hec_cg_dist", "hec_from_csr_hyb", "hec_reorder_rcm", "hec_permute",
 ]
 
@@ -162,6 +162,10 @@ def load(build: bool = True):
     L.hec_dist_free.argtypes = [vp]
     L.hec_spmv_axpby.restype = st
     L.hec_spmv_axpby.argtypes = [vp, dbl, vp, dbl, vp, vp]
+    L.hec_diag.restype = st
+    L.hec_diag.argtypes = [vp, vp, vp]
+    L.hec_jacobi.restype = st
+    L.hec_jacobi.argtypes = [vp, vp, vp, vp, vp, dbl, vp]
     L.hec_axpby.restype = st
     L.hec_axpby.argtypes = [i64, dbl, vp, dbl, vp, vp]
     L.hec_axpbyz.restype = st
@@ -308,6 +312,18 @@ class Matrix:
         _check(_lib.hec_spmv_axpby(self._h, float(alpha), _dptr(x, self.n_cols, "x"), float(beta),
                                    _dptr(y, self.n_rows, "y"), _stream_ptr(stream)))
         return y
+
+    def diag(self, d, stream=None):
+        """d[i] = A_ii (+0.0 where row i stores no diagonal entry), on the device."""
+        _check(_lib.hec_diag(self._h, _dptr(d, self.n_rows, "d"), _stream_ptr(stream)))
+        return d
+
+    def jacobi(self, d, b, x, x_out, omega: float, stream=None):
+        """One damped-Jacobi sweep x_out = x + omega D^-1 (b - A x) on the device (A22)."""
+        n = self.n_rows
+        _check(_lib.hec_jacobi(self._h, _dptr(d, n, "d"), _dptr(b, n, "b"), _dptr(x, n, "x"),
+                               _dptr(x_out, n, "x_out"), float(omega), _stream_ptr(stream)))
+        return x_out
 
     def bicgstab(self, b, x, tol: float = 1e-8, max_it: int = 1000, stream=None) -> SolveInfoT:
         """Alg. 4 (unpreconditioned) on the device; x holds x0 on entry."""
