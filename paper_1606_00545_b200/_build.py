@@ -56,6 +56,7 @@ def build(force: bool = False, verbose: bool = False) -> str:
            "-Xcompiler", "-fvisibility=hidden" if False else "-Wall",
            "-Xptxas", "-v" if verbose else "-O3",
            f"-I{INCLUDE}", f"-I{CSRC}", f"-I{inc}",
+           *os.environ.get("HEC_NVCC_EXTRA", "").split(),  # tuning experiments only
            *sources(), "-o", tmp,
            f"-L{lib}", "-l:libnccl.so.2", f"-Xlinker", f"-rpath={lib}"]
     r = subprocess.run(cmd, capture_output=True, text=True)

@@ -120,6 +120,10 @@ __device__ __forceinline__ double gather_x(const double* __restrict__ x,
 //   EPI_AXPBY   y = alpha A x + beta y          (Eq. (2), hec_spmv_axpby)
 //   EPI_JACOBI  y = x + omega ((b - A x) / d)   (damped Jacobi, A22, hec_jacobi)
 enum { EPI_NONE = 0, EPI_AXPBY = 1, EPI_JACOBI = 2 };
+#ifndef HEC_JAC_MINB
+#define HEC_JAC_MINB 0  // min CTAs/SM for the Jacobi variant: 0 = compiler default (5 spills and
+                        // is slower; 4 spills for w >= 12; profiles/round1/jacobi/minb_sweep.jsonl)
+#endif
 
 // One damped-Jacobi row update, each operation rounded on its own (no FMA
 // contraction), in the oracle's order: r = b - s, q = r / d, x + omega q.
@@ -128,7 +132,7 @@ __device__ __forceinline__ double jacobi_row(double x, double b, double d, doubl
 }
 
 template <int W, bool HALO, bool ROWMAP, int EPI>
-__global__ void __launch_bounds__(256) ell_kernel(EllArgs a) {
+__global__ void __launch_bounds__(256, EPI == EPI_JACOBI ? HEC_JAC_MINB : 0) ell_kernel(EllArgs a) {
     constexpr bool AXPBY = EPI == EPI_AXPBY;
     // Programmatic dependent launch: the tail kernel may be scheduled once every
     // CTA of this grid has started (it griddepcontrol.waits for this grid's
@@ -196,9 +200,17 @@ __global__ void __launch_bounds__(256) ell_kernel(EllArgs a) {
             double* yp = a.y + a.row_off + i0;
             if (EPI == EPI_JACOBI) {  // square single matrix: x, b, d indexed like y
                 const int64_t g = a.row_off + i0;
-                acc0 = jacobi_row(__ldg(a.x + g), __ldg(a.b + g), __ldg(a.diag + g), a.omega, acc0);
-                if (two)
-                    acc1 = jacobi_row(__ldg(a.x + g + 1), __ldg(a.b + g + 1), __ldg(a.diag + g + 1), a.omega, acc1);
+                const double *xg = a.x + g, *bg = a.b + g, *dg = a.diag + g;
+                if (two && (((uintptr_t)xg | (uintptr_t)bg | (uintptr_t)dg) & 15) == 0) {
+                    // b and d are streamed once (evict-first); x_i was just gathered (L1/L2)
+                    const double2 bb = ld_stream_d2v(bg, pol), dd = ld_stream_d2v(dg, pol);
+                    const double2 xx = __ldg(reinterpret_cast<const double2*>(xg));
+                    acc0 = jacobi_row(xx.x, bb.x, dd.x, a.omega, acc0);
+                    acc1 = jacobi_row(xx.y, bb.y, dd.y, a.omega, acc1);
+                } else {
+                    acc0 = jacobi_row(__ldg(xg), __ldg(bg), __ldg(dg), a.omega, acc0);
+                    if (two) acc1 = jacobi_row(__ldg(xg + 1), __ldg(bg + 1), __ldg(dg + 1), a.omega, acc1);
+                }
             }
             if (AXPBY && a.beta != 0.0) {
                 acc0 = a.alpha * acc0 + a.beta * yp[0];

@@ -7,10 +7,8 @@ diagonal, omega = 1/2) and, for rows without a tail, wherever the oracle's four
 roundings are the kernel's (integer data, any d, any omega)."""
 import numpy as np
 import pytest
-import scipy.sparse as sp
-import scipy.sparse.linalg as spla
-
 import hecgen
+import oracle
 from oracle import jacobi_ref as J
 
 pytestmark = pytest.mark.gpu
@@ -121,14 +119,14 @@ def test_exact_regime_with_tail_bitwise():
     assert out.cpu().numpy().tobytes() == J.jacobi(A, d, b, x, 0.5).tobytes()
 
 
-def test_sweeps_converge_to_direct_solve():
+def test_sweeps_converge():
     # the smoother as a solver: strictly diagonally dominant power-law matrix
-    # with long rows in the tail; 400 ping-pong sweeps reach A^{-1} b
+    # (d_i = 1 + sum |off|) with long rows in the tail; 400 ping-pong sweeps
+    # drive the residual b - A x (oracle O1) to rounding level
     A = hecgen.powerlaw(1 << 15, lmin=3, lmax=40, band=64, seed=9)
     M = hec.from_csr(A)
     assert M.info.tail_rows > 0
     b = hecgen.vector(A.n_rows, "uniform", seed=10)
-    xs = spla.spsolve(sp.csr_matrix((A.val, A.col, A.row_ptr), shape=(A.n_rows, A.n_cols)).tocsc(), b)
     d = gpu_diag(M, A.n_rows)
     bd = dev(b)
     u, v = torch.zeros(A.n_rows, dtype=torch.float64, device="cuda"), nan_vec(A.n_rows)
@@ -136,7 +134,8 @@ def test_sweeps_converge_to_direct_solve():
         M.jacobi(d, bd, u, v, 1.0)
         u, v = v, u
     torch.cuda.synchronize()
-    assert np.max(np.abs(u.cpu().numpy() - xs)) <= 1e-9 * np.max(np.abs(xs))
+    x = u.cpu().numpy()
+    assert np.max(np.abs(b - oracle.csr_spmv(A, x))) <= 1e-10 * np.max(np.abs(b))
 
 
 def test_errors():
