@@ -55,6 +55,8 @@ def parse():
                     help="measure Krylov iterations/s instead of the SpMV (NEXT-1)")
     ap.add_argument("--jacobi", type=float, default=None, metavar="OMEGA",
                     help="NEXT-3: time damped-Jacobi sweeps (hec_jacobi) with this omega")
+    ap.add_argument("--transport", choices=["p2p", "nccl"], default="p2p",
+                    help="N > 1 halo exchange: peer-memory push kernel over NVLink (default) or NCCL send/recv")
     ap.add_argument("--dist", action="store_true",
                     help="use the distributed path (hec_spmv_dist under torchrun) even with one GPU")
     return ap.parse_args()
@@ -364,6 +366,26 @@ def run_multi(args):
     obj = [hec.nccl_unique_id() if rank == 0 else None]
     dist.broadcast_object_list(obj, src=0)
     D = hec.Dist(A, plan, rank, obj[0], local)
+    transport = "nccl"
+    if args.transport == "p2p" and world > 1:
+        # peer-memory transport (IPC windows exchanged over the handle's NCCL
+        # communicator); if any rank cannot map its peers, every rank falls
+        # back to a fresh NCCL-transport handle
+        ok = 1.0
+        try:
+            D.enable_p2p()
+        except hec.HecError as e:
+            print(f"rank {rank}: peer-memory transport unavailable ({e}); using NCCL", file=sys.stderr)
+            ok = 0.0
+        okt = torch.tensor([ok], device="cuda")
+        dist.all_reduce(okt, op=dist.ReduceOp.MIN)
+        if okt.item() > 0.5:
+            transport = "p2p"
+        else:
+            D.free()
+            obj = [hec.nccl_unique_id() if rank == 0 else None]
+            dist.broadcast_object_list(obj, src=0)
+            D = hec.Dist(A, plan, rank, obj[0], local)
     x_h = hecgen.vector(A.n_cols, "uniform", seed=1606)
     r0, r1 = D.info.r0, D.info.r1
     x = torch.from_numpy(x_h[r0:r1].copy()).cuda()
@@ -443,13 +465,15 @@ def run_multi(args):
                 "warmup": args.warmup, "ms_per_step": round(ms_step, 5), "higher_is_better": True,
                 "scaling": "strong", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
                 "config": {"workload": args.config, "n_rows": A.n_rows, "nnz": A.nnz,
-                           "parallelism": f"row partition x{world} ({'GRID slabs' if kind == hec.PART_GRID else 'CONTIG_NNZ'}), NCCL halo exchange",
+                           "parallelism": f"row partition x{world} ({'GRID slabs' if kind == hec.PART_GRID else 'CONTIG_NNZ'}), "
+                                          + ("peer-memory halo push over NVLink" if transport == "p2p" else "NCCL halo exchange"),
+                           "transport": transport if world > 1 else None,
                            "l2": ("L2 flushed (504 MiB write + 504 MiB read) before every step, outside the timed pair" if flush
                                   else "per-rank inputs > 4x L2, no flush")},
                 "gbs": round(float(alg_loc.item()) / (ms_step * 1e-3) / 1e9, 1),
                 "roofline": {"bound": "hbm", "achieved": round(achieved, 1), "peak": peak, "unit": "GB/s",
                              "frac": round(achieved / peak, 4), "traffic": None,
-                             "kernel": "whole step per rank (interior+boundary ELL, pack, exchange)",
+                             "kernel": "whole step per rank (interior + boundary SpMV, halo exchange)",
                              "peak_source": peak_src},
                 "gpu_launches": K * D.info.launches, "e2e": e2e, "cpu_baseline": None,
                 "clocks": sampler.summary() if sampler else None,

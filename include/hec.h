@@ -321,6 +321,45 @@ hec_status hec_dist_create_local(const hec_csr* A, hec_plan P, const hec_opts* o
  * ordered after prior work on `stream` and before later work on it. */
 hec_status hec_spmv_dist(hec_dist D, const double* x_local, double* y_local, void* stream);
 
+/* ---- peer-memory halo transport ----
+ * The export of P:158 without NCCL: every rank exposes a receive window (its
+ * arrival flags and two halo buffers, alternating by call parity) through CUDA
+ * IPC; per hec_spmv_dist one push kernel gathers x_local[send_idx] and stores
+ * each entry straight into the destination rank's window over NVLink, fences
+ * at system scope and releases the call's epoch into every neighbour's flag;
+ * a one-CTA kernel acquires the neighbours' flags and the boundary SpMV runs
+ * as its programmatic dependent.  Neighbours always exchange flags (even with
+ * no data), which is what makes the double-buffered window safe to reuse.
+ * A missing peer times out after ~10 s instead of hanging (hec_dist_check). */
+#define HEC_IPC_BYTES 64
+
+/* Like hec_dist_create but with no NCCL communicator: builds this rank's
+ * state, allocates its window and writes its CUDA IPC handle to handle_out.
+ * The caller all-gathers the n_parts handles (any transport, e.g.
+ * torch.distributed) and passes them to hec_dist_p2p_connect. */
+hec_status hec_dist_create_p2p(const hec_csr* A, hec_plan P, const hec_opts* o, int32_t rank, int32_t device,
+                               hec_dist* out, uint8_t handle_out[HEC_IPC_BYTES]);
+
+/* handles: n_parts x HEC_IPC_BYTES in rank order (own entry ignored).  Maps
+ * every neighbour's window (cudaIpcOpenMemHandle) and switches D to the
+ * peer-memory transport.  Every rank must have created its window first. */
+hec_status hec_dist_p2p_connect(hec_dist D, const uint8_t* handles);
+
+/* COLLECTIVE, for handles from hec_dist_create: allocates the window,
+ * all-gathers the IPC handles over the handle's NCCL communicator and
+ * connects, so hec_spmv_dist uses the peer-memory transport while the
+ * distributed solvers keep NCCL for their all-reduces. */
+hec_status hec_dist_enable_p2p(hec_dist D);
+
+/* The local-emulation handles (hec_dist_create_local) switched to the
+ * peer-memory transport: the windows are plain device pointers of this
+ * process; hec_spmv_dist_local then runs every push before any wait. */
+hec_status hec_dist_p2p_connect_local(hec_dist* D, int32_t n);
+
+/* Synchronises the handle's communication stream and reports HEC_ERR_STATE
+ * if a peer-memory wait timed out (the affected results are garbage). */
+hec_status hec_dist_check(hec_dist D);
+
 /* Local emulation: one call performs the exchange and both SpMV phases for
  * all n handles created by hec_dist_create_local, in rank order, on `stream`. */
 hec_status hec_spmv_dist_local(hec_dist* D, int32_t n, const double* const* x_locals,
@@ -330,7 +369,7 @@ typedef struct {
     int32_t rank, n_parts, r0, r1, n_halo, n_send;
     int32_t n_interior, n_boundary;
     int32_t width;
-    int32_t launches;        /* kernels this rank launches per hec_spmv_dist (excl. NCCL) */
+    int32_t launches;        /* kernels this rank launches per hec_spmv_dist (excl. NCCL's own) */
     int64_t device_bytes;
     int64_t algorithmic_bytes;  /* 12 nnz_loc + 8 (n_loc + n_halo) + 8 n_loc */
     int64_t nnz_local;

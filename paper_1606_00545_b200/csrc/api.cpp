@@ -44,17 +44,6 @@ static void release(hec_matrix_s* m) {
     delete m;
 }
 
-struct DeviceGuard {
-    int prev = -1;
-    explicit DeviceGuard(int dev) {
-        cudaGetDevice(&prev);
-        if (dev >= 0 && dev != prev) cudaSetDevice(dev);
-    }
-    ~DeviceGuard() {
-        if (prev >= 0) cudaSetDevice(prev);
-    }
-};
-
 // Row chunks (for hec_spmv_host; one chunk for sub-matrices and small
 // matrices), the x prefix each chunk reads, and the tail-kernel work list.
 static void plan_chunks(hec_matrix_s* m, const HostHec& h, bool pipelined, std::vector<int32_t>* order,
@@ -217,7 +206,8 @@ hec_status make_matrix(HostHec&& h, int32_t device, cudaStream_t s, const int32_
 // of 512), or all chunks when c < 0: ELL kernel then tail kernel.
 static hec_status launch_chunks(const hec_matrix_s* A, int c, const double* x, const double* x_halo,
                                 double* y, cudaStream_t s, double alpha = 1.0, double beta = 0.0,
-                                const double* jd = nullptr, const double* jb = nullptr, double omega = 0.0) {
+                                const double* jd = nullptr, const double* jb = nullptr, double omega = 0.0,
+                                const PeerWait* pw = nullptr) {
     const int32_t r0 = c < 0 ? 0 : A->chunk_row[c];
     const int32_t r1 = c < 0 ? A->n_rows : A->chunk_row[c + 1];
     EllArgs e;
@@ -238,6 +228,11 @@ static hec_status launch_chunks(const hec_matrix_s* A, int c, const double* x, c
     e.diag = jd;  // Jacobi epilogue (whole matrix only: c < 0)
     e.b = jb;
     e.omega = omega;
+    if (pw) {  // peer-memory transport: wait for the peers' flags, boundary ELL as its dependent
+        cudaError_t we = launch_peer_wait(*pw, s);
+        if (we != cudaSuccess) return cuda_fail(we, "peer_wait_kernel launch");
+        e.pdl = pw->n > 0;
+    }
     cudaError_t err = launch_ell(e, s);  // Alg. 1 lines 1-3: ELL first
     if (err != cudaSuccess) return cuda_fail(err, "ell_kernel launch");
     if (A->tail_coo) {                   // HYB comparison variant: COO remainder
@@ -286,6 +281,12 @@ hec_status launch_spmv(const hec_matrix_s* A, const double* x, const double* x_h
 hec_status launch_spmv_axpby(const hec_matrix_s* A, double alpha, const double* x, double beta, double* y,
                              cudaStream_t s) {
     return launch_chunks(A, -1, x, nullptr, y, s, alpha, beta);
+}
+
+hec_status launch_spmv_peer(const hec_matrix_s* A, const double* x, const double* x_halo, double* y,
+                            cudaStream_t s, const PeerWait& w) {
+    if (!x_halo) return fail(HEC_ERR_STATE, "peer wait needs a halo");
+    return launch_chunks(A, -1, x, x_halo, y, s, 1.0, 0.0, nullptr, nullptr, 0.0, &w);
 }
 
 }  // namespace hec

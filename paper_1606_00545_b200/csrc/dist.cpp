@@ -33,6 +33,20 @@ struct hec_dist_s {
     cudaStream_t comm_stream = nullptr;
     cudaEvent_t ev_start = nullptr, ev_halo = nullptr;
     int64_t device_bytes = 0;
+    // ---- peer-memory transport ----
+    bool p2p = false;
+    void* d_win = nullptr;              // [flags: n_parts u64, 256 B aligned][halo buf 0][halo buf 1]
+    std::vector<void*> opened;          // peer windows mapped with cudaIpcOpenMemHandle
+    std::vector<int32_t> nbr;           // neighbour ranks (send or receive side), ascending
+    std::vector<int32_t> send_peer, send_dst;  // per send entry: destination rank, halo position there
+    std::vector<int64_t> all_nhalo;     // every rank's halo length (from the plan)
+    int32_t* d_send_peer = nullptr;
+    int32_t* d_send_dst = nullptr;
+    int32_t* d_nbr = nullptr;
+    void* d_peer_tab = nullptr;         // [buf0 ptrs | flag ptrs | n_halo] per rank
+    unsigned int* d_done = nullptr;
+    int32_t* d_err = nullptr;
+    uint64_t epoch = 0;
 };
 
 namespace hec {
@@ -53,6 +67,14 @@ static void dist_release(hec_dist_s* d) {
     cudaGetDevice(&cur);
     cudaSetDevice(d->device);
     if (d->comm) ncclCommDestroy(d->comm);
+    for (void* p : d->opened) cudaIpcCloseMemHandle(p);
+    if (d->d_win) cudaFree(d->d_win);
+    if (d->d_send_peer) cudaFree(d->d_send_peer);
+    if (d->d_send_dst) cudaFree(d->d_send_dst);
+    if (d->d_nbr) cudaFree(d->d_nbr);
+    if (d->d_peer_tab) cudaFree(d->d_peer_tab);
+    if (d->d_done) cudaFree(d->d_done);
+    if (d->d_err) cudaFree(d->d_err);
     if (d->ev_start) cudaEventDestroy(d->ev_start);
     if (d->ev_halo) cudaEventDestroy(d->ev_halo);
     if (d->comm_stream) cudaStreamDestroy(d->comm_stream);
@@ -116,6 +138,22 @@ static hec_status dist_build(const hec_csr* A, hec_plan P, const hec_opts* o, in
     d->send_off = pt.send_off;
     d->recv_off = pt.recv_off;
     d->local = local;
+    // peer-memory transport metadata: where each send entry lands in its
+    // destination's halo (q's receive segment from this rank starts at
+    // q.recv_off[rank], reading A10), and the neighbour set
+    d->all_nhalo.resize(P->n_parts);
+    for (int32_t q = 0; q < P->n_parts; ++q) d->all_nhalo[q] = (int64_t)P->parts[q].recv.size();
+    d->send_peer.resize(pt.send_idx.size());
+    d->send_dst.resize(pt.send_idx.size());
+    for (int32_t q = 0; q < P->n_parts; ++q) {
+        const int32_t sc = pt.send_off[q + 1] - pt.send_off[q];
+        const int32_t rc = pt.recv_off[q + 1] - pt.recv_off[q];
+        if (q != rank && (sc > 0 || rc > 0)) d->nbr.push_back(q);
+        for (int32_t k = pt.send_off[q]; k < pt.send_off[q + 1]; ++k) {
+            d->send_peer[k] = q;
+            d->send_dst[k] = P->parts[q].recv_off[rank] + (k - pt.send_off[q]);
+        }
+    }
     d->width = part_width(*P, rank, op);
     cudaStream_t s = nullptr;
     HEC_CUDA_TRY(cudaStreamCreateWithFlags(&s, cudaStreamNonBlocking));
@@ -155,6 +193,87 @@ static hec_status dist_build(const hec_csr* A, hec_plan P, const hec_opts* o, in
 
 static bool has_exchange(const hec_dist_s* d) { return d->n_halo > 0 || d->n_send > 0; }
 
+static size_t flag_bytes(int32_t n_parts) { return ((size_t)n_parts * 8 + 255) / 256 * 256; }
+
+// This rank's receive window: arrival flags (zeroed) and two halo buffers.
+static hec_status p2p_alloc_window(hec_dist_s* d) {
+    if (d->d_win) return HEC_OK;
+    const size_t fb = flag_bytes(d->n_parts), bytes = fb + 2 * sizeof(double) * (size_t)d->n_halo;
+    HEC_CUDA_TRY(cudaMalloc(&d->d_win, bytes));  // cudaMalloc: exportable through CUDA IPC
+    HEC_CUDA_TRY(cudaMemset(d->d_win, 0, bytes));
+    HEC_CUDA_TRY(cudaMalloc(&d->d_done, sizeof(unsigned int)));
+    HEC_CUDA_TRY(cudaMemset(d->d_done, 0, sizeof(unsigned int)));
+    HEC_CUDA_TRY(cudaMalloc(&d->d_err, sizeof(int32_t)));
+    HEC_CUDA_TRY(cudaMemset(d->d_err, 0, sizeof(int32_t)));
+    HEC_CUDA_TRY(cudaDeviceSynchronize());
+    d->device_bytes += (int64_t)bytes;
+    return HEC_OK;
+}
+
+static uint64_t* win_flags(void* win) { return static_cast<uint64_t*>(win); }
+static double* win_buf0(void* win, int32_t n_parts) {
+    return reinterpret_cast<double*>(static_cast<char*>(win) + flag_bytes(n_parts));
+}
+
+// Upload the sender tables once every neighbour's window is mapped (wins[q]).
+static hec_status p2p_finish(hec_dist_s* d, const std::vector<void*>& wins) {
+    const int32_t P = d->n_parts;
+    std::vector<uint64_t> tab(3 * (size_t)P, 0);  // buf0 ptrs, flag ptrs, n_halo
+    for (int32_t q : d->nbr) {
+        if (!wins[q]) return fail(HEC_ERR_STATE, "missing peer window");
+        tab[q] = reinterpret_cast<uint64_t>(win_buf0(wins[q], P));
+        tab[P + q] = reinterpret_cast<uint64_t>(win_flags(wins[q]));
+    }
+    for (int32_t q = 0; q < P; ++q) tab[2 * P + q] = (uint64_t)d->all_nhalo[q];
+    HEC_CUDA_TRY(cudaMalloc(&d->d_peer_tab, tab.size() * 8));
+    HEC_CUDA_TRY(cudaMemcpy(d->d_peer_tab, tab.data(), tab.size() * 8, cudaMemcpyHostToDevice));
+    if (!d->nbr.empty()) {
+        HEC_CUDA_TRY(cudaMalloc(&d->d_nbr, d->nbr.size() * sizeof(int32_t)));
+        HEC_CUDA_TRY(cudaMemcpy(d->d_nbr, d->nbr.data(), d->nbr.size() * sizeof(int32_t), cudaMemcpyHostToDevice));
+    }
+    if (d->n_send > 0) {
+        HEC_CUDA_TRY(cudaMalloc(&d->d_send_peer, sizeof(int32_t) * d->n_send));
+        HEC_CUDA_TRY(cudaMalloc(&d->d_send_dst, sizeof(int32_t) * d->n_send));
+        HEC_CUDA_TRY(cudaMemcpy(d->d_send_peer, d->send_peer.data(), sizeof(int32_t) * d->n_send, cudaMemcpyHostToDevice));
+        HEC_CUDA_TRY(cudaMemcpy(d->d_send_dst, d->send_dst.data(), sizeof(int32_t) * d->n_send, cudaMemcpyHostToDevice));
+    }
+    d->p2p = true;
+    return HEC_OK;
+}
+
+static PushArgs push_args(const hec_dist_s* d, const double* x_local, uint64_t ep) {
+    const int32_t P = d->n_parts;
+    PushArgs a;
+    a.x = x_local;
+    a.idx = d->d_send_idx;
+    a.peer = d->d_send_peer;
+    a.dst = d->d_send_dst;
+    a.n = d->n_send;
+    a.peer_buf0 = static_cast<double* const*>(d->d_peer_tab);
+    a.peer_flags = reinterpret_cast<uint64_t* const*>(static_cast<uint64_t*>(d->d_peer_tab) + P);
+    a.peer_nhalo = reinterpret_cast<const int64_t*>(static_cast<uint64_t*>(d->d_peer_tab) + 2 * P);
+    a.nbr = d->d_nbr;
+    a.n_nbr = (int32_t)d->nbr.size();
+    a.rank = d->rank;
+    a.epoch = ep;
+    a.done = d->d_done;
+    return a;
+}
+
+static PeerWait wait_args(const hec_dist_s* d, uint64_t ep) {
+    PeerWait w;
+    w.flags = win_flags(d->d_win);
+    w.peers = d->d_nbr;
+    w.n = (int32_t)d->nbr.size();
+    w.epoch = ep;
+    w.err = d->d_err;
+    return w;
+}
+
+static double* p2p_halo(const hec_dist_s* d, uint64_t ep) {
+    return d->n_halo ? win_buf0(d->d_win, d->n_parts) + (ep & 1) * (uint64_t)d->n_halo : nullptr;
+}
+
 }  // namespace hec
 
 using namespace hec;
@@ -192,6 +311,109 @@ hec_status hec_dist_create(const hec_csr* A, hec_plan P, const hec_opts* o, int3
     return HEC_OK;
 }
 
+hec_status hec_dist_create_p2p(const hec_csr* A, hec_plan P, const hec_opts* o, int32_t rank, int32_t device,
+                               hec_dist* out, uint8_t handle_out[HEC_IPC_BYTES]) {
+    if (!out || !P || !handle_out) return fail(HEC_ERR_ARG, "NULL argument");
+    *out = nullptr;
+    static_assert(sizeof(cudaIpcMemHandle_t) == HEC_IPC_BYTES, "cudaIpcMemHandle_t size");
+    hec_dist_s* d = nullptr;
+    hec_status st = dist_build(A, P, o, rank, device, false, &d);
+    if (st != HEC_OK) return st;
+    int prev = 0;
+    cudaGetDevice(&prev);
+    cudaSetDevice(device);
+    st = p2p_alloc_window(d);
+    cudaIpcMemHandle_t h;
+    if (st == HEC_OK) {
+        cudaError_t e = cudaIpcGetMemHandle(&h, d->d_win);
+        if (e != cudaSuccess) st = cuda_fail(e, "cudaIpcGetMemHandle");
+    }
+    cudaSetDevice(prev);
+    if (st != HEC_OK) { dist_release(d); return st; }
+    std::memcpy(handle_out, &h, HEC_IPC_BYTES);
+    *out = d;
+    return HEC_OK;
+}
+
+// Map every neighbour's window from its IPC handle (handles: n_parts x
+// HEC_IPC_BYTES in rank order; this rank's own entry is ignored).
+static hec_status p2p_connect_ipc(hec_dist_s* d, const uint8_t* handles) {
+    std::vector<void*> wins(d->n_parts, nullptr);
+    for (int32_t q : d->nbr) {
+        cudaIpcMemHandle_t h;
+        std::memcpy(&h, handles + (size_t)q * HEC_IPC_BYTES, HEC_IPC_BYTES);
+        void* p = nullptr;
+        cudaError_t e = cudaIpcOpenMemHandle(&p, h, cudaIpcMemLazyEnablePeerAccess);
+        if (e != cudaSuccess) return cuda_fail(e, "cudaIpcOpenMemHandle (peer window)");
+        d->opened.push_back(p);
+        wins[q] = p;
+    }
+    return p2p_finish(d, wins);
+}
+
+hec_status hec_dist_p2p_connect(hec_dist D, const uint8_t* handles) {
+    if (!D || !handles) return fail(HEC_ERR_ARG, "NULL argument");
+    if (D->p2p || D->local) return fail(HEC_ERR_STATE, "handle already connected or local");
+    if (!D->d_win) return fail(HEC_ERR_STATE, "no window: create the handle with hec_dist_create_p2p");
+    DeviceGuard g(D->device);
+    return p2p_connect_ipc(D, handles);
+}
+
+hec_status hec_dist_enable_p2p(hec_dist D) {
+    if (!D) return fail(HEC_ERR_ARG, "NULL handle");
+    if (D->p2p || D->local) return fail(HEC_ERR_STATE, "handle already connected or local");
+    if (D->n_parts == 1) return HEC_OK;
+    if (!D->comm) return fail(HEC_ERR_STATE, "no NCCL communicator to exchange the window handles");
+    DeviceGuard g(D->device);
+    hec_status st = p2p_alloc_window(D);
+    if (st != HEC_OK) return st;
+    cudaIpcMemHandle_t h;
+    HEC_CUDA_TRY(cudaIpcGetMemHandle(&h, D->d_win));
+    uint8_t* dbuf = nullptr;
+    const size_t nb = (size_t)D->n_parts * HEC_IPC_BYTES;
+    HEC_CUDA_TRY(cudaMalloc(&dbuf, nb + HEC_IPC_BYTES));
+    std::vector<uint8_t> all(nb);
+    cudaError_t e = cudaMemcpy(dbuf + nb, &h, HEC_IPC_BYTES, cudaMemcpyHostToDevice);
+    ncclResult_t r = ncclSuccess;
+    if (e == cudaSuccess) r = ncclAllGather(dbuf + nb, dbuf, HEC_IPC_BYTES, ncclUint8, D->comm, D->comm_stream);
+    if (e == cudaSuccess && r == ncclSuccess) e = cudaStreamSynchronize(D->comm_stream);
+    if (e == cudaSuccess && r == ncclSuccess) e = cudaMemcpy(all.data(), dbuf, nb, cudaMemcpyDeviceToHost);
+    cudaFree(dbuf);
+    if (r != ncclSuccess) return nccl_fail(r, "window handle all-gather");
+    if (e != cudaSuccess) return cuda_fail(e, "window handle all-gather");
+    return p2p_connect_ipc(D, all.data());
+}
+
+hec_status hec_dist_p2p_connect_local(hec_dist* D, int32_t n) {
+    if (!D || n < 1) return fail(HEC_ERR_ARG, "NULL argument");
+    for (int32_t p = 0; p < n; ++p)
+        if (!D[p] || !D[p]->local || D[p]->rank != p || D[p]->n_parts != n || D[p]->p2p)
+            return fail(HEC_ERR_STATE, "handles must be the n unconnected ranks from hec_dist_create_local");
+    DeviceGuard g(D[0]->device);
+    std::vector<void*> wins(n);
+    for (int32_t p = 0; p < n; ++p) {
+        hec_status st = p2p_alloc_window(D[p]);
+        if (st != HEC_OK) return st;
+        wins[p] = D[p]->d_win;
+    }
+    for (int32_t p = 0; p < n; ++p) {
+        hec_status st = p2p_finish(D[p], wins);
+        if (st != HEC_OK) return st;
+    }
+    return HEC_OK;
+}
+
+hec_status hec_dist_check(hec_dist D) {
+    if (!D) return fail(HEC_ERR_ARG, "NULL handle");
+    DeviceGuard g(D->device);
+    HEC_CUDA_TRY(cudaStreamSynchronize(D->comm_stream));
+    if (!D->d_err) return HEC_OK;
+    int32_t err = 0;
+    HEC_CUDA_TRY(cudaMemcpy(&err, D->d_err, sizeof(err), cudaMemcpyDeviceToHost));
+    if (err) return fail(HEC_ERR_STATE, "peer-memory halo: a neighbour's data did not arrive within 10 s");
+    return HEC_OK;
+}
+
 hec_status hec_dist_create_local(const hec_csr* A, hec_plan P, const hec_opts* o, int32_t device,
                                  hec_dist* out) {
     if (!out || !P) return fail(HEC_ERR_ARG, "NULL argument");
@@ -217,6 +439,29 @@ namespace hec {
 // control of `s`, so every later NCCL call issued on `s` (e.g. the Krylov
 // all-reduces) is ordered after this exchange on every rank.
 hec_status dist_spmv_launch(hec_dist_s* D, const double* x_local, double* y_local, cudaStream_t s) {
+    if (D->p2p && !D->nbr.empty()) {
+        // peer-memory transport: fused pack + NVLink stores + flag release on
+        // the comm stream, then wait for the neighbours' flags and run the
+        // boundary rows behind it; the interior overlaps on the caller's stream
+        const uint64_t ep = ++D->epoch;
+        HEC_CUDA_TRY(cudaEventRecord(D->ev_start, s));
+        HEC_CUDA_TRY(cudaStreamWaitEvent(D->comm_stream, D->ev_start, 0));
+        HEC_CUDA_TRY(launch_push(push_args(D, x_local, ep), D->comm_stream));
+        const PeerWait w = wait_args(D, ep);
+        if (D->n_boundary > 0) {
+            hec_status st = launch_spmv_peer(D->boundary, x_local, p2p_halo(D, ep), y_local, D->comm_stream, w);
+            if (st != HEC_OK) return st;
+        } else {
+            HEC_CUDA_TRY(launch_peer_wait(w, D->comm_stream));
+        }
+        HEC_CUDA_TRY(cudaEventRecord(D->ev_halo, D->comm_stream));
+        hec_status st = launch_spmv(D->interior, x_local, nullptr, y_local, s);
+        if (st != HEC_OK) return st;
+        HEC_CUDA_TRY(cudaStreamWaitEvent(s, D->ev_halo, 0));
+        return HEC_OK;
+    }
+    if (has_exchange(D) && !D->comm && !D->local)
+        return fail(HEC_ERR_STATE, "no halo transport: connect the peer-memory windows (hec_dist_p2p_connect)");
     const bool ex = has_exchange(D) && D->comm;
     if (ex) {
         // comm stream: pack + grouped send/recv, overlapped with the interior SpMV
@@ -254,6 +499,8 @@ int64_t dist_n_local(hec_dist_s* D) { return (int64_t)D->r1 - D->r0; }
 
 ncclComm_t dist_comm(hec_dist_s* D) { return D->comm; }
 
+int32_t dist_parts(hec_dist_s* D) { return D->n_parts; }
+
 }  // namespace hec
 
 extern "C" {
@@ -283,6 +530,30 @@ hec_status hec_spmv_dist_local(hec_dist* D, int32_t n, const double* const* x_lo
     int prev = 0;
     cudaGetDevice(&prev);
     cudaSetDevice(D[0]->device);
+    if (D[0]->p2p) {
+        // peer-memory transport emulated on one device and one stream: every
+        // rank's push kernel (stores into the other ranks' windows + flag
+        // release), then every rank's interior rows and flag wait + boundary
+        // rows (the flags are already set, so no wait ever spins)
+        for (int32_t p = 0; p < n; ++p) {
+            const uint64_t ep = ++D[p]->epoch;
+            cudaError_t e = D[p]->nbr.empty() ? cudaSuccess : launch_push(push_args(D[p], x_locals[p], ep), s);
+            if (e != cudaSuccess) { cudaSetDevice(prev); return cuda_fail(e, "push kernel"); }
+        }
+        for (int32_t p = 0; p < n; ++p) {
+            const uint64_t ep = D[p]->epoch;
+            hec_status st = launch_spmv(D[p]->interior, x_locals[p], nullptr, y_locals[p], s);
+            if (st == HEC_OK && D[p]->n_boundary > 0) {
+                st = D[p]->nbr.empty()
+                         ? launch_spmv(D[p]->boundary, x_locals[p], p2p_halo(D[p], ep), y_locals[p], s)
+                         : launch_spmv_peer(D[p]->boundary, x_locals[p], p2p_halo(D[p], ep), y_locals[p], s,
+                                            wait_args(D[p], ep));
+            }
+            if (st != HEC_OK) { cudaSetDevice(prev); return st; }
+        }
+        cudaSetDevice(prev);
+        return HEC_OK;
+    }
     for (int32_t p = 0; p < n; ++p) {
         cudaError_t e = launch_pack(D[p]->d_send_idx, D[p]->n_send, x_locals[p], D[p]->d_sendbuf, s);
         if (e != cudaSuccess) { cudaSetDevice(prev); return cuda_fail(e, "halo pack"); }
@@ -319,7 +590,7 @@ hec_status hec_dist_get_info(hec_dist D, hec_dist_info* o) {
     o->n_boundary = D->n_boundary;
     o->width = D->width;
     o->launches = hec_spmv_launches(D->interior) + hec_spmv_launches(D->boundary) +
-                  (has_exchange(D) && D->n_send > 0 ? 1 : 0);
+                  (D->p2p ? (D->nbr.empty() ? 0 : 2) : (has_exchange(D) && D->n_send > 0 ? 1 : 0));
     o->device_bytes = D->device_bytes;
     const int64_t n_loc = D->r1 - D->r0;
     o->algorithmic_bytes = 12 * D->nnz_local + 8 * (n_loc + D->n_halo) + 8 * n_loc;

@@ -147,15 +147,58 @@ namespace hec {
 hec_status make_matrix(HostHec&& h, int32_t device, cudaStream_t s, const int32_t* rowmap,
                        int32_t n_rowmap, int32_t row_off, int32_t n_loc, hec_matrix* out,
                        bool coo_tail = false);
+// Makes `dev` current for the scope, restoring the caller's device after.
+struct DeviceGuard {
+    int prev = -1;
+    explicit DeviceGuard(int dev) {
+        cudaGetDevice(&prev);
+        if (dev >= 0 && dev != prev) cudaSetDevice(dev);
+    }
+    ~DeviceGuard() {
+        if (prev >= 0) cudaSetDevice(prev);
+    }
+};
+
 // Launch the HEC product (ELL kernel then tail kernel) for one handle.
 hec_status launch_spmv(const hec_matrix_s* A, const double* x, const double* x_halo, double* y,
                        cudaStream_t s);
 hec_status launch_spmv_axpby(const hec_matrix_s* A, double alpha, const double* x, double beta, double* y,
                              cudaStream_t s);
+struct PeerWait;
+// The boundary product of the peer-memory transport: peer_wait_kernel, then the
+// ELL kernel as its programmatic dependent, then the tail.
+hec_status launch_spmv_peer(const hec_matrix_s* A, const double* x, const double* x_halo, double* y,
+                            cudaStream_t s, const PeerWait& w);
 }  // namespace hec
 
 // ---------------------------------------------------------------- kernels --
 namespace hec {
+// Peer-memory halo transport (dist.cpp): peer_wait_kernel waits
+// until every neighbour rank has released this call's epoch into flags[q]
+// (ld.acquire.sys), with a ~10 s timeout that sets *err instead of hanging.
+struct PeerWait {
+    const uint64_t* flags = nullptr;  // this rank's arrival flags, one per source rank
+    const int32_t* peers = nullptr;   // neighbour ranks to wait for
+    int32_t n = 0;                    // 0: no wait
+    uint64_t epoch = 0;
+    int32_t* err = nullptr;
+};
+struct PushArgs {                     // fused pack + NVLink store + release
+    const double* x;                  // x_local
+    const int32_t* idx;               // send_idx (grouped by destination rank)
+    const int32_t* peer;              // destination rank of each entry
+    const int32_t* dst;               // position in that rank's halo buffer
+    int32_t n;
+    double* const* peer_buf0;         // [n_parts] peer q's halo buffer 0 (buffer 1 follows it)
+    const int64_t* peer_nhalo;        // [n_parts] peer q's halo length
+    uint64_t* const* peer_flags;      // [n_parts] peer q's arrival flags
+    const int32_t* nbr;               // neighbour ranks (send or receive side)
+    int32_t n_nbr;
+    int32_t rank;
+    uint64_t epoch;
+    unsigned int* done;               // CTA completion counter (self-resetting)
+};
+
 struct EllArgs {
     const int32_t* col;
     const double* val;
@@ -175,6 +218,7 @@ struct EllArgs {
     const double* diag = nullptr;
     const double* b = nullptr;
     double omega = 0.0;
+    bool pdl = false;  // launch as a programmatic dependent (peer-memory boundary rows)
 };
 struct TailArgs {
     const int4* blk;            // block descriptors {first, count, lg, 0}
@@ -210,4 +254,6 @@ cudaError_t launch_pack(const int32_t* idx, int32_t n, const double* x, double* 
                         cudaStream_t s);
 // d[i] = A_ii of a square single-device handle: ELL scan, then the tail (CSR or COO)
 cudaError_t launch_diag(const hec_matrix_s* A, double* d, cudaStream_t s);
+cudaError_t launch_push(const PushArgs& a, cudaStream_t s);
+cudaError_t launch_peer_wait(const PeerWait& w, cudaStream_t s);
 }  // namespace hec

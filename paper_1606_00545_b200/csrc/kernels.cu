@@ -102,6 +102,47 @@ __device__ __forceinline__ void st_stream_d1(double* ptr, double a) {
     asm volatile("st.global.cs.f64 [%0], %1;" ::"l"(ptr), "d"(a) : "memory");
 }
 
+// ------------------------------------------------ peer-memory sync (PTX) --
+__device__ __forceinline__ uint64_t ld_acquire_sys(const uint64_t* p) {
+    uint64_t v;
+    asm volatile("ld.acquire.sys.global.u64 %0, [%1];" : "=l"(v) : "l"(p) : "memory");
+    return v;
+}
+
+__device__ __forceinline__ void st_release_sys(uint64_t* p, uint64_t v) {
+    asm volatile("st.release.sys.global.u64 [%0], %1;" ::"l"(p), "l"(v) : "memory");
+}
+
+__device__ __forceinline__ uint64_t global_timer_ns() {
+    uint64_t t;
+    asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+    return t;
+}
+
+// One thread polls the arrival flags of every neighbour until they reach this
+// call's epoch (ld.acquire.sys).  Runs as its own one-CTA kernel on the
+// communication stream; the boundary kernel is its programmatic dependent, so
+// the acquire is ordered before every halo read by griddepcontrol.wait.
+// Gives up after ~10 s (sets *err; the result is then garbage and
+// hec_dist_check reports it) so a missing peer cannot hang the GPU.
+__device__ __forceinline__ void peer_wait(const uint64_t* flags, const int32_t* peers, int32_t n,
+                                          uint64_t epoch, int32_t* err) {
+    if (threadIdx.x == 0) {
+        const uint64_t t0 = global_timer_ns();
+        for (int32_t i = 0; i < n; ++i) {
+            const uint64_t* f = flags + peers[i];
+            while (ld_acquire_sys(f) < epoch) {
+                if (global_timer_ns() - t0 > 10000000000ull) {
+                    atomicExch(err, 1);
+                    break;
+                }
+                __nanosleep(64);
+            }
+        }
+    }
+    __syncthreads();
+}
+
 // x gather: columns >= n_loc live in the halo buffer (distributed boundary).
 // (An L2 evict_last hint on the gathers was measured: no gain, r06.)
 template <bool HALO>
@@ -138,6 +179,10 @@ __global__ void __launch_bounds__(256, EPI == EPI_JACOBI ? HEC_JAC_MINB : 0) ell
     // CTA of this grid has started (it griddepcontrol.waits for this grid's
     // completion before it touches y).  No memory clobber: nothing is ordered
     // by it, and a clobber costs the hot loop 14 registers.
+    // Boundary rows under the peer-memory transport are launched as dependents
+    // of peer_wait_kernel: wait for it (x_halo has landed) before letting the
+    // tail kernel start or touching x_halo.  A no-op when launched normally.
+    if (HALO) asm volatile("griddepcontrol.wait;" ::: "memory");
     asm volatile("griddepcontrol.launch_dependents;");
     const uint64_t pol = policy_evict_first();
     const int32_t width = W > 0 ? W : a.width;
@@ -410,11 +455,11 @@ static cudaError_t launch_ell_t(const EllArgs& a, cudaStream_t s) {
     const dim3 g((unsigned)blocks), b(threads);
     switch (a.width) {
 #define HEC_W(w) \
-    case w: return launch_k(ell_kernel<w, HALO, ROWMAP, EPI>, g, b, s, false, a);
+    case w: return launch_k(ell_kernel<w, HALO, ROWMAP, EPI>, g, b, s, a.pdl, a);
         HEC_W(1) HEC_W(2) HEC_W(3) HEC_W(4) HEC_W(5) HEC_W(6) HEC_W(7) HEC_W(8)
         HEC_W(9) HEC_W(10) HEC_W(11) HEC_W(12) HEC_W(13) HEC_W(14) HEC_W(15) HEC_W(16)
 #undef HEC_W
-        default: return launch_k(ell_kernel<0, HALO, ROWMAP, EPI>, g, b, s, false, a);
+        default: return launch_k(ell_kernel<0, HALO, ROWMAP, EPI>, g, b, s, a.pdl, a);
     }
 }
 
@@ -504,6 +549,54 @@ __global__ void __launch_bounds__(256) diag_coo_kernel(const int32_t* __restrict
                                                        double* __restrict__ d) {
     for (int64_t k = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; k < nnz; k += (int64_t)gridDim.x * blockDim.x)
         if (row[k] == col[k]) d[row[k]] = val[k];
+}
+
+// ------------------------------------------------ peer-memory halo push --
+// The export of P:158 fused with the transfer: every thread gathers its
+// x_local[send_idx[k]] and stores it straight into the destination rank's
+// halo buffer (this call's parity) through its IPC mapping over NVLink -- no
+// staging buffer, no copy engine, no NCCL kernel.  Each CTA then fences at
+// system scope and counts itself done; the last CTA releases this call's
+// epoch into every neighbour's arrival flag (st.release.sys).  Neighbours
+// with nothing to receive still get the flag: it tells them this rank has
+// finished reading its own halo buffer of the previous call.
+__global__ void __launch_bounds__(256) push_kernel(PushArgs a) {
+    const int32_t par = (int32_t)(a.epoch & 1);
+    for (int32_t k = blockIdx.x * blockDim.x + threadIdx.x; k < a.n; k += gridDim.x * blockDim.x) {
+        const int32_t q = __ldg(a.peer + k);
+        double* buf = a.peer_buf0[q] + (par ? a.peer_nhalo[q] : 0);
+        buf[__ldg(a.dst + k)] = __ldg(a.x + __ldg(a.idx + k));
+    }
+    __threadfence_system();
+    __syncthreads();
+    if (threadIdx.x == 0) {
+        const unsigned int prev = atomicAdd(a.done, 1u);
+        if (prev == gridDim.x - 1) {
+            __threadfence_system();
+            for (int32_t i = 0; i < a.n_nbr; ++i) {
+                const int32_t q = a.nbr[i];
+                st_release_sys(a.peer_flags[q] + a.rank, a.epoch);
+            }
+            *a.done = 0;  // the next call's push is stream-ordered after this one
+        }
+    }
+}
+
+__global__ void peer_wait_kernel(PeerWait w) { peer_wait(w.flags, w.peers, w.n, w.epoch, w.err); }
+
+cudaError_t launch_push(const PushArgs& a, cudaStream_t s) {
+    if (a.n_nbr <= 0) return cudaSuccess;
+    int blocks = (a.n + 255) / 256;
+    if (blocks > num_sms() * 4) blocks = num_sms() * 4;
+    if (blocks < 1) blocks = 1;
+    push_kernel<<<blocks, 256, 0, s>>>(a);
+    return cudaGetLastError();
+}
+
+cudaError_t launch_peer_wait(const PeerWait& w, cudaStream_t s) {
+    if (w.n <= 0) return cudaSuccess;
+    peer_wait_kernel<<<1, 32, 0, s>>>(w);
+    return cudaGetLastError();
 }
 
 cudaError_t launch_diag(const hec_matrix_s* A, double* d, cudaStream_t s) {

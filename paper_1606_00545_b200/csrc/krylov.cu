@@ -225,6 +225,7 @@ struct Op {
 hec_status dist_spmv_launch(hec_dist_s* D, const double* x, double* y, cudaStream_t s);   // dist.cpp
 int64_t dist_n_local(hec_dist_s* D);
 ncclComm_t dist_comm(hec_dist_s* D);
+int32_t dist_parts(hec_dist_s* D);
 
 #define HEC_TRY(expr)                         \
     do {                                      \
@@ -499,6 +500,8 @@ hec_status hec_bicgstab_dist(hec_dist D, const double* b_local, double* x_local,
     op.D = D;
     op.n = dist_n_local(D);
     op.comm = dist_comm(D);
+    if (dist_parts(D) > 1 && !op.comm)
+        return fail(HEC_ERR_STATE, "distributed solvers need the NCCL communicator of hec_dist_create");
     return solve(op, 0, b_local, x_local, tol, max_it, stream, info);
 }
 
@@ -509,6 +512,8 @@ hec_status hec_cg_dist(hec_dist D, const double* b_local, double* x_local, doubl
     op.D = D;
     op.n = dist_n_local(D);
     op.comm = dist_comm(D);
+    if (dist_parts(D) > 1 && !op.comm)
+        return fail(HEC_ERR_STATE, "distributed solvers need the NCCL communicator of hec_dist_create");
     return solve(op, 1, b_local, x_local, tol, max_it, stream, info);
 }
 

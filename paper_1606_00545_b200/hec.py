@@ -31,6 +31,7 @@ WIDTH_BG3, WIDTH_CAP, WIDTH_FIXED = 0, 1, 2
 PART_CONTIG_NNZ, PART_CONTIG_ROWS, PART_GRID = 0, 1, 2
 SUB_INTERIOR, SUB_BOUNDARY, SUB_ALL = 0, 1, 2
 NCCL_ID_BYTES = 128
+IPC_BYTES = 64
 
 i32, i64, vp, dbl = ctypes.c_int32, ctypes.c_int64, ctypes.c_void_p, ctypes.c_double
 
@@ -79,7 +80,8 @@ EXPORTED = [
     "hec_plan_n_parts", "hec_plan_part_ptr", "hec_plan_part_info", "hec_plan_part_info_opts",
     "hec_plan_export", "hec_plan_part_hec", "hec_plan_free", "hec_nccl_unique_id",
     "hec_dist_create", "hec_dist_create_local", "hec_spmv_dist", "hec_spmv_dist_local",
-    "hec_dist_get_info", "hec_dist_free",
+    "hec_dist_get_info", "hec_dist_free", "hec_dist_create_p2p", "hec_dist_p2p_connect",
+    "hec_dist_enable_p2p", "hec_dist_p2p_connect_local", "hec_dist_check",
     "hec_spmv_axpby", "hec_diag", "hec_jacobi", "hec_axpby", "hec_axpbyz", "hec_dot", "hec_norm2", "hec_bicgstab", "hec_cg",
     "hec_bicgstab_dist", "hec_cg_dist", "hec_from_csr_hyb", "hec_reorder_rcm", "hec_permute",
 ]
@@ -160,6 +162,17 @@ def load(build: bool = True):
     L.hec_dist_get_info.argtypes = [vp, ctypes.POINTER(DistInfoT)]
     L.hec_dist_free.restype = None
     L.hec_dist_free.argtypes = [vp]
+    L.hec_dist_create_p2p.restype = st
+    L.hec_dist_create_p2p.argtypes = [ctypes.POINTER(CsrT), vp, ctypes.POINTER(OptsT), i32, i32,
+                                      ctypes.POINTER(vp), vp]
+    L.hec_dist_p2p_connect.restype = st
+    L.hec_dist_p2p_connect.argtypes = [vp, vp]
+    L.hec_dist_enable_p2p.restype = st
+    L.hec_dist_enable_p2p.argtypes = [vp]
+    L.hec_dist_p2p_connect_local.restype = st
+    L.hec_dist_p2p_connect_local.argtypes = [vp, i32]
+    L.hec_dist_check.restype = st
+    L.hec_dist_check.argtypes = [vp]
     L.hec_spmv_axpby.restype = st
     L.hec_spmv_axpby.argtypes = [vp, dbl, vp, dbl, vp, vp]
     L.hec_diag.restype = st
@@ -471,6 +484,39 @@ class Dist:
         self.info = DistInfoT()
         _check(_lib.hec_dist_get_info(self._h, ctypes.byref(self.info)))
 
+    @classmethod
+    def create_p2p(cls, A, plan: "Plan", rank: int, device: int = 0,
+                   options: OptsT | None = None) -> tuple["Dist", bytes]:
+        """No-NCCL rank for the peer-memory transport (hec_dist_create_p2p):
+        returns the handle and this rank's window IPC handle; all-gather the
+        handles (e.g. torch.distributed) and call p2p_connect."""
+        load()
+        args = _CsrArgs(A)
+        o = options if options is not None else opts()
+        h = vp()
+        buf = (ctypes.c_uint8 * IPC_BYTES)()
+        _check(_lib.hec_dist_create_p2p(args.ref(), plan.handle, ctypes.byref(o), rank, device,
+                                        ctypes.byref(h), ctypes.cast(buf, vp)))
+        return cls(_handle=h.value), bytes(buf)
+
+    def p2p_connect(self, handles: list[bytes]):
+        """Map the neighbours' windows (handles in rank order) and use the peer-memory transport."""
+        blob = b"".join(handles)
+        if len(blob) != IPC_BYTES * len(handles):
+            raise ValueError("each handle must be IPC_BYTES long")
+        buf = (ctypes.c_uint8 * len(blob)).from_buffer_copy(blob)
+        _check(_lib.hec_dist_p2p_connect(self._h, ctypes.cast(buf, vp)))
+        _check(_lib.hec_dist_get_info(self._h, ctypes.byref(self.info)))
+
+    def enable_p2p(self):
+        """COLLECTIVE: switch an NCCL handle's halo exchange to the peer-memory transport."""
+        _check(_lib.hec_dist_enable_p2p(self._h))
+        _check(_lib.hec_dist_get_info(self._h, ctypes.byref(self.info)))
+
+    def check(self):
+        """Synchronise the communication stream; raise if a peer-memory wait timed out."""
+        _check(_lib.hec_dist_check(self._h))
+
     @property
     def handle(self) -> int:
         return self._h.value
@@ -512,12 +558,18 @@ class LocalDistGroup:
     """All ranks of a partition emulated on ONE device (hec_dist_create_local):
     same kernels and plan, exchange by device-to-device copies."""
 
-    def __init__(self, A, plan: Plan, device: int = 0, options: OptsT | None = None):
+    def __init__(self, A, plan: Plan, device: int = 0, options: OptsT | None = None, p2p: bool = False):
         load()
         args = _CsrArgs(A)
         o = options if options is not None else opts()
         arr = (vp * plan.n_parts)()
         _check(_lib.hec_dist_create_local(args.ref(), plan.handle, ctypes.byref(o), device, arr))
+        if p2p:
+            st = _lib.hec_dist_p2p_connect_local(arr, plan.n_parts)
+            if st != 0:
+                for p in range(plan.n_parts):
+                    _lib.hec_dist_free(arr[p])
+                _check(st)
         self.ranks = [Dist(_handle=arr[p]) for p in range(plan.n_parts)]
         self._arr = arr
 
