@@ -5,6 +5,8 @@
 #include <cstdint>
 #include <string>
 #include <vector>
+#include <cstdlib>
+#include <algorithm>
 
 #include <cuda_runtime.h>
 

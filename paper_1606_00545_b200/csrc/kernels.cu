@@ -284,14 +284,13 @@ __global__ void __launch_bounds__(256, EPI == EPI_JACOBI ? HEC_JAC_MINB : 0) ell
 // ELL result (this kernel runs after ell_kernel on the same stream).
 // Blocks of one super-block run back to back, so its entries and the x window
 // they touch are reused in L2.  Fixed reduction order: deterministic.
+// One block descriptor's work for the 256 threads tid = 0..255 of a group.
 template <bool HALO, bool JACOBI>
-__global__ void __launch_bounds__(256) tail_kernel(TailArgs a) {
-    const uint64_t pol = policy_evict_first();
-    const int4 d = __ldg(a.blk + a.blk_begin + blockIdx.x);  // {first, count, lg, 0}
+__device__ __forceinline__ void tail_desc(const TailArgs& a, int4 d, int tid, uint64_t pol) {
     const int lg = d.z;
     const int G = 1 << lg;
-    const int lane = threadIdx.x & (G - 1);
-    const int grp = threadIdx.x >> lg;
+    const int lane = tid & (G - 1);
+    const int grp = tid >> lg;
     double acc = 0.0;
     double* yp = nullptr;
     int32_t orow = 0;
@@ -315,7 +314,7 @@ __global__ void __launch_bounds__(256) tail_kernel(TailArgs a) {
     for (int off = G >> 1; off > 0; off >>= 1) acc += __shfl_xor_sync(0xffffffffu, acc, off, G);
     // y holds the ELL result: with programmatic dependent launch this kernel may
     // have started before ell_kernel finished, so wait for it here (a no-op
-    // when launched normally)
+    // when launched normally or once it has returned)
     asm volatile("griddepcontrol.wait;" ::: "memory");
     if (lane == 0 && active) {
         if (JACOBI)  // the ELL kernel wrote x + omega ((b - s_ell) / d): subtract omega (s_tail / d)
@@ -323,6 +322,12 @@ __global__ void __launch_bounds__(256) tail_kernel(TailArgs a) {
         else
             *yp = *yp + a.alpha * acc;
     }
+}
+
+template <bool HALO, bool JACOBI>
+__global__ void __launch_bounds__(256) tail_kernel(TailArgs a) {
+    const uint64_t pol = policy_evict_first();
+    tail_desc<HALO, JACOBI>(a, __ldg(a.blk + a.blk_begin + blockIdx.x), threadIdx.x, pol);
 }
 
 // ------------------------------------------------------- HYB: COO kernel --
@@ -500,10 +505,8 @@ cudaError_t launch_tail(const TailArgs& a, cudaStream_t s) {
     if (blocks <= 0) return cudaSuccess;
     if (blocks > 0x7fffffff) return cudaErrorInvalidValue;
     const bool pdl = tail_pdl();
-    if (a.diag) {
-        if (a.x_halo) return cudaErrorInvalidValue;
-        return launch_k(tail_kernel<false, true>, dim3((unsigned)blocks), dim3(256), s, pdl, a);
-    }
+    if (a.diag && a.x_halo) return cudaErrorInvalidValue;
+    if (a.diag) return launch_k(tail_kernel<false, true>, dim3((unsigned)blocks), dim3(256), s, pdl, a);
     if (a.x_halo) return launch_k(tail_kernel<true, false>, dim3((unsigned)blocks), dim3(256), s, pdl, a);
     return launch_k(tail_kernel<false, false>, dim3((unsigned)blocks), dim3(256), s, pdl, a);
 }
