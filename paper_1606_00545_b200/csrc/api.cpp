@@ -29,6 +29,7 @@ static void release(hec_matrix_s* m) {
         int cur = 0;
         cudaGetDevice(&cur);
         cudaSetDevice(m->device);
+        if (m->ws && m->ws_free) m->ws_free(m->ws);
         void* ptrs[] = {m->d_ell_col, m->d_ell_val, m->d_tail_out, m->d_tail_blk,
                         m->d_tail_ptr, m->d_tail_col, m->d_tail_val, m->d_rowmap, m->d_coo_row, m->d_stage_x,
                         m->d_stage_y};

@@ -47,6 +47,8 @@ struct hec_dist_s {
     unsigned int* d_done = nullptr;
     int32_t* d_err = nullptr;
     uint64_t epoch = 0;
+    void* ws = nullptr;                 // Krylov workspace (krylov.cu), freed through ws_free
+    void (*ws_free)(void*) = nullptr;
 };
 
 namespace hec {
@@ -66,6 +68,7 @@ static void dist_release(hec_dist_s* d) {
     int cur = 0;
     cudaGetDevice(&cur);
     cudaSetDevice(d->device);
+    if (d->ws && d->ws_free) d->ws_free(d->ws);
     if (d->comm) ncclCommDestroy(d->comm);
     for (void* p : d->opened) cudaIpcCloseMemHandle(p);
     if (d->d_win) cudaFree(d->d_win);
@@ -500,6 +503,11 @@ int64_t dist_n_local(hec_dist_s* D) { return (int64_t)D->r1 - D->r0; }
 ncclComm_t dist_comm(hec_dist_s* D) { return D->comm; }
 
 int32_t dist_parts(hec_dist_s* D) { return D->n_parts; }
+
+void** dist_ws_slot(hec_dist_s* D, void (***free_fn)(void*)) {
+    *free_fn = &D->ws_free;
+    return &D->ws;
+}
 
 }  // namespace hec
 

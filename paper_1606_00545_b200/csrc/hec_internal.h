@@ -108,6 +108,10 @@ hec_status build_plan(const CsrView& A, int32_t P, int32_t kind, const int32_t* 
 
 // ------------------------------------------------------------ device HEC --
 struct hec_matrix_s {
+    // Krylov workspace cached by the first solve on this handle (krylov.cu);
+    // freed with the handle through ws_free
+    void* ws = nullptr;
+    void (*ws_free)(void*) = nullptr;
     int32_t device = -1;
     int32_t n_rows = 0, n_cols = 0, width = 0, stride = 0;
     int64_t nnz = 0, ell_nnz = 0, tail_nnz = 0;

@@ -21,6 +21,8 @@
 #include <algorithm>
 #include <cmath>
 #include <cstring>
+#include <memory>
+#include <mutex>
 #include <vector>
 
 #include "hec_internal.h"
@@ -57,8 +59,14 @@ enum VecOp {
 
 struct VecArgs {
     int64_t n;
-    const double* sc;   // device scalars; null for the stand-alone Eq. (3)-(6) calls
+    double* sc;         // device scalars; null for the stand-alone Eq. (3)-(6) calls
     double* part;       // [2][kRedBlocks] partial dots (null: no dots)
+    unsigned int* ctr;  // non-null: the last CTA reduces the partials and runs the step (fused)
+    int n_dots;         // dots this pass produces (fused reduce)
+    int step_mode;      // step to run after the reduce (-1: none)
+    int first;
+    double tol;
+    bool vec2;          // every vector 16-byte aligned: 128-bit loads/stores of element pairs
     double ca, cb;      // coefficients of OP_AXPBY / OP_AXPBYZ
     double *x, *r, *r0, *p, *v, *s, *t, *b;
     const double *a1, *b1, *c1, *d1;
@@ -79,36 +87,73 @@ __device__ __forceinline__ double block_sum(double v, double* sh) {
     return v;  // valid in thread 0
 }
 
-// One element of each op; d0/d1 accumulate the pass's dot products.
-template <int OP>
+// Element pairs: the same expressions on two adjacent elements through one
+// 128-bit access per vector.
+struct D2 { double x, y; };
+__device__ __forceinline__ D2 operator+(D2 a, D2 b) { return {a.x + b.x, a.y + b.y}; }
+__device__ __forceinline__ D2 operator-(D2 a, D2 b) { return {a.x - b.x, a.y - b.y}; }
+__device__ __forceinline__ D2 operator*(double c, D2 a) { return {c * a.x, c * a.y}; }
+
+template <typename T> __device__ __forceinline__ T LD(const double* p, int64_t i);
+template <> __device__ __forceinline__ double LD<double>(const double* p, int64_t i) { return p[i]; }
+template <> __device__ __forceinline__ D2 LD<D2>(const double* p, int64_t i) {
+    const double2 v = reinterpret_cast<const double2*>(p)[i];
+    return {v.x, v.y};
+}
+__device__ __forceinline__ void ST(double* p, int64_t i, double v) { p[i] = v; }
+__device__ __forceinline__ void ST(double* p, int64_t i, D2 v) {
+    reinterpret_cast<double2*>(p)[i] = make_double2(v.x, v.y);
+}
+__device__ __forceinline__ void ACC(double& d, double a, double b) { d += a * b; }
+__device__ __forceinline__ void ACC(double& d, D2 a, D2 b) { d += a.x * b.x; d += a.y * b.y; }
+
+// One unit (an element, or a pair when T = D2) of each op; d0/d1 accumulate
+// the pass's dot products.
+template <int OP, typename T>
 __device__ __forceinline__ void vec_elem(const VecArgs& a, int64_t i, double alpha, double omega, double beta,
                                          double& d0, double& d1) {
-    if (OP == OP_DOT1) { d0 += a.a1[i] * a.b1[i]; }
-    if (OP == OP_DOT2) { d0 += a.a1[i] * a.b1[i]; d1 += a.c1[i] * a.d1[i]; }
-    if (OP == OP_RESID) { const double ri = a.b[i] - a.v[i]; a.r[i] = ri; a.r0[i] = ri; d0 += ri * ri; }
-    if (OP == OP_COPY) { a.p[i] = a.r[i]; }
-    if (OP == OP_BICG_P) { a.p[i] = a.r[i] + beta * (a.p[i] - omega * a.v[i]); }
-    if (OP == OP_BICG_S) { const double si = a.r[i] - alpha * a.v[i]; a.s[i] = si; d0 += si * si; }
+    if (OP == OP_DOT1) { ACC(d0, LD<T>(a.a1, i), LD<T>(a.b1, i)); }
+    if (OP == OP_DOT2) { ACC(d0, LD<T>(a.a1, i), LD<T>(a.b1, i)); ACC(d1, LD<T>(a.c1, i), LD<T>(a.d1, i)); }
+    if (OP == OP_RESID) { const T ri = LD<T>(a.b, i) - LD<T>(a.v, i); ST(a.r, i, ri); ST(a.r0, i, ri); ACC(d0, ri, ri); }
+    if (OP == OP_COPY) { ST(a.p, i, LD<T>(a.r, i)); }
+    if (OP == OP_BICG_P) { ST(a.p, i, LD<T>(a.r, i) + beta * (LD<T>(a.p, i) - omega * LD<T>(a.v, i))); }
+    if (OP == OP_BICG_S) { const T si = LD<T>(a.r, i) - alpha * LD<T>(a.v, i); ST(a.s, i, si); ACC(d0, si, si); }
     if (OP == OP_BICG_XR) {
-        const double si = a.s[i];
-        a.x[i] = a.x[i] + alpha * a.p[i] + omega * si;
-        const double ri = si - omega * a.t[i];
-        a.r[i] = ri; d0 += ri * ri; d1 += a.r0[i] * ri;
+        const T si = LD<T>(a.s, i);
+        ST(a.x, i, LD<T>(a.x, i) + alpha * LD<T>(a.p, i) + omega * si);
+        const T ri = si - omega * LD<T>(a.t, i);
+        ST(a.r, i, ri); ACC(d0, ri, ri); ACC(d1, LD<T>(a.r0, i), ri);
     }
-    if (OP == OP_X_ALPHA_P) { a.x[i] = a.x[i] + alpha * a.p[i]; }
+    if (OP == OP_X_ALPHA_P) { ST(a.x, i, LD<T>(a.x, i) + alpha * LD<T>(a.p, i)); }
     if (OP == OP_CG_XR) {
-        a.x[i] = a.x[i] + alpha * a.p[i];
-        const double ri = a.r[i] - alpha * a.v[i];
-        a.r[i] = ri; d0 += ri * ri;
+        ST(a.x, i, LD<T>(a.x, i) + alpha * LD<T>(a.p, i));
+        const T ri = LD<T>(a.r, i) - alpha * LD<T>(a.v, i);
+        ST(a.r, i, ri); ACC(d0, ri, ri);
     }
-    if (OP == OP_CG_P) { a.p[i] = a.r[i] + beta * a.p[i]; }
-    if (OP == OP_AXPBY) { a.r[i] = a.ca * a.a1[i] + a.cb * a.r[i]; }
-    if (OP == OP_AXPBYZ) { a.r[i] = a.ca * a.a1[i] + a.cb * a.b1[i]; }
+    if (OP == OP_CG_P) { ST(a.p, i, LD<T>(a.r, i) + beta * LD<T>(a.p, i)); }
+    if (OP == OP_AXPBY) { ST(a.r, i, a.ca * LD<T>(a.a1, i) + a.cb * LD<T>(a.r, i)); }
+    if (OP == OP_AXPBYZ) { ST(a.r, i, a.ca * LD<T>(a.a1, i) + a.cb * LD<T>(a.b1, i)); }
+}
+
+__device__ void step_body(double* sc, int mode, double tol, int first);
+
+template <int OP, typename T>
+__device__ __forceinline__ void vec_loop(const VecArgs& a, int64_t n_units, double alpha, double omega,
+                                         double beta, double& d0, double& d1) {
+    // 4 independent units per thread per trip (memory-level parallelism)
+    const int64_t stride = (int64_t)gridDim.x * blockDim.x;
+    int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    for (; i + 3 * stride < n_units; i += 4 * stride) {
+#pragma unroll
+        for (int u = 0; u < 4; ++u) vec_elem<OP, T>(a, i + u * stride, alpha, omega, beta, d0, d1);
+    }
+    for (; i < n_units; i += stride) vec_elem<OP, T>(a, i, alpha, omega, beta, d0, d1);
 }
 
 template <int OP>
 __global__ void __launch_bounds__(kRedThreads) vec_kernel(VecArgs a) {
     __shared__ double sh[2][32];
+    __shared__ bool last;
     double alpha = 0.0, omega = 0.0, beta = 0.0;
     bool skip = false;
     if (a.sc) {
@@ -120,14 +165,13 @@ __global__ void __launch_bounds__(kRedThreads) vec_kernel(VecArgs a) {
     }
     double d0 = 0.0, d1 = 0.0;
     if (!skip) {
-        // 4 independent elements per thread per trip (memory-level parallelism)
-        const int64_t stride = (int64_t)gridDim.x * blockDim.x;
-        int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
-        for (; i + 3 * stride < a.n; i += 4 * stride) {
-#pragma unroll
-            for (int u = 0; u < 4; ++u) vec_elem<OP>(a, i + u * stride, alpha, omega, beta, d0, d1);
+        if (a.vec2) {
+            vec_loop<OP, D2>(a, a.n >> 1, alpha, omega, beta, d0, d1);
+            if ((a.n & 1) && blockIdx.x == 0 && threadIdx.x == 0)  // odd length: the last element
+                vec_elem<OP, double>(a, a.n - 1, alpha, omega, beta, d0, d1);
+        } else {
+            vec_loop<OP, double>(a, a.n, alpha, omega, beta, d0, d1);
         }
-        for (; i < a.n; i += stride) vec_elem<OP>(a, i, alpha, omega, beta, d0, d1);
     }
     if (a.part) {
         d0 = block_sum(d0, sh[0]);
@@ -135,6 +179,29 @@ __global__ void __launch_bounds__(kRedThreads) vec_kernel(VecArgs a) {
         if (threadIdx.x == 0) {
             a.part[blockIdx.x] = d0;
             a.part[kRedBlocks + blockIdx.x] = d1;
+        }
+    }
+    if (a.ctr) {
+        // fused reduce + step: the last CTA to finish sums the partials in the
+        // fixed order of reduce_kernel and runs the scalar step (one launch
+        // instead of three; the summation order, hence every bit, is unchanged)
+        if (threadIdx.x == 0) {
+            __threadfence();
+            last = atomicAdd(a.ctr, 1u) == gridDim.x - 1;
+        }
+        __syncthreads();
+        if (last) {
+            __threadfence();
+            for (int k = 0; k < a.n_dots; ++k) {
+                double v = 0.0;
+                for (int b = threadIdx.x; b < kRedBlocks; b += blockDim.x) v += __ldcg(a.part + k * kRedBlocks + b);
+                v = block_sum(v, sh[0]);
+                if (threadIdx.x == 0) a.sc[SC_D0 + k] = v;
+            }
+            if (threadIdx.x == 0) {
+                if (a.step_mode >= 0) step_body(a.sc, a.step_mode, a.tol, a.first);
+                *a.ctr = 0;
+            }
         }
     }
 }
@@ -157,14 +224,12 @@ enum Step {
     ST_BICG_S,        // ||s|| <= thr -> converged (x += alpha p pending)
     ST_BICG_OMEGA,    // omega = (t, s) / (t, t)
     ST_BICG_R,        // ||r|| <= thr -> converged; omega = 0 -> breakdown 2; rho = (r0, r)
-    ST_CG_BEGIN,      // count the iteration
-    ST_CG_ALPHA,      // alpha = rho / (p, q)
+    ST_CG_ALPHA,      // count the iteration; alpha = rho / (p, q)
     ST_CG_R,          // rho_new = (r, r): converged?; beta = rho_new / rho
     ST_FINAL_DONE,    // clear the pending x += alpha p
 };
 
-__global__ void step_kernel(double* sc, int mode, double tol, int first) {
-    if (threadIdx.x != 0 || blockIdx.x != 0) return;
+__device__ void step_body(double* sc, int mode, double tol, int first) {
     if (mode == ST_FINAL_DONE) { if (sc[SC_FINAL_S] == 1.0) sc[SC_FINAL_S] = 2.0; return; }
     if (sc[SC_DONE] != 0.0) return;
     switch (mode) {
@@ -201,8 +266,10 @@ __global__ void step_kernel(double* sc, int mode, double tol, int first) {
             sc[SC_RHO_PREV] = sc[SC_RHO];
             sc[SC_RHO] = sc[SC_D1];                                                          // rho_k = (r0, r)
             break;
-        case ST_CG_BEGIN: sc[SC_ITER] += 1.0; break;
-        case ST_CG_ALPHA: sc[SC_ALPHA] = sc[SC_RHO] / sc[SC_D0]; break;
+        case ST_CG_ALPHA:  // counts the iteration (nothing between its start and here can stop it)
+            sc[SC_ITER] += 1.0;
+            sc[SC_ALPHA] = sc[SC_RHO] / sc[SC_D0];
+            break;
         case ST_CG_R:
             sc[SC_RES] = sqrt(sc[SC_D0]) / sc[SC_R0NORM];
             if (sqrt(sc[SC_D0]) <= sc[SC_THR]) { sc[SC_DONE] = 1.0; sc[SC_CONV] = 1.0; break; }
@@ -211,6 +278,11 @@ __global__ void step_kernel(double* sc, int mode, double tol, int first) {
             sc[SC_RHO] = sc[SC_D0];
             break;
     }
+}
+
+__global__ void step_kernel(double* sc, int mode, double tol, int first) {
+    if (threadIdx.x != 0 || blockIdx.x != 0) return;
+    step_body(sc, mode, tol, first);
 }
 
 // ------------------------------------------------------------------ host --
@@ -226,12 +298,21 @@ hec_status dist_spmv_launch(hec_dist_s* D, const double* x, double* y, cudaStrea
 int64_t dist_n_local(hec_dist_s* D);
 ncclComm_t dist_comm(hec_dist_s* D);
 int32_t dist_parts(hec_dist_s* D);
+void** dist_ws_slot(hec_dist_s* D, void (***free_fn)(void*));
 
 #define HEC_TRY(expr)                         \
     do {                                      \
         hec_status _st = (expr);              \
         if (_st != HEC_OK) return _st;        \
     } while (0)
+
+// 128-bit element pairs need every vector the pass touches 16-byte aligned.
+static bool aligned16(const VecArgs& a) {
+    const void* ps[] = {a.x, a.r, a.r0, a.p, a.v, a.s, a.t, a.b, a.a1, a.b1, a.c1, a.d1};
+    for (const void* p : ps)
+        if (p && (reinterpret_cast<uintptr_t>(p) & 15)) return false;
+    return true;
+}
 
 template <int OP>
 static cudaError_t launch_vec(const VecArgs& a, cudaStream_t s) {
@@ -257,6 +338,44 @@ static cudaError_t launch_vec_op(int op, const VecArgs& a, cudaStream_t s) {
     return cudaErrorInvalidValue;
 }
 
+// Device workspace of a solve: scalars, block partials, the fused-pass
+// counter, a pinned scalar mirror and 6 vectors (BiCGSTAB's r, r0, p, v, s, t;
+// CG uses 4).  Cached in the matrix / dist handle by the first solve and
+// reused (allocation and the implicit synchronisation of cudaFree cost ~10 ms
+// per solve otherwise); a second host thread solving on the same handle at the
+// same time gets a private one.
+struct SolverWs {
+    int64_t n = 0;
+    std::mutex busy;
+    double* sc = nullptr;
+    double* part = nullptr;
+    unsigned int* ctr = nullptr;
+    double* h_sc = nullptr;
+    std::vector<double*> vecs;
+    hec_status alloc(int64_t n_) {
+        n = n_;
+        HEC_CUDA_TRY(cudaMalloc(&sc, SC_N * sizeof(double)));
+        HEC_CUDA_TRY(cudaMalloc(&part, 2 * kRedBlocks * sizeof(double)));
+        HEC_CUDA_TRY(cudaMalloc(&ctr, sizeof(unsigned int)));
+        HEC_CUDA_TRY(cudaMallocHost(&h_sc, SC_N * sizeof(double)));
+        for (int k = 0; k < 6; ++k) {
+            double* v = nullptr;
+            HEC_CUDA_TRY(cudaMalloc(&v, sizeof(double) * (size_t)(n > 0 ? n : 1)));
+            vecs.push_back(v);
+        }
+        return HEC_OK;
+    }
+    ~SolverWs() {
+        if (sc) cudaFree(sc);
+        if (part) cudaFree(part);
+        if (ctr) cudaFree(ctr);
+        if (h_sc) cudaFreeHost(h_sc);
+        for (double* v : vecs) cudaFree(v);
+    }
+};
+
+static void ws_delete(void* p) { delete static_cast<SolverWs*>(p); }
+
 struct Solver {
     Op op;
     cudaStream_t s;
@@ -264,44 +383,69 @@ struct Solver {
     double* sc = nullptr;
     double* part = nullptr;
     double* h_sc = nullptr;  // pinned mirror
+    unsigned int* ctr = nullptr;  // last-CTA counter of the fused passes (self-resetting)
     std::vector<double*> vecs;
+    SolverWs* ws = nullptr;
+    std::unique_ptr<SolverWs> own;        // private workspace (cached one busy)
+    std::unique_lock<std::mutex> lock;
 
-    hec_status init(int n_vecs) {
-        HEC_CUDA_TRY(cudaMalloc(&sc, SC_N * sizeof(double)));
-        HEC_CUDA_TRY(cudaMemsetAsync(sc, 0, SC_N * sizeof(double), s));
-        HEC_CUDA_TRY(cudaMalloc(&part, 2 * kRedBlocks * sizeof(double)));
-        HEC_CUDA_TRY(cudaMallocHost(&h_sc, SC_N * sizeof(double)));
-        for (int k = 0; k < n_vecs; ++k) {
-            double* v = nullptr;
-            HEC_CUDA_TRY(cudaMalloc(&v, sizeof(double) * (size_t)(op.n > 0 ? op.n : 1)));
-            vecs.push_back(v);
+    hec_status init() {
+        void** slot;
+        void (**free_fn)(void*);
+        if (op.A) { slot = &op.A->ws; free_fn = &op.A->ws_free; }
+        else slot = dist_ws_slot(op.D, &free_fn);
+        {
+            static std::mutex create;  // first solve on a handle creates its cached workspace
+            std::lock_guard<std::mutex> g(create);
+            if (!*slot) {
+                std::unique_ptr<SolverWs> w(new SolverWs());
+                HEC_TRY(w->alloc(op.n));
+                *slot = w.release();
+                *free_fn = ws_delete;
+            }
         }
+        ws = static_cast<SolverWs*>(*slot);
+        lock = std::unique_lock<std::mutex>(ws->busy, std::try_to_lock);
+        if (!lock.owns_lock()) {
+            own.reset(new SolverWs());
+            HEC_TRY(own->alloc(op.n));
+            ws = own.get();
+        }
+        sc = ws->sc; part = ws->part; ctr = ws->ctr; h_sc = ws->h_sc; vecs = ws->vecs;
+        HEC_CUDA_TRY(cudaMemsetAsync(sc, 0, SC_N * sizeof(double), s));
+        HEC_CUDA_TRY(cudaMemsetAsync(ctr, 0, sizeof(unsigned int), s));
         return HEC_OK;
-    }
-    ~Solver() {
-        if (sc) cudaFree(sc);
-        if (part) cudaFree(part);
-        if (h_sc) cudaFreeHost(h_sc);
-        for (double* v : vecs) cudaFree(v);
     }
     hec_status spmv(const double* x, double* y) {
         if (op.A) return launch_spmv(op.A, x, nullptr, y, s);
         return dist_spmv_launch(op.D, x, y, s);
     }
-    // one fused vector pass; n_dots > 0: its dots land in SC_D0.. (all-reduced across ranks)
-    hec_status pass(int vop, VecArgs a, int n_dots) {
+    // One vector pass; n_dots > 0: its dots land in SC_D0.. (all-reduced across
+    // ranks); then the scalar step `mode` (-1: none).  One GPU: a single launch
+    // (the pass's last CTA reduces and steps).  Distributed: pass, reduce,
+    // ncclAllReduce, step kernel.
+    hec_status pass(int vop, VecArgs a, int n_dots, int mode = -1, int first = 0) {
         a.n = op.n;
         a.sc = sc;
         a.part = n_dots > 0 ? part : nullptr;
+        a.vec2 = aligned16(a);
+        if (!op.comm) {
+            a.ctr = (n_dots > 0 || mode >= 0) ? ctr : nullptr;
+            a.n_dots = n_dots;
+            a.step_mode = mode;
+            a.first = first;
+            a.tol = tol;
+            HEC_CUDA_TRY(launch_vec_op(vop, a, s));
+            return HEC_OK;
+        }
         HEC_CUDA_TRY(launch_vec_op(vop, a, s));
         if (n_dots > 0) {
             reduce_kernel<<<1, kRedThreads, 0, s>>>(part, n_dots, sc);
             HEC_CUDA_TRY(cudaGetLastError());
-            if (op.comm) {
-                ncclResult_t r = ncclAllReduce(sc + SC_D0, sc + SC_D0, n_dots, ncclDouble, ncclSum, op.comm, s);
-                if (r != ncclSuccess) return fail(HEC_ERR_NCCL, std::string("ncclAllReduce: ") + ncclGetErrorString(r));
-            }
+            ncclResult_t r = ncclAllReduce(sc + SC_D0, sc + SC_D0, n_dots, ncclDouble, ncclSum, op.comm, s);
+            if (r != ncclSuccess) return fail(HEC_ERR_NCCL, std::string("ncclAllReduce: ") + ncclGetErrorString(r));
         }
+        if (mode >= 0) HEC_TRY(step(mode, first));
         return HEC_OK;
     }
     hec_status step(int mode, int first = 0) {
@@ -342,8 +486,7 @@ static hec_status bicgstab(Solver& S, const double* b, double* x, int32_t max_it
     HEC_TRY(S.spmv(x, v));
     VecArgs a = {};
     a.b = const_cast<double*>(b); a.v = v; a.r = r; a.r0 = r0;
-    HEC_TRY(S.pass(OP_RESID, a, 1));
-    HEC_TRY(S.step(ST_INIT));
+    HEC_TRY(S.pass(OP_RESID, a, 1, ST_INIT));
     auto iteration = [&](int32_t k) -> hec_status {
         HEC_TRY(S.step(ST_BICG_BEGIN, k == 1));               // rho_{k-1} = 0 -> Fails; beta_{k-1}
         VecArgs q = {};
@@ -351,21 +494,17 @@ static hec_status bicgstab(Solver& S, const double* b, double* x, int32_t max_it
         HEC_TRY(S.pass(k == 1 ? OP_COPY : OP_BICG_P, q, 0));  // p = r | p = r + beta (p - omega v)
         HEC_TRY(S.spmv(p, v));                                // v = A p*
         q = {}; q.a1 = r0; q.b1 = v;
-        HEC_TRY(S.pass(OP_DOT1, q, 1));                       // (r0, v)
-        HEC_TRY(S.step(ST_BICG_ALPHA));                       // alpha_k = rho_{k-1} / (r0, v)
+        HEC_TRY(S.pass(OP_DOT1, q, 1, ST_BICG_ALPHA));        // (r0, v); alpha_k = rho_{k-1} / (r0, v)
         q = {}; q.r = r; q.v = v; q.s = s;
-        HEC_TRY(S.pass(OP_BICG_S, q, 1));                     // s = r - alpha v ; ||s||^2
-        HEC_TRY(S.step(ST_BICG_S));                           // ||s|| is satisfied?
+        HEC_TRY(S.pass(OP_BICG_S, q, 1, ST_BICG_S));          // s = r - alpha v ; ||s|| is satisfied?
         q = {}; q.x = x; q.p = p;
-        HEC_TRY(S.pass(OP_X_ALPHA_P, q, 0));                  //   then x = x + alpha p* ; stop
-        HEC_TRY(S.step(ST_FINAL_DONE));
+        HEC_TRY(S.pass(OP_X_ALPHA_P, q, 0, ST_FINAL_DONE));   //   then x = x + alpha p* ; stop
         HEC_TRY(S.spmv(s, t));                                // t = A s*
         q = {}; q.a1 = t; q.b1 = s; q.c1 = t; q.d1 = t;
-        HEC_TRY(S.pass(OP_DOT2, q, 2));                       // (t, s), (t, t)
-        HEC_TRY(S.step(ST_BICG_OMEGA));                       // omega_k = (t, s) / ||t||^2
+        HEC_TRY(S.pass(OP_DOT2, q, 2, ST_BICG_OMEGA));        // (t, s), (t, t); omega_k = (t, s) / ||t||^2
         q = {}; q.x = x; q.p = p; q.s = s; q.t = t; q.r = r; q.r0 = r0;
-        HEC_TRY(S.pass(OP_BICG_XR, q, 2));                    // x, r updates; ||r||^2 ; (r0, r)
-        return S.step(ST_BICG_R);                             // ||r|| satisfied? omega = 0? rho_k
+        // x, r updates; ||r||^2, (r0, r); ||r|| satisfied? omega = 0? rho_k
+        return S.pass(OP_BICG_XR, q, 2, ST_BICG_R);
     };
     return run_batches(S, max_it, iteration, info);
 }
@@ -376,20 +515,16 @@ static hec_status cg(Solver& S, const double* b, double* x, int32_t max_it, hec_
     HEC_TRY(S.spmv(x, q));
     VecArgs a = {};
     a.b = const_cast<double*>(b); a.v = q; a.r = r; a.r0 = r0;   // r = b - A x ; rho = (r, r)
-    HEC_TRY(S.pass(OP_RESID, a, 1));
-    HEC_TRY(S.step(ST_INIT));
+    HEC_TRY(S.pass(OP_RESID, a, 1, ST_INIT));
     a = {}; a.r = r; a.p = p;                                     // p = r
     HEC_TRY(S.pass(OP_COPY, a, 0));
     auto iteration = [&](int32_t) -> hec_status {
-        HEC_TRY(S.step(ST_CG_BEGIN));
         HEC_TRY(S.spmv(p, q));                                    // q = A p
         VecArgs c = {};
         c.a1 = p; c.b1 = q;
-        HEC_TRY(S.pass(OP_DOT1, c, 1));                           // (p, q)
-        HEC_TRY(S.step(ST_CG_ALPHA));                             // alpha = rho / (p, q)
+        HEC_TRY(S.pass(OP_DOT1, c, 1, ST_CG_ALPHA));              // (p, q); count; alpha = rho / (p, q)
         c = {}; c.x = x; c.p = p; c.r = r; c.v = q;
-        HEC_TRY(S.pass(OP_CG_XR, c, 1));                          // x += alpha p; r -= alpha q; (r, r)
-        HEC_TRY(S.step(ST_CG_R));                                 // converged?  beta = (r,r)/rho
+        HEC_TRY(S.pass(OP_CG_XR, c, 1, ST_CG_R));                 // x += alpha p; r -= alpha q; (r, r); beta
         c = {}; c.r = r; c.p = p;
         return S.pass(OP_CG_P, c, 0);                             // p = r + beta p
     };
@@ -405,7 +540,7 @@ static hec_status solve(Op op, int method, const double* b, double* x, double to
     S.op = op;
     S.s = (cudaStream_t)stream;
     S.tol = tol;
-    HEC_TRY(S.init(method == 0 ? 6 : 4));
+    HEC_TRY(S.init());
     hec_status st = method == 0 ? bicgstab(S, b, x, max_it, info) : cg(S, b, x, max_it, info);
     if (st == HEC_OK) HEC_CUDA_TRY(cudaStreamSynchronize(S.s));
     return st;
@@ -417,6 +552,7 @@ static hec_status vec_op(int op, int64_t n, double ca, const double* xa, double 
     if (n == 0) return HEC_OK;
     VecArgs a = {};
     a.n = n; a.ca = ca; a.cb = cb; a.a1 = xa; a.b1 = xb; a.r = out;
+    a.vec2 = aligned16(a);
     HEC_CUDA_TRY(launch_vec_op(op, a, (cudaStream_t)stream));
     return HEC_OK;
 }
@@ -429,6 +565,7 @@ static hec_status dot_op(int64_t n, const double* xa, const double* xb, double* 
     HEC_CUDA_TRY(cudaMalloc(&d, SC_N * sizeof(double)));
     VecArgs a = {};
     a.n = n; a.a1 = xa; a.b1 = xb; a.part = part;
+    a.vec2 = aligned16(a);
     cudaError_t e = launch_vec_op(OP_DOT1, a, s);
     if (e == cudaSuccess) {
         reduce_kernel<<<1, kRedThreads, 0, s>>>(part, 1, d);

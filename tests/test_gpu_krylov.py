@@ -116,7 +116,7 @@ def test_bicgstab_spe10_trajectory_matches_oracle():
 
 @pytest.mark.parametrize("maker,tol", [(lambda: hecgen.powerlaw(20000, seed=3), 1e-10),
                                        (lambda: hecgen.poisson2d(40, 30), 1e-10)])
-def test_bicgstab_matches_oracle(maker, tol):
+def test_bicgstab_matches_oracle(maker, tol, monkeypatch):
     A = maker()
     b = hecgen.vector(A.n_rows, "uniform", seed=12)
     ref = K.bicgstab(A, b, np.zeros(A.n_rows), tol, 2000)
@@ -124,7 +124,20 @@ def test_bicgstab_matches_oracle(maker, tol):
     xd = torch.zeros(A.n_rows, dtype=torch.float64, device="cuda")
     info = M.bicgstab(dev(b), xd, tol, 2000)
     assert info.converged == ref.converged and info.breakdown == ref.breakdown == 0
-    assert abs(info.iterations - ref.iterations) <= max(2, ref.iterations // 20)
+    # BiCGSTAB's iteration count depends on the rounding of its dot products:
+    # the oracle itself, with other equally valid summation orders for (x, y)
+    # (reversed, even/odd halves), spans a range (e.g. 165-182 around 170 on
+    # the power-law matrix).  The GPU's count must fall inside that spread.
+    counts = [ref.iterations]
+    plain = K.dot
+    for alt in (lambda x, y: plain(x[::-1], y[::-1]),
+                lambda x, y: plain(x[0::2], y[0::2]) + plain(x[1::2], y[1::2])):
+        monkeypatch.setattr(K, "dot", alt)
+        counts.append(K.bicgstab(A, b, np.zeros(A.n_rows), tol, 2000).iterations)
+    monkeypatch.setattr(K, "dot", plain)
+    lo, hi = min(counts), max(counts)
+    slack = max(2, ref.iterations // 20)
+    assert lo - slack <= info.iterations <= hi + slack, (info.iterations, counts)
     x = xd.cpu().numpy()
     rel_true = np.linalg.norm(b - oracle.csr_spmv(A, x)) / np.linalg.norm(b)
     assert rel_true <= 5 * tol
