@@ -37,7 +37,8 @@ def sources() -> list[str]:
 
 
 def deps() -> list[str]:
-    return sources() + glob.glob(os.path.join(CSRC, "*.h")) + [os.path.join(INCLUDE, "hec.h"), __file__]
+    return (sources() + glob.glob(os.path.join(CSRC, "*.h")) + glob.glob(os.path.join(CSRC, "*.cuh"))
+            + [os.path.join(INCLUDE, "hec.h"), __file__])
 
 
 def stale() -> bool:
