@@ -320,9 +320,11 @@ hec_status hec_dist_create_local(const hec_csr* A, hec_plan P, const hec_opts* o
 /* COLLECTIVE: y_local = (A x)[r0:r1] for this rank (every rank calls it in the
  * same order).  x_local/y_local: device, n_loc doubles, must not overlap.
  * On `stream`: the interior SpMV (x_local only) runs while a high-priority
- * stream packs x_local[send_idx] and exchanges it with the peers (NCCL
- * grouped send/recv); the boundary SpMV waits for the exchange.  Asynchronous;
- * ordered after prior work on `stream` and before later work on it. */
+ * stream exchanges the halo with the peers -- the peer-memory push kernel once
+ * the handle is connected (hec_dist_enable_p2p / hec_dist_p2p_connect, below),
+ * else a pack kernel and NCCL grouped send/recv -- and then runs the boundary
+ * SpMV.  HEC_ERR_STATE for a multi-rank handle with neither transport.
+ * Asynchronous; ordered after prior work on `stream` and before later work on it. */
 hec_status hec_spmv_dist(hec_dist D, const double* x_local, double* y_local, void* stream);
 
 /* ---- peer-memory halo transport ----

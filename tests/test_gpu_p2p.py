@@ -89,6 +89,19 @@ def test_local_p2p_every_row_its_own_part():
         assert np.all(np.abs(y - oracle.csr_spmv(B, x)) <= oracle.tolerance(B, x))
 
 
+def test_local_p2p_256_slabs_8_parts_sampled():
+    # BASELINE configs[2] at full size, the 8-slab partition of the scaling
+    # run, through the peer-memory transport (two calls: both window parities)
+    A = hecgen.poisson3d(256, 256, 256)
+    xs = [hecgen.vector(A.n_cols, "uniform", seed=s) for s in (1606, 7)]
+    got, _ = local_calls(A, xs, 8, hec.PART_GRID, (256, 256, 256))
+    plane = 256 * 256
+    for x, y in zip(xs, got):
+        for r0 in [0, 31 * plane, 32 * plane - 100, 100 * plane + 77, A.n_rows - 5000]:
+            ref = oracle.csr_spmv(A, x, r0, r0 + 5000)
+            assert np.all(np.abs(y[r0:r0 + 5000] - ref) <= oracle.tolerance(A, x, r0, r0 + 5000))
+
+
 def test_p2p_handle_without_transport_is_refused():
     A = hecgen.poisson2d(16, 16)
     plan = hec.partition(A, 2, hec.PART_CONTIG_ROWS)
