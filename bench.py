@@ -312,6 +312,30 @@ def run_single(args):
             "p10_step_ms": round(float(np.percentile(per, 10)), 5),
             "p90_step_ms": round(float(np.percentile(per, 90)), 5)}
 
+    # SURVEY §8(d) secondary: warm timing, back-to-back SpMVs replayed from one
+    # captured CUDA graph (no flush), reported beside the primary number
+    if not args.profile:
+        try:
+            G = 50
+            g = torch.cuda.CUDAGraph()
+            with torch.cuda.graph(g, stream=stream):
+                for _ in range(G):
+                    M.spmv(x, y, stream)
+            g.replay()
+            torch.cuda.synchronize()
+            w0, w1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            with torch.cuda.stream(stream):
+                w0.record(stream)
+                for _ in range(4):
+                    g.replay()
+                w1.record(stream)
+            torch.cuda.synchronize()
+            roof["warm_graph_ms_per_spmv"] = round(w0.elapsed_time(w1) / (4 * G), 5)
+            del g
+        except Exception as e:  # capture is diagnostic only
+            roof["warm_graph_ms_per_spmv"] = None
+            roof["warm_graph_error"] = str(e)[:200]
+
     # end to end through the public API with HOST buffers (pinned), copies inside
     e2e = None
     if not args.no_e2e and not args.profile:
