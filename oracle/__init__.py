@@ -10,6 +10,7 @@ is ``hecgen`` (seeded input generators, no method arithmetic).
 
 Contents (SURVEY.md §8(c) names):
   O1  csr_spmv      serial CSR y = A x, column order, no FMA   (spmv_oracle.c)
+  O1p csr_spmv_parallel  the same rows over OpenMP threads (bit-identical; timing only)
   O1' csr_absmv     (|A||x|)_i, the tolerance scale           (spmv_oracle.c)
   Eq1 column_spmv   y = sum_k x_k A[:,k]  (Eq. (1))  (numpy, column order)
   O2  hec_ref       HEC reference builder                     (hec_ref.py)
@@ -40,7 +41,7 @@ def build(force: bool = False) -> str:
     """Compile the C oracle: -O2 -ffp-contract=off -fno-fast-math (no FMA)."""
     if force or not os.path.exists(_LIB) or os.path.getmtime(_LIB) < os.path.getmtime(_SRC):
         tmp = _LIB + f".tmp{os.getpid()}"
-        subprocess.check_call(["gcc", "-O2", "-std=c11", "-ffp-contract=off", "-fno-fast-math",
+        subprocess.check_call(["gcc", "-O2", "-std=c11", "-ffp-contract=off", "-fno-fast-math", "-fopenmp",
                                "-fPIC", "-shared", "-o", tmp, _SRC, "-lm"])
         os.replace(tmp, _LIB)
     return _LIB
@@ -54,6 +55,8 @@ def _load():
         for f in (lib.oracle_csr_spmv, lib.oracle_csr_absmv):
             f.restype = None
             f.argtypes = [i32, i32, vp, vp, vp, vp, vp]
+        lib.oracle_csr_spmv_omp.restype = ctypes.c_int
+        lib.oracle_csr_spmv_omp.argtypes = [i32, i32, vp, vp, vp, vp, vp]
         _lib = lib
     return _lib
 
@@ -79,6 +82,18 @@ def csr_spmv(A, x: np.ndarray, r0: int = 0, r1: int | None = None) -> np.ndarray
     y = np.empty(r1 - r0, dtype=np.float64)
     _load().oracle_csr_spmv(r0, r1, _p(rp), _p(col), _p(val), _p(x), _p(y))
     return y
+
+
+def csr_spmv_parallel(A, x: np.ndarray) -> tuple[np.ndarray, int]:
+    """O1 with its rows split over host threads (OpenMP):
+    bit-identical to csr_spmv, for timing a parallel CPU baseline.  Returns
+    (y, threads used)."""
+    x = np.ascontiguousarray(x, dtype=np.float64)
+    assert x.shape[0] == A.n_cols
+    rp, col, val = _arrays(A)
+    y = np.empty(A.n_rows, dtype=np.float64)
+    t = _load().oracle_csr_spmv_omp(0, A.n_rows, _p(rp), _p(col), _p(val), _p(x), _p(y))
+    return y, int(t)
 
 
 def csr_absmv(A, x: np.ndarray, r0: int = 0, r1: int | None = None) -> np.ndarray:

@@ -15,9 +15,14 @@
  *     of the same sums), taken row by row in column order.
  * O1' r_i = sum_k |val[k]| * |x[col[k]]|, the scale of the parity tolerance
  *     tau_i = 1e-12 * r_i (BASELINE.json north_star).
+ * O1p the same O1 loop with its rows split over host threads (OpenMP static
+ *     schedule; SURVEY.md §8(d) CPU timing (ii)).  Each row is still summed by
+ *     one thread in column order, so the result is bit-identical to O1; it is
+ *     used only to time a parallel CPU baseline.
  */
 #include <stdint.h>
 #include <math.h>
+#include <omp.h>
 
 void oracle_csr_spmv(int32_t r0, int32_t r1, const int32_t* row_ptr, const int32_t* col,
                      const double* val, const double* x, double* y) {
@@ -41,4 +46,24 @@ void oracle_csr_absmv(int32_t r0, int32_t r1, const int32_t* row_ptr, const int3
         }
         r[i - r0] = s;
     }
+}
+
+int oracle_csr_spmv_omp(int32_t r0, int32_t r1, const int32_t* row_ptr, const int32_t* col,
+                        const double* val, const double* x, double* y) {
+    int threads = 1;
+#pragma omp parallel
+    {
+#pragma omp single
+        threads = omp_get_num_threads();
+#pragma omp for schedule(static)
+        for (int32_t i = r0; i < r1; ++i) {
+            double s = 0.0;
+            for (int32_t k = row_ptr[i]; k < row_ptr[i + 1]; ++k) {
+                double prod = val[k] * x[col[k]];
+                s = s + prod;
+            }
+            y[i - r0] = s;
+        }
+    }
+    return threads;
 }

@@ -91,6 +91,15 @@ def test_o1_scipy_crosscheck():
         assert np.all(d <= oracle.tolerance(A, x) + 0.0)
 
 
+def test_o1_parallel_is_bit_identical():
+    # O1p (OpenMP rows, timing only) must be O1 bit for bit: one thread per row, same order
+    for A in (hecgen.powerlaw(50000, seed=2), hecgen.spe10(20, 30, 10, seed=1), hecgen.poisson3d(30, 20, 10)):
+        x = hecgen.vector(A.n_cols, "uniform", seed=3)
+        y, threads = oracle.csr_spmv_parallel(A, x)
+        assert threads >= 1
+        assert y.tobytes() == oracle.csr_spmv(A, x).tobytes()
+
+
 def test_o1_dense_random_1e13():
     # random 100x100 at 5% vs dense matvec to 1e-13 relative.
     A = hecgen.random_csr(100, 100, 0.05, seed=41)
