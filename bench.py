@@ -377,7 +377,7 @@ def run_single(args):
                        "tail_nnz": inf.tail_nnz, "parallelism": "1 GPU",
                        "l2": (f"inputs {alg / 1e9:.2f} GB > 4x {L2_BYTES / 2**20:.0f} MiB L2, no flush" if not flush
                               else f"L2 flushed ({4 * L2_BYTES / 2**20:.0f} MiB write + read) before every step, outside the timed pair"),
-                       "checksum": A.checksum(), "setup_s": {"generate": round(t_gen, 2), "convert_upload": round(t_conv, 2)},
+                       "checksum": A.checksum(), "x_checksum": hecgen.fnv1a(x_h), "setup_s": {"generate": round(t_gen, 2), "convert_upload": round(t_conv, 2)},
                        "reorder": reorder_info},
             "gbs": round(alg / (ms_step * 1e-3) / 1e9, 1),
             "roofline": roof, "gpu_launches": K * launches_per_step,

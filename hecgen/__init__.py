@@ -92,12 +92,17 @@ class Csr:
         return int(self.col.shape[0])
 
     def checksum(self) -> str:
-        lib = _load()
-        h = 0
-        for a in (self.row_ptr, self.col, self.val):
-            a = np.ascontiguousarray(a)
-            h = lib.hecgen_fnv1a(_p(a), a.nbytes, h)
-        return f"{h:016x}"
+        return fnv1a(self.row_ptr, self.col, self.val)
+
+
+def fnv1a(*arrays) -> str:
+    """FNV-1a over the raw bytes of the arrays, in order (run logs)."""
+    lib = _load()
+    h = 0
+    for a in arrays:
+        a = np.ascontiguousarray(a)
+        h = lib.hecgen_fnv1a(_p(a), a.nbytes, h)
+    return f"{h:016x}"
 
 
 def checksum(a: np.ndarray) -> str:
