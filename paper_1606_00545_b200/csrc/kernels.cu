@@ -172,6 +172,34 @@ __device__ __forceinline__ double jacobi_row(double x, double b, double d, doubl
     return __dadd_rn(x, __dmul_rn(omega, __ddiv_rn(__dsub_rn(b, s), d)));
 }
 
+#ifndef HEC_ELL_PHASE
+#define HEC_ELL_PHASE 8  // widths above this load their slots in two phases (measured: 8 > 16 > 6)
+#endif
+
+// Slots [J0, J1) of a row pair: loads, then gathers, then FMAs in slot order.
+template <int J0, int J1, bool HALO>
+__device__ __forceinline__ void ell_phase(const EllArgs& a, const int32_t* cp, const double* vp, int64_t s,
+                                          uint64_t pol, double& acc0, double& acc1) {
+    constexpr int N = J1 - J0;
+    int2 c[N];
+    double2 v[N];
+#pragma unroll
+    for (int j = 0; j < N; ++j) c[j] = ld_stream_i2v(cp + (J0 + j) * s, pol);
+#pragma unroll
+    for (int j = 0; j < N; ++j) v[j] = ld_stream_d2v(vp + (J0 + j) * s, pol);
+    double x0[N], x1[N];
+#pragma unroll
+    for (int j = 0; j < N; ++j) {
+        x0[j] = c[j].x >= 0 ? gather_x<HALO>(a.x, a.x_halo, a.n_loc, c[j].x) : 0.0;
+        x1[j] = c[j].y >= 0 ? gather_x<HALO>(a.x, a.x_halo, a.n_loc, c[j].y) : 0.0;
+    }
+#pragma unroll
+    for (int j = 0; j < N; ++j) {
+        acc0 = fma(v[j].x, x0[j], acc0);
+        acc1 = fma(v[j].y, x1[j], acc1);
+    }
+}
+
 template <int W, bool HALO, bool ROWMAP, int EPI>
 __global__ void __launch_bounds__(256, EPI == EPI_JACOBI ? HEC_JAC_MINB : 0) ell_kernel(EllArgs a) {
     constexpr bool AXPBY = EPI == EPI_AXPBY;
@@ -197,24 +225,12 @@ __global__ void __launch_bounds__(256, EPI == EPI_JACOBI ? HEC_JAC_MINB : 0) ell
         if (W > 0) {
             // All slot loads of the row pair first (2W independent 64/128-bit
             // streams in flight), then the x gathers, then the FMAs in slot order.
+            // Widths above HEC_ELL_PHASE run in two such phases (fewer live
+            // registers, more resident warps).
             constexpr int WW = W > 0 ? W : 1;
-            int2 c[WW];
-            double2 v[WW];
-#pragma unroll
-            for (int j = 0; j < WW; ++j) c[j] = ld_stream_i2v(cp + j * s, pol);
-#pragma unroll
-            for (int j = 0; j < WW; ++j) v[j] = ld_stream_d2v(vp + j * s, pol);
-            double x0[WW], x1[WW];
-#pragma unroll
-            for (int j = 0; j < WW; ++j) {
-                x0[j] = c[j].x >= 0 ? gather_x<HALO>(a.x, a.x_halo, a.n_loc, c[j].x) : 0.0;
-                x1[j] = c[j].y >= 0 ? gather_x<HALO>(a.x, a.x_halo, a.n_loc, c[j].y) : 0.0;
-            }
-#pragma unroll
-            for (int j = 0; j < WW; ++j) {
-                acc0 = fma(v[j].x, x0[j], acc0);
-                acc1 = fma(v[j].y, x1[j], acc1);
-            }
+            constexpr int P1 = WW > HEC_ELL_PHASE ? (WW + 1) / 2 : WW;
+            ell_phase<0, P1, HALO>(a, cp, vp, s, pol, acc0, acc1);
+            if constexpr (P1 < WW) ell_phase<P1, WW, HALO>(a, cp, vp, s, pol, acc0, acc1);
         } else {
 #pragma unroll 4
             for (int j = 0; j < width; ++j) {
