@@ -57,6 +57,8 @@ def parse():
                     help="measure Krylov iterations/s instead of the SpMV (NEXT-1)")
     ap.add_argument("--jacobi", type=float, default=None, metavar="OMEGA",
                     help="NEXT-3: time damped-Jacobi sweeps (hec_jacobi) with this omega")
+    ap.add_argument("--ell-width", type=int, default=None,
+                    help="experiment: FIXED ELL width instead of the BG3 rule (reading A1)")
     ap.add_argument("--transport", choices=["p2p", "nccl"], default="p2p",
                     help="N > 1 halo exchange: peer-memory push kernel over NVLink (default) or NCCL send/recv")
     ap.add_argument("--dist", action="store_true",
@@ -272,7 +274,8 @@ def run_single(args):
     x_h = hecgen.vector(A.n_cols, "uniform", seed=1606)
     stream = torch.cuda.Stream()
     t0 = time.perf_counter()
-    M = hec.from_csr(A, device=dev, stream=stream)
+    o = hec.opts(hec.WIDTH_FIXED, 20, args.ell_width) if args.ell_width is not None else None
+    M = hec.from_csr(A, o, device=dev, stream=stream)
     t_conv = time.perf_counter() - t0
     x = torch.from_numpy(x_h).to(f"cuda:{dev}")
     y = torch.empty(A.n_rows, dtype=torch.float64, device=f"cuda:{dev}")
@@ -375,6 +378,7 @@ def run_single(args):
             "config": {"workload": args.config, "n_rows": A.n_rows, "n_cols": A.n_cols, "nnz": A.nnz,
                        "ell_width": inf.ell_width, "ell_stride": inf.ell_stride, "tail_rows": inf.tail_rows,
                        "tail_nnz": inf.tail_nnz, "parallelism": "1 GPU",
+                       "width_policy": "BG3 (A1)" if args.ell_width is None else f"FIXED {args.ell_width} (experiment)",
                        "l2": (f"inputs {alg / 1e9:.2f} GB > 4x {L2_BYTES / 2**20:.0f} MiB L2, no flush" if not flush
                               else f"L2 flushed ({4 * L2_BYTES / 2**20:.0f} MiB write + read) before every step, outside the timed pair"),
                        "checksum": A.checksum(), "x_checksum": hecgen.fnv1a(x_h), "setup_s": {"generate": round(t_gen, 2), "convert_upload": round(t_conv, 2)},

@@ -1,12 +1,9 @@
 #!/bin/bash
-set -u
-TAG=${1:-r11}
-OUT=gpurun_out/$TAG
+OUT=gpurun_out/epl
 mkdir -p $OUT
-for e in 1 2 4 8; do
-  HEC_TAIL_EPL=$e timeout 300 python bench.py --config powerlaw_8M --no-cpu-baseline --no-e2e --steps 50 > $OUT/pl_epl$e.json 2>> $OUT/err.log
-  HEC_TAIL_EPL=$e timeout 300 python bench.py --config spe10 --no-cpu-baseline --no-e2e > $OUT/spe_epl$e.json 2>> $OUT/err.log
+python -c "import __graft_entry__ as g; g.build()" > $OUT/build.log 2>&1
+for e in 8 12 16 6; do
+  echo "== epl $e" >> $OUT/bench.jsonl
+  HEC_TAIL_EPL=$e timeout 600 python bench.py --config powerlaw_8M --no-cpu-baseline --no-e2e --steps 200 --warmup 20 >> $OUT/bench.jsonl 2>> $OUT/bench.err
 done
-timeout 600 ncu --set full --clock-control none --import-source on -k regex:tail_kernel -s 3 -c 1 -o $OUT/prof_tail \
-  python bench.py --config powerlaw_8M --profile --steps 5 --warmup 3 > $OUT/ncu_full.log 2>&1
-echo done > $OUT/DONE
+timeout 600 ncu --metrics gpu__time_duration.sum,dram__bytes_read.sum --clock-control none -c 12 --csv --log-file $OUT/launches.csv python bench.py --config powerlaw_8M --profile --steps 5 --warmup 1 > /dev/null 2>&1
