@@ -85,14 +85,16 @@ def measured_peak():
 
 
 def ncu_traffic(config: str):
-    """dram__bytes_read.sum + dram__bytes_write.sum per launch of the dominant
-    kernel from the committed ncu --set full capture (profiles/), or None."""
+    """dram__bytes_read.sum + dram__bytes_write.sum per step (summed over the
+    step's kernels: ell_kernel, plus tail_kernel where the matrix has a tail)
+    from the committed ncu --set full captures (profiles/ncu_traffic.json), and
+    the per-kernel split; (None, None) if absent."""
     p = os.path.join(ROOT, "profiles", "ncu_traffic.json")
     try:
-        d = json.load(open(p))
-        return d.get(config, {}).get("dram_bytes_per_launch")
+        d = json.load(open(p)).get(config, {})
+        return d.get("dram_bytes_per_step"), {k: v["dram_bytes_per_launch"] for k, v in d.get("kernels", {}).items()}
     except Exception:
-        return None
+        return None, None
 
 
 class L2Flusher:
@@ -319,8 +321,9 @@ def run_single(args):
     # dominant kernel: the ELL kernel (the only launch per step when there is no tail)
     mean_launch_ms = statistics.mean(per)
     achieved = alg / (mean_launch_ms * 1e-3) / 1e9
+    traffic, traffic_split = ncu_traffic(args.config)
     roof = {"bound": "hbm", "achieved": round(achieved, 1), "peak": peak, "unit": "GB/s",
-            "frac": round(achieved / peak, 4), "traffic": ncu_traffic(args.config),
+            "frac": round(achieved / peak, 4), "traffic": traffic, "traffic_by_kernel": traffic_split,
             "kernel": "ell_kernel" + ("" if launches_per_step == 1 else "+tail_kernel (step)"),
             "algorithmic_bytes_per_launch": alg, "format_bytes_per_launch": fmt_bytes,
             "peak_source": peak_src, "frac_of_8TBs_nominal": round(achieved / 8000.0, 4),

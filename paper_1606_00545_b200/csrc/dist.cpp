@@ -38,10 +38,9 @@ struct hec_dist_s {
     void* d_win = nullptr;              // [flags: n_parts u64, 256 B aligned][halo buf 0][halo buf 1]
     std::vector<void*> opened;          // peer windows mapped with cudaIpcOpenMemHandle
     std::vector<int32_t> nbr;           // neighbour ranks (send or receive side), ascending
-    std::vector<int32_t> send_peer, send_dst;  // per send entry: destination rank, halo position there
+    std::vector<int4> push_chunks;      // {destination rank, first send entry, end, halo position there}
     std::vector<int64_t> all_nhalo;     // every rank's halo length (from the plan)
-    int32_t* d_send_peer = nullptr;
-    int32_t* d_send_dst = nullptr;
+    int4* d_push_chunks = nullptr;
     int32_t* d_nbr = nullptr;
     void* d_peer_tab = nullptr;         // [buf0 ptrs | flag ptrs | n_halo] per rank
     unsigned int* d_done = nullptr;
@@ -72,8 +71,7 @@ static void dist_release(hec_dist_s* d) {
     if (d->comm) ncclCommDestroy(d->comm);
     for (void* p : d->opened) cudaIpcCloseMemHandle(p);
     if (d->d_win) cudaFree(d->d_win);
-    if (d->d_send_peer) cudaFree(d->d_send_peer);
-    if (d->d_send_dst) cudaFree(d->d_send_dst);
+    if (d->d_push_chunks) cudaFree(d->d_push_chunks);
     if (d->d_nbr) cudaFree(d->d_nbr);
     if (d->d_peer_tab) cudaFree(d->d_peer_tab);
     if (d->d_done) cudaFree(d->d_done);
@@ -146,16 +144,16 @@ static hec_status dist_build(const hec_csr* A, hec_plan P, const hec_opts* o, in
     // q.recv_off[rank], reading A10), and the neighbour set
     d->all_nhalo.resize(P->n_parts);
     for (int32_t q = 0; q < P->n_parts; ++q) d->all_nhalo[q] = (int64_t)P->parts[q].recv.size();
-    d->send_peer.resize(pt.send_idx.size());
-    d->send_dst.resize(pt.send_idx.size());
     for (int32_t q = 0; q < P->n_parts; ++q) {
         const int32_t sc = pt.send_off[q + 1] - pt.send_off[q];
         const int32_t rc = pt.recv_off[q + 1] - pt.recv_off[q];
         if (q != rank && (sc > 0 || rc > 0)) d->nbr.push_back(q);
-        for (int32_t k = pt.send_off[q]; k < pt.send_off[q + 1]; ++k) {
-            d->send_peer[k] = q;
-            d->send_dst[k] = P->parts[q].recv_off[rank] + (k - pt.send_off[q]);
-        }
+        // one push CTA per kPushChunk entries of one destination: the
+        // destination's buffer pointer is loaded once per CTA and the stores
+        // of a CTA are contiguous there
+        for (int32_t k = pt.send_off[q]; k < pt.send_off[q + 1]; k += kPushChunk)
+            d->push_chunks.push_back(make_int4(q, k, std::min(pt.send_off[q + 1], k + kPushChunk),
+                                               P->parts[q].recv_off[rank] + (k - pt.send_off[q])));
     }
     d->width = part_width(*P, rank, op);
     cudaStream_t s = nullptr;
@@ -234,11 +232,10 @@ static hec_status p2p_finish(hec_dist_s* d, const std::vector<void*>& wins) {
         HEC_CUDA_TRY(cudaMalloc(&d->d_nbr, d->nbr.size() * sizeof(int32_t)));
         HEC_CUDA_TRY(cudaMemcpy(d->d_nbr, d->nbr.data(), d->nbr.size() * sizeof(int32_t), cudaMemcpyHostToDevice));
     }
-    if (d->n_send > 0) {
-        HEC_CUDA_TRY(cudaMalloc(&d->d_send_peer, sizeof(int32_t) * d->n_send));
-        HEC_CUDA_TRY(cudaMalloc(&d->d_send_dst, sizeof(int32_t) * d->n_send));
-        HEC_CUDA_TRY(cudaMemcpy(d->d_send_peer, d->send_peer.data(), sizeof(int32_t) * d->n_send, cudaMemcpyHostToDevice));
-        HEC_CUDA_TRY(cudaMemcpy(d->d_send_dst, d->send_dst.data(), sizeof(int32_t) * d->n_send, cudaMemcpyHostToDevice));
+    if (!d->push_chunks.empty()) {
+        const size_t nb = d->push_chunks.size() * sizeof(int4);
+        HEC_CUDA_TRY(cudaMalloc(&d->d_push_chunks, nb));
+        HEC_CUDA_TRY(cudaMemcpy(d->d_push_chunks, d->push_chunks.data(), nb, cudaMemcpyHostToDevice));
     }
     d->p2p = true;
     return HEC_OK;
@@ -249,9 +246,8 @@ static PushArgs push_args(const hec_dist_s* d, const double* x_local, uint64_t e
     PushArgs a;
     a.x = x_local;
     a.idx = d->d_send_idx;
-    a.peer = d->d_send_peer;
-    a.dst = d->d_send_dst;
-    a.n = d->n_send;
+    a.chunks = d->d_push_chunks;
+    a.n_chunks = (int32_t)d->push_chunks.size();
     a.peer_buf0 = static_cast<double* const*>(d->d_peer_tab);
     a.peer_flags = reinterpret_cast<uint64_t* const*>(static_cast<uint64_t*>(d->d_peer_tab) + P);
     a.peer_nhalo = reinterpret_cast<const int64_t*>(static_cast<uint64_t*>(d->d_peer_tab) + 2 * P);

@@ -189,12 +189,12 @@ struct PeerWait {
     uint64_t epoch = 0;
     int32_t* err = nullptr;
 };
+constexpr int32_t kPushChunk = 512;  // send entries per push CTA (2 per thread; 256-2048 measured alike)
 struct PushArgs {                     // fused pack + NVLink store + release
     const double* x;                  // x_local
     const int32_t* idx;               // send_idx (grouped by destination rank)
-    const int32_t* peer;              // destination rank of each entry
-    const int32_t* dst;               // position in that rank's halo buffer
-    int32_t n;
+    const int4* chunks;               // per CTA: {destination rank, first entry, end, halo position}
+    int32_t n_chunks;
     double* const* peer_buf0;         // [n_parts] peer q's halo buffer 0 (buffer 1 follows it)
     const int64_t* peer_nhalo;        // [n_parts] peer q's halo length
     uint64_t* const* peer_flags;      // [n_parts] peer q's arrival flags

@@ -571,24 +571,27 @@ __global__ void __launch_bounds__(256) diag_coo_kernel(const int32_t* __restrict
 }
 
 // ------------------------------------------------ peer-memory halo push --
-// The export of P:158 fused with the transfer: every thread gathers its
-// x_local[send_idx[k]] and stores it straight into the destination rank's
-// halo buffer (this call's parity) through its IPC mapping over NVLink -- no
-// staging buffer, no copy engine, no NCCL kernel.  Each CTA then fences at
-// system scope and counts itself done; the last CTA releases this call's
-// epoch into every neighbour's arrival flag (st.release.sys).  Neighbours
+// The export of P:158 fused with the transfer: each CTA takes kPushChunk send
+// entries of one destination rank, gathers x_local[send_idx[k]] and stores
+// them straight into that rank's halo buffer (this call's parity) through its
+// IPC mapping over NVLink -- no staging buffer, no copy engine, no NCCL
+// kernel.  Each CTA then fences at system scope and counts itself done; the
+// last CTA releases this call's epoch into every neighbour's arrival flag
+// (st.release.sys).  Neighbours
 // with nothing to receive still get the flag: it tells them this rank has
 // finished reading its own halo buffer of the previous call.
 __global__ void __launch_bounds__(256) push_kernel(PushArgs a) {
-    const int32_t par = (int32_t)(a.epoch & 1);
-    for (int32_t k = blockIdx.x * blockDim.x + threadIdx.x; k < a.n; k += gridDim.x * blockDim.x) {
-        const int32_t q = __ldg(a.peer + k);
-        double* buf = a.peer_buf0[q] + (par ? a.peer_nhalo[q] : 0);
-        buf[__ldg(a.dst + k)] = __ldg(a.x + __ldg(a.idx + k));
+    if ((int32_t)blockIdx.x < a.n_chunks) {
+        const int4 c = __ldg(a.chunks + blockIdx.x);  // {q, k0, k1, halo position of k0 at q}
+        double* dst = a.peer_buf0[c.x] + ((a.epoch & 1) ? a.peer_nhalo[c.x] : 0) + c.w - c.y;
+#pragma unroll 8
+        for (int32_t k = c.y + threadIdx.x; k < c.z; k += blockDim.x) dst[k] = __ldg(a.x + __ldg(a.idx + k));
     }
-    __threadfence_system();
+    // every CTA's stores, then one system-scope fence per CTA (after the
+    // barrier, as in a grid-wide sync); the last CTA releases the epoch
     __syncthreads();
     if (threadIdx.x == 0) {
+        __threadfence_system();
         const unsigned int prev = atomicAdd(a.done, 1u);
         if (prev == gridDim.x - 1) {
             __threadfence_system();
@@ -605,9 +608,7 @@ __global__ void peer_wait_kernel(PeerWait w) { peer_wait(w.flags, w.peers, w.n, 
 
 cudaError_t launch_push(const PushArgs& a, cudaStream_t s) {
     if (a.n_nbr <= 0) return cudaSuccess;
-    int blocks = (a.n + 255) / 256;
-    if (blocks > num_sms() * 4) blocks = num_sms() * 4;
-    if (blocks < 1) blocks = 1;
+    const int blocks = a.n_chunks > 0 ? a.n_chunks : 1;  // >= 1: the flags go out even with no data
     push_kernel<<<blocks, 256, 0, s>>>(a);
     return cudaGetLastError();
 }

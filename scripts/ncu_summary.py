@@ -74,8 +74,14 @@ def main():
         except Exception:
             cur = {}
         vals = [l["dram_bytes_per_launch"] for l in launches if l["dram_bytes_per_launch"]]
-        cur[config] = {"dram_bytes_per_launch": round(sum(vals) / len(vals)), "kernel": launches[0]["kernel"],
-                       "source": os.path.relpath(out, os.path.dirname(tj))}
+        ent = cur.get(config, {})
+        kern = ent.get("kernels", {})
+        kname = launches[0]["kernel"].split("(")[0].replace("void ", "")
+        kern[kname.split("<")[0]] = {"dram_bytes_per_launch": round(sum(vals) / len(vals)), "kernel": kname,
+                                     "source": os.path.relpath(out, os.path.dirname(tj))}
+        # a step launches each of these kernels once: its traffic is their sum
+        ent = {"dram_bytes_per_step": sum(k["dram_bytes_per_launch"] for k in kern.values()), "kernels": kern}
+        cur[config] = ent
         json.dump(cur, open(tj, "w"), indent=1)
     print("\n".join(lines))
 
