@@ -104,11 +104,12 @@ static void plan_chunks(hec_matrix_s* m, const HostHec& h, bool pipelined, std::
         while (t1 < tr && h.tail_rows[t1] < m->chunk_row[c + 1]) ++t1;
         for (int32_t sb = t0; sb < t1; sb += kTailSuperRows) {
             const int32_t se = std::min(t1, sb + kTailSuperRows);
-            int32_t cnt[6] = {0, 0, 0, 0, 0, 0}, pos[6];
+            constexpr int NG = kTailMaxLg + 1;
+            int32_t cnt[NG] = {}, pos[NG];
             for (int32_t t = sb; t < se; ++t) cnt[tail_lg_for(tp[t + 1] - tp[t], epl)]++;
             pos[0] = sb;
-            for (int g = 1; g < 6; ++g) pos[g] = pos[g - 1] + cnt[g - 1];
-            for (int g = 0; g < 6; ++g) {
+            for (int g = 1; g < NG; ++g) pos[g] = pos[g - 1] + cnt[g - 1];
+            for (int g = 0; g < NG; ++g) {
                 const int32_t per_blk = 256 >> g;
                 for (int32_t f = pos[g]; f < pos[g] + cnt[g]; f += per_blk)
                     blk->push_back(make_int4(f, std::min(per_blk, pos[g] + cnt[g] - f), g, 0));

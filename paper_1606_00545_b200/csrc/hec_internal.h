@@ -69,10 +69,22 @@ hec_status convert(const CsrView& A, int32_t width, int32_t stride_unit, HostHec
 constexpr int kTailSuperRows = 4096;   // tail rows regrouped by length within blocks of this many
 
 // Lanes per tail row: the smallest power of two >= ceil(L / epl), capped at
-// 32, where epl = target entries per lane.
+// 2^kTailMaxLg, where epl = target entries per lane.  Up to 32 lanes a row
+// lives in one warp (shuffle reduction); 64-256 lanes span 2-8 warps of one
+// CTA (shuffle, then the warps' partials combined through shared memory).
+constexpr int kTailMaxLg = 8;
+inline int tail_max_lg() {             // HEC_TAIL_MAXLG (tuning): 5..8
+    static int v = -1;
+    if (v < 0) {
+        const char* e = std::getenv("HEC_TAIL_MAXLG");
+        v = e ? std::max(5, std::min(kTailMaxLg, std::atoi(e))) : kTailMaxLg;
+    }
+    return v;
+}
 inline int tail_lg_for(int32_t L, int epl) {
     int lg = 0;
-    while (lg < 5 && (epl << lg) < L) ++lg;
+    const int cap = tail_max_lg();
+    while (lg < cap && (epl << lg) < L) ++lg;
     return lg;
 }
 

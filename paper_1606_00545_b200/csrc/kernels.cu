@@ -303,6 +303,7 @@ __global__ void __launch_bounds__(256, EPI == EPI_JACOBI ? HEC_JAC_MINB : 0) ell
 // One block descriptor's work for the 256 threads tid = 0..255 of a group.
 template <bool HALO, bool JACOBI>
 __device__ __forceinline__ void tail_desc(const TailArgs& a, int4 d, int tid, uint64_t pol) {
+    __shared__ double wsum[8];  // per-warp partials of rows wider than a warp
     const int lg = d.z;
     const int G = 1 << lg;
     const int lane = tid & (G - 1);
@@ -327,7 +328,20 @@ __device__ __forceinline__ void tail_desc(const TailArgs& a, int4 d, int tid, ui
             acc = fma(v, gather_x<HALO>(a.x, a.x_halo, a.n_loc, c), acc);
         }
     }
-    for (int off = G >> 1; off > 0; off >>= 1) acc += __shfl_xor_sync(0xffffffffu, acc, off, G);
+    if (lg <= 5) {
+        for (int off = G >> 1; off > 0; off >>= 1) acc += __shfl_xor_sync(0xffffffffu, acc, off, G);
+    } else {
+        // a row spans G / 32 warps: full-warp shuffle, then the row's first
+        // warp adds the warps' partials in warp order (deterministic)
+        for (int off = 16; off > 0; off >>= 1) acc += __shfl_xor_sync(0xffffffffu, acc, off);
+        if ((tid & 31) == 0) wsum[tid >> 5] = acc;
+        __syncthreads();
+        if (lane == 0) {
+            const int w0 = tid >> 5, nw = G >> 5;
+            acc = wsum[w0];
+            for (int w = 1; w < nw; ++w) acc += wsum[w0 + w];
+        }
+    }
     // y holds the ELL result: with programmatic dependent launch this kernel may
     // have started before ell_kernel finished, so wait for it here (a no-op
     // when launched normally or once it has returned)
