@@ -99,7 +99,7 @@ typedef struct {
     int64_t nnz;           /* nnz(A) = ell_nnz + tail_nnz */
     int64_t ell_nnz;       /* non-padding ELL slots */
     int32_t tail_rows;     /* rows that spill into the CSR part */
-    int32_t tail_group;    /* lanes per tail row used by the tail kernel (1..32) */
+    int32_t tail_group;    /* maximum lanes per tail row used by the tail kernel (rows take 1..256) */
     int64_t tail_nnz;
     int64_t device_bytes;  /* bytes of device arrays owned by the handle */
     int32_t device;        /* CUDA device ordinal, or -1 for a host-only handle */

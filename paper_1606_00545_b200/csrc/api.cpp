@@ -346,7 +346,7 @@ hec_status hec_info(hec_matrix A, hec_matrix_info* o) {
     o->nnz = A->nnz;
     o->ell_nnz = A->ell_nnz;
     o->tail_rows = A->tail_rows;
-    o->tail_group = 32;
+    o->tail_group = 1 << tail_max_lg();
     o->tail_nnz = A->tail_nnz;
     o->device_bytes = A->device_bytes;
     o->device = A->device;

@@ -8,9 +8,15 @@
 //                loads.  The matrix streams are read once with L1::no_allocate
 //                and an L2 evict_first policy so x stays cached for the gathers.
 //   tail_kernel  Alg. 1 lines 5-7: the CSR remainder of the rows
-//                that spill, G lanes per row, reduced with __shfl_xor_sync and
-//                added into the ELL result (ordered after ell_kernel).
-//   pack_kernel  the halo export of P:158: sendbuf[k] = x_local[send_idx[k]].
+//                that spill, G = 1..256 lanes per row, reduced with
+//                __shfl_xor_sync (and shared memory across warps) and added
+//                into the ELL result (ordered after ell_kernel).
+//   coo_kernel   HYB comparison variant: the remainder as COO with atomics.
+//   pack_kernel  the halo export of P:158 for the NCCL transport:
+//                sendbuf[k] = x_local[send_idx[k]].
+//   push_kernel / peer_wait_kernel  the peer-memory transport (export + NVLink
+//                stores + epoch flags).
+//   diag kernels  A_ii for the damped-Jacobi sweep (EPI_JACOBI epilogue).
 //
 // No tensor cores: SpMV is not a dense contraction (BASELINE.json north_star);
 // the roofline is HBM bandwidth.
