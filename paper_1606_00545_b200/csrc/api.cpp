@@ -51,7 +51,8 @@ static void plan_chunks(hec_matrix_s* m, const HostHec& h, bool pipelined, std::
                         std::vector<int4>* blk) {
     const int32_t n = h.n_rows;
     // ~1M-row chunks, at most 16 (32 chunks measured slower: 3.62 vs 3.41 ms on
-    // 256^3; the floor is the concurrent H2D + D2H of x and y, 2.75 ms there)
+    // 256^3; smaller first/last chunks too: 3.36 vs 3.31 ms; the floor is the
+    // concurrent H2D + D2H of x and y, 2.78 ms there)
     int32_t K = pipelined ? n / (1 << 20) : 1;
     K = K < 1 ? 1 : (K > 16 ? 16 : K);
     int64_t per = ((int64_t)n + K - 1) / K;
@@ -511,11 +512,11 @@ hec_status hec_spmv_host(hec_matrix A, const double* x_host, double* y_host, voi
             HEC_CUDA_TRY(cudaEventCreateWithFlags(&A->ev_y[c], cudaEventDisableTiming));
         }
     }
+    // x piece p = the part of the x prefix chunk p needs beyond chunk p-1's
+    // (chunk_xend is non-decreasing), so chunk p waits for exactly its piece
     std::vector<int64_t> xb(K + 1);
-    for (int p = 0; p <= K; ++p) {
-        int64_t b = ((int64_t)p * A->n_cols / K + 511) / 512 * 512;
-        xb[p] = std::min<int64_t>(b, A->n_cols);
-    }
+    xb[0] = 0;
+    for (int p = 1; p < K; ++p) xb[p] = std::max<int64_t>(xb[p - 1], std::min<int64_t>(A->chunk_xend[p - 1], A->n_cols));
     xb[K] = A->n_cols;
     HEC_CUDA_TRY(cudaEventRecord(A->ev_start, s));  // ordered after prior work on s
     HEC_CUDA_TRY(cudaStreamWaitEvent(A->s_h2d, A->ev_start, 0));
