@@ -549,10 +549,11 @@ def run_solver(args):
     K = args.steps
     x.zero_()
     e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-    e0.record()
-    info = solve(b, x, 0.0, K)                                   # tol 0: exactly K iterations
-    e1.record()
-    torch.cuda.synchronize()
+    with ClockSampler(0) as clk:
+        e0.record()
+        info = solve(b, x, 0.0, K)                               # tol 0: exactly K iterations
+        e1.record()
+        torch.cuda.synchronize()
     ms = e0.elapsed_time(e1)
     n, alg = A.n_rows, algorithmic_bytes(A.nnz, A.n_rows, A.n_cols)
     # per iteration: CG = 1 SpMV + dot(p,q) 2n + x,r update 6n + p update 3n (doubles)
@@ -580,7 +581,10 @@ def run_solver(args):
                          "frac": round(per_it * it_s / 1e9 / peak, 4), "traffic": None,
                          "kernel": "whole iteration (SpMV + fused vector passes)",
                          "algorithmic_bytes_per_iteration": per_it, "peak_source": peak_src},
-            "cpu_baseline": cpu}
+            "cpu_baseline": cpu,
+            # per iteration: CG = SpMV + 3 fused passes; BiCGSTAB = 2 SpMV + 6 passes + 1 step kernel
+            "gpu_launches": info.iterations * (M.launches + 3 if args.solver == "cg" else 2 * M.launches + 7),
+            "clocks": clk.summary()}
     print(json.dumps(line), flush=True)
     return 0
 
