@@ -348,16 +348,19 @@ __device__ __forceinline__ void tail_desc(const TailArgs& a, int4 d, int tid, ui
             for (int w = 1; w < nw; ++w) acc += wsum[w0 + w];
         }
     }
+    // The row's one addition into the ELL result, y_i = ell_i + tail_i, as a
+    // fire-and-forget reduction at L2 (red.global.add.f64): no load of y, so
+    // the CTA retires without another memory round trip.  Each row has exactly
+    // one tail sum and the ELL kernel has finished, so the result is the same
+    // single rounded addition as a load-add-store (y - q == y + (-q) in IEEE).
+    double q = 0.0;
+    if (lane == 0 && active)  // the ELL kernel wrote x + omega ((b - s_ell) / d): add -omega (s_tail / d)
+        q = JACOBI ? -__dmul_rn(a.omega, __ddiv_rn(acc, __ldg(a.diag + orow))) : __dmul_rn(a.alpha, acc);
     // y holds the ELL result: with programmatic dependent launch this kernel may
     // have started before ell_kernel finished, so wait for it here (a no-op
     // when launched normally or once it has returned)
     asm volatile("griddepcontrol.wait;" ::: "memory");
-    if (lane == 0 && active) {
-        if (JACOBI)  // the ELL kernel wrote x + omega ((b - s_ell) / d): subtract omega (s_tail / d)
-            *yp = __dsub_rn(*yp, __dmul_rn(a.omega, __ddiv_rn(acc, __ldg(a.diag + orow))));
-        else
-            *yp = *yp + a.alpha * acc;
-    }
+    if (lane == 0 && active) asm volatile("red.global.add.f64 [%0], %1;" ::"l"(yp), "d"(q) : "memory");
 }
 
 template <bool HALO, bool JACOBI>
