@@ -55,6 +55,8 @@ def _load():
         lib.hecgen_powerlaw_rowptr.argtypes = [i32, i32, i32, dbl, u64, vp]
         lib.hecgen_powerlaw_fill.restype = ctypes.c_int
         lib.hecgen_powerlaw_fill.argtypes = [i32, i32, dbl, ctypes.c_int, u64, vp, vp, vp]
+        lib.hecgen_degree_sort.restype = ctypes.c_int
+        lib.hecgen_degree_sort.argtypes = [i32, vp, vp, vp, vp, vp, vp, vp]
         lib.hecgen_spe10.restype = ctypes.c_int
         lib.hecgen_spe10.argtypes = [i32, i32, i32, u64, ctypes.POINTER(i32), ctypes.POINTER(i64),
                                      ctypes.POINTER(ctypes.POINTER(i32)), ctypes.POINTER(ctypes.POINTER(i32)),
@@ -175,6 +177,26 @@ def powerlaw(n: int, lmin: int = 4, lmax: int = 2000, alpha: float = POWERLAW_AL
     return Csr(n, n, rp, col, val, name=f"powerlaw_{n}{'_int' if integer_values else ''}")
 
 
+def degree_sorted(A: Csr) -> Csr:
+    """Degree-sorted stress variant (SURVEY §8(d) power-law recipe): the
+    symmetric permutation P A P^T that puts rows in descending length order
+    (stable), columns renamed with it and re-sorted.  Returns the matrix; its
+    ``perm`` attribute holds perm[new] = old."""
+    lib = _load()
+    n = A.n_rows
+    if A.n_cols != n:
+        raise ValueError("degree_sorted: square matrices only")
+    perm = np.empty(n, np.int32)
+    rp = np.empty(n + 1, np.int32)
+    col = np.empty(A.nnz, np.int32)
+    val = np.empty(A.nnz, np.float64)
+    if lib.hecgen_degree_sort(n, _p(A.row_ptr), _p(A.col), _p(A.val), _p(perm), _p(rp), _p(col), _p(val)) != 0:
+        raise ValueError("degree_sorted failed")
+    B = Csr(n, n, rp, col, val, name=f"{A.name}_dsorted")
+    B.perm = perm
+    return B
+
+
 def spe10(nx: int = 60, ny: int = 220, nz: int = 85, seed: int = 10) -> Csr:
     """SPE10-shaped reservoir matrix (SURVEY §8(d) 'SPE10 recipe')."""
     lib = _load()
@@ -240,4 +262,6 @@ CONFIGS = {
     "spe10": lambda: spe10(60, 220, 85),
     "powerlaw_8M": lambda: powerlaw(1 << 23),
     "poisson3d_150": lambda: poisson3d(150, 150, 150),  # the paper's own 3D_Poisson
+    # SURVEY §8(d) secondary row: the power-law matrix with rows in descending length order
+    "powerlaw_8M_dsorted": lambda: degree_sorted(powerlaw(1 << 23)),
 }

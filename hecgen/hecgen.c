@@ -238,6 +238,51 @@ int hecgen_powerlaw_fill(int32_t n, int32_t band, double p_local, int integer_va
     return 0;
 }
 
+/* Degree-sorted stress variant (SURVEY §8(d) power-law recipe): B = P A P^T
+ * with rows in descending length order, ties by ascending original row
+ * (stable), i.e. perm[r] = the original row placed at r, and every column
+ * renamed j -> inv[j] then re-sorted within its row (values move with their
+ * columns).  Square A only.  Output arrays sized like A's. */
+typedef struct { int32_t c; int32_t k; } hg_ck;
+static int cmp_ck(const void* a, const void* b) {
+    int32_t x = ((const hg_ck*)a)->c, y = ((const hg_ck*)b)->c;
+    return (x > y) - (x < y);
+}
+
+int hecgen_degree_sort(int32_t n, const int32_t* row_ptr, const int32_t* col, const double* val,
+                       int32_t* perm, int32_t* out_rp, int32_t* out_col, double* out_val) {
+    if (n < 1) return 1;
+    int32_t lmax = 0;
+    for (int32_t i = 0; i < n; ++i) {
+        int32_t L = row_ptr[i + 1] - row_ptr[i];
+        if (L > lmax) lmax = L;
+    }
+    /* counting sort by descending length, stable */
+    int64_t* start = calloc((size_t)lmax + 2, sizeof(int64_t));
+    int32_t* inv = malloc(sizeof(int32_t) * (size_t)n);
+    hg_ck* buf = malloc(sizeof(hg_ck) * ((size_t)lmax + 1));
+    if (!start || !inv || !buf) { free(start); free(inv); free(buf); return 2; }
+    for (int32_t i = 0; i < n; ++i) start[lmax - (row_ptr[i + 1] - row_ptr[i]) + 1]++;
+    for (int32_t l = 1; l <= lmax + 1; ++l) start[l] += start[l - 1];
+    for (int32_t i = 0; i < n; ++i) {
+        int64_t r = start[lmax - (row_ptr[i + 1] - row_ptr[i])]++;
+        perm[r] = i;
+        inv[i] = (int32_t)r;
+    }
+    out_rp[0] = 0;
+    for (int32_t r = 0; r < n; ++r) {
+        const int32_t i = perm[r];
+        const int32_t b = row_ptr[i], L = row_ptr[i + 1] - b;
+        for (int32_t k = 0; k < L; ++k) { buf[k].c = inv[col[b + k]]; buf[k].k = b + k; }
+        qsort(buf, (size_t)L, sizeof(hg_ck), cmp_ck);
+        const int32_t o = out_rp[r];
+        for (int32_t k = 0; k < L; ++k) { out_col[o + k] = buf[k].c; out_val[o + k] = val[buf[k].k]; }
+        out_rp[r + 1] = o + L;
+    }
+    free(start); free(inv); free(buf);
+    return 0;
+}
+
 /* ------------------------------------------------------ SPE10-shaped ---- */
 /* 60 x 220 x 85 grid (SURVEY §8(d) "SPE10 recipe"), cells inactive with
  * probability p_inact, log-permeability from seeded smooth fields (Tarbert-like

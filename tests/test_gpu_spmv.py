@@ -40,6 +40,7 @@ CONFIGS = [
     ("poisson3d_32", lambda: hecgen.poisson3d(32, 32, 32)),
     ("spe10", lambda: hecgen.spe10(60, 220, 85)),                # configs[3], full size
     ("powerlaw_64k", lambda: hecgen.powerlaw(1 << 16)),
+    ("powerlaw_64k_dsorted", lambda: hecgen.degree_sorted(hecgen.powerlaw(1 << 16))),  # §8(d) stress variant
     ("random_rect", lambda: hecgen.random_csr(300, 170, 0.05, seed=3)),
 ]
 
@@ -54,13 +55,15 @@ def test_parity_uniform_x(name, maker):
         assert M.info.tail_rows > 0 and M.launches == 2        # the CSR tail is exercised
 
 
-@pytest.mark.parametrize("name,maker", CONFIGS[:4])
+@pytest.mark.parametrize("name,maker", CONFIGS[:5])
 def test_integer_regime_bitwise(name, maker):
     A = maker()
     if name == "spe10":
         pytest.skip("SPE10 coefficients are not integers")
     if name.startswith("powerlaw"):
         A = hecgen.powerlaw(1 << 16, integer_values=True)
+        if name.endswith("dsorted"):
+            A = hecgen.degree_sorted(A)
     x = hecgen.vector(A.n_cols, "int", seed=7)
     y, _ = gpu_spmv(A, x)
     assert y.tobytes() == oracle.csr_spmv(A, x).tobytes()
@@ -104,6 +107,19 @@ def test_powerlaw_full_size_sampled():
     assert M.info.ell_width == 9 and M.info.tail_rows > 2_000_000
     rng = np.random.default_rng(1)
     for r0 in np.concatenate([[0, A.n_rows - 2048], rng.integers(0, A.n_rows - 2048, 20)]):
+        assert_parity(A, x, y[r0:r0 + 2048], int(r0), int(r0) + 2048)
+
+
+def test_powerlaw_degree_sorted_full_size_sampled():
+    # SURVEY §8(d) secondary row: configs[4] with rows in descending length
+    # order -- every tail row is at the top, the longest (2,000) first.
+    A = hecgen.degree_sorted(hecgen.powerlaw(1 << 23))
+    x = hecgen.vector(A.n_cols, "uniform", seed=1606)
+    y, M = gpu_spmv(A, x)
+    assert M.info.ell_width == 9
+    assert np.all(np.diff(A.row_ptr)[:M.info.tail_rows] > 9)   # the tail is exactly the top rows
+    rng = np.random.default_rng(2)
+    for r0 in np.concatenate([[0, M.info.tail_rows - 1024, A.n_rows - 2048], rng.integers(0, A.n_rows - 2048, 12)]):
         assert_parity(A, x, y[r0:r0 + 2048], int(r0), int(r0) + 2048)
 
 
