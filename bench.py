@@ -736,6 +736,9 @@ def run_formats(args):
 
 def main():
     args = parse()
+    # stdout carries exactly one JSON line: NCCL's own messages (the box may
+    # set NCCL_DEBUG, e.g. the "NCCL version" banner) go to stderr instead
+    os.environ.setdefault("NCCL_DEBUG_FILE", "/dev/stderr")
     if args.formats:
         return run_formats(args)
     if args.solver:
