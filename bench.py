@@ -736,9 +736,13 @@ def run_formats(args):
 
 def main():
     args = parse()
-    # stdout carries exactly one JSON line: NCCL's own messages (the box may
-    # set NCCL_DEBUG, e.g. the "NCCL version" banner) go to stderr instead
-    os.environ.setdefault("NCCL_DEBUG_FILE", "/dev/stderr")
+    # stdout carries exactly the JSON line: whatever native code writes to
+    # file descriptor 1 (NCCL prints its "NCCL version" banner there) goes to
+    # stderr, and Python's stdout keeps the original descriptor
+    sys.stdout.flush()
+    json_fd = os.dup(1)
+    os.dup2(2, 1)
+    sys.stdout = os.fdopen(json_fd, "w", buffering=1)
     if args.formats:
         return run_formats(args)
     if args.solver:
@@ -753,7 +757,7 @@ def main():
             # self-launch under torchrun
             cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", f"--nproc-per-node={args.gpus}",
                    "--master-addr=127.0.0.1", "--master-port=29533", __file__] + sys.argv[1:]
-            return subprocess.call(cmd)
+            return subprocess.call(cmd, stdout=sys.stdout)
         return run_multi(args)
     return run_single(args)
 

@@ -94,6 +94,18 @@ __device__ __forceinline__ int32_t ld_l1_i1(const int32_t* ptr, uint64_t pol) {
     return r;
 }
 
+__device__ __forceinline__ int2 ld_l1_i2(const int32_t* ptr, uint64_t pol) {
+    int2 r;
+    asm("ld.global.nc.L2::cache_hint.v2.s32 {%0, %1}, [%2], %3;" : "=r"(r.x), "=r"(r.y) : "l"(ptr), "l"(pol));
+    return r;
+}
+
+__device__ __forceinline__ double2 ld_l1_d2(const double* ptr, uint64_t pol) {
+    double2 r;
+    asm("ld.global.nc.L2::cache_hint.v2.f64 {%0, %1}, [%2], %3;" : "=d"(r.x), "=d"(r.y) : "l"(ptr), "l"(pol));
+    return r;
+}
+
 __device__ __forceinline__ double ld_l1_d1(const double* ptr, uint64_t pol) {
     double r;
     asm("ld.global.nc.L2::cache_hint.f64 %0, [%1], %2;" : "=d"(r) : "l"(ptr), "l"(pol));
@@ -178,6 +190,10 @@ __device__ __forceinline__ double jacobi_row(double x, double b, double d, doubl
     return __dadd_rn(x, __dmul_rn(omega, __ddiv_rn(__dsub_rn(b, s), d)));
 }
 
+#ifndef HEC_TAIL_UNROLL
+#define HEC_TAIL_UNROLL 2  // entry pairs per lane unrolled (measured 2 > 4 = 8)
+#endif
+constexpr int kTailUnroll = HEC_TAIL_UNROLL;
 #ifndef HEC_ELL_PHASE
 #define HEC_ELL_PHASE 8  // widths above this load their slots in two phases (measured: 8 > 16 > 6)
 #endif
@@ -325,13 +341,19 @@ __device__ __forceinline__ void tail_desc(const TailArgs& a, int4 d, int tid, ui
             orow = __ldg(a.out_rows + t);
             yp = a.y + orow;
         }
-#pragma unroll 8
-        for (int32_t k = kb + lane; k < ke; k += G) {
-            // L1-allocating: the G lanes of a row revisit each 32-byte sector
-            // on consecutive iterations (k += G), which then hit in L1
-            const int32_t c = ld_l1_i1(a.col + k, pol);
-            const double v = ld_l1_d1(a.val + k, pol);
-            acc = fma(v, gather_x<HALO>(a.x, a.x_halo, a.n_loc, c), acc);
+        // Entry pairs: rows start at even positions and have even (padded)
+        // length, so lane l takes entries 2l, 2l+1, 2l+2G, ... as one 64-bit
+        // index and one 128-bit value load.  L1-allocating: the lanes of a
+        // row revisit each 32-byte sector on consecutive iterations.  The
+        // padding entry (-1, +0.0) reads no x and adds nothing.
+#pragma unroll kTailUnroll
+        for (int32_t k = kb + 2 * lane; k < ke; k += 2 * G) {
+            const int2 c = ld_l1_i2(a.col + k, pol);
+            const double2 v = ld_l1_d2(a.val + k, pol);
+            const double x0 = gather_x<HALO>(a.x, a.x_halo, a.n_loc, c.x);
+            const double x1 = c.y >= 0 ? gather_x<HALO>(a.x, a.x_halo, a.n_loc, c.y) : 0.0;
+            acc = fma(v.x, x0, acc);
+            if (c.y >= 0) acc = fma(v.y, x1, acc);
         }
     }
     if (lg <= 5) {
@@ -363,8 +385,12 @@ __device__ __forceinline__ void tail_desc(const TailArgs& a, int4 d, int tid, ui
     if (lane == 0 && active) asm volatile("red.global.add.f64 [%0], %1;" ::"l"(yp), "d"(q) : "memory");
 }
 
+#ifndef HEC_TAIL_MINB
+#define HEC_TAIL_MINB 8  // 8 CTAs (64 warps) per SM: the latency-bound tail wants every warp slot
+#endif
+
 template <bool HALO, bool JACOBI>
-__global__ void __launch_bounds__(256) tail_kernel(TailArgs a) {
+__global__ void __launch_bounds__(256, HEC_TAIL_MINB) tail_kernel(TailArgs a) {
     const uint64_t pol = policy_evict_first();
     tail_desc<HALO, JACOBI>(a, __ldg(a.blk + a.blk_begin + blockIdx.x), threadIdx.x, pol);
 }
@@ -539,7 +565,23 @@ cudaError_t launch_ell(const EllArgs& a, cudaStream_t s) {
     return rowmap ? launch_ell_t<false, true, EPI_NONE>(a, s) : launch_ell_t<false, false, EPI_NONE>(a, s);
 }
 
+// HEC_TAIL_CARVEOUT (tuning): the tail kernels' preferred shared-memory
+// carveout in percent (0 = as much L1 as possible for the x gathers)
+static void tail_carveout() {
+    static bool done = false;
+    if (done) return;
+    done = true;
+    const char* e = std::getenv("HEC_TAIL_CARVEOUT");
+    if (!e) return;
+    const int pct = std::atoi(e);
+    cudaFuncSetAttribute(tail_kernel<false, false>, cudaFuncAttributePreferredSharedMemoryCarveout, pct);
+    cudaFuncSetAttribute(tail_kernel<true, false>, cudaFuncAttributePreferredSharedMemoryCarveout, pct);
+    cudaFuncSetAttribute(tail_kernel<false, true>, cudaFuncAttributePreferredSharedMemoryCarveout, pct);
+    cudaGetLastError();
+}
+
 cudaError_t launch_tail(const TailArgs& a, cudaStream_t s) {
+    tail_carveout();
     const int64_t blocks = a.blk_end - a.blk_begin;
     if (blocks <= 0) return cudaSuccess;
     if (blocks > 0x7fffffff) return cudaErrorInvalidValue;
