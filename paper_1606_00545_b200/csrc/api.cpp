@@ -177,13 +177,13 @@ hec_status make_matrix(HostHec&& h, int32_t device, cudaStream_t s, const int32_
         // inside super-blocks, plan_chunks): a block's rows and their entries
         // are contiguous, and the kernel needs no indirection.  hec_export
         // undoes the permutation with m->h_tail_order.
-        // Every row starts at an even position (rows of odd length get one
-        // padding entry (-1, +0.0), reading A4's convention) so the kernel
-        // reads entry pairs as 64-bit index / 128-bit value loads.
+        // Every row starts at a multiple of kTailVec (rows are padded with
+        // (-1, +0.0) entries, reading A4's convention) so the kernel reads
+        // kTailVec entries per lane as vector index / value loads.
         const size_t tr = h.tail_rows.size();
         std::vector<int32_t> dptr(tr + 1), dout(tr);
         int64_t padded = 0;
-        for (size_t t = 0; t < tr; ++t) padded += (h.tail_ptr[t + 1] - h.tail_ptr[t] + 1) & ~1;
+        for (size_t t = 0; t < tr; ++t) padded += (h.tail_ptr[t + 1] - h.tail_ptr[t] + kTailVec - 1) / kTailVec * kTailVec;
         if (padded > INT32_MAX) return fail(HEC_ERR_DIM, "padded CSR tail exceeds int32 positions");
         std::vector<int32_t> dcol((size_t)padded, -1);
         std::vector<double> dval((size_t)padded, 0.0);
@@ -193,7 +193,7 @@ hec_status make_matrix(HostHec&& h, int32_t device, cudaStream_t s, const int32_
             const int32_t b = h.tail_ptr[t], e = h.tail_ptr[t + 1];
             std::copy(h.tail_col.begin() + b, h.tail_col.begin() + e, dcol.begin() + dptr[p]);
             std::copy(h.tail_val.begin() + b, h.tail_val.begin() + e, dval.begin() + dptr[p]);
-            dptr[p + 1] = dptr[p] + ((e - b + 1) & ~1);
+            dptr[p + 1] = dptr[p] + (e - b + kTailVec - 1) / kTailVec * kTailVec;
             dout[p] = rowmap ? rowmap[h.tail_rows[t]] : row_off + h.tail_rows[t];
         }
         m->h_tail_order = order;
@@ -403,7 +403,7 @@ hec_status hec_export(hec_matrix A, hec_host_arrays* o) {
     for (size_t t = 0; t < tr; ++t) {
         const int32_t p = where[t], b = dptr[p];
         int32_t e = dptr[p + 1];
-        if (e > b && dcol[e - 1] < 0) --e;  // drop the padding entry
+        while (e > b && dcol[e - 1] < 0) --e;  // drop the padding entries
         if (o->tail_ptr) o->tail_ptr[t] = k;
         if (o->tail_col) std::copy(dcol.begin() + b, dcol.begin() + e, o->tail_col + k);
         if (o->tail_val) std::copy(dval.begin() + b, dval.begin() + e, o->tail_val + k);

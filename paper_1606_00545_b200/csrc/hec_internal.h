@@ -66,6 +66,11 @@ int32_t choose_width(const CsrView& A, const hec_opts& o);
 hec_status convert(const CsrView& A, int32_t width, int32_t stride_unit, HostHec* out);
 // CSR-tail work unit: at most this many spilled entries start rows owned by
 // one warp (see plan_chunks in api.cpp), so a unit owns <= 256 rows.
+#ifndef HEC_TAIL_VEC
+#define HEC_TAIL_VEC 2  // tail entries per lane load (2: int2/double2; 4: int4 + 2 double2)
+#endif
+constexpr int kTailVec = HEC_TAIL_VEC;  // device tail rows padded to a multiple of this
+static_assert(kTailVec == 2 || kTailVec == 4, "HEC_TAIL_VEC must be 2 or 4");
 constexpr int kTailSuperRows = 4096;   // tail rows regrouped by length within blocks of this many
 
 // Lanes per tail row: the smallest power of two >= ceil(L / epl), capped at

@@ -100,6 +100,13 @@ __device__ __forceinline__ int2 ld_l1_i2(const int32_t* ptr, uint64_t pol) {
     return r;
 }
 
+__device__ __forceinline__ int4 ld_l1_i4(const int32_t* ptr, uint64_t pol) {
+    int4 r;
+    asm("ld.global.nc.L2::cache_hint.v4.s32 {%0, %1, %2, %3}, [%4], %5;"
+        : "=r"(r.x), "=r"(r.y), "=r"(r.z), "=r"(r.w) : "l"(ptr), "l"(pol));
+    return r;
+}
+
 __device__ __forceinline__ double2 ld_l1_d2(const double* ptr, uint64_t pol) {
     double2 r;
     asm("ld.global.nc.L2::cache_hint.v2.f64 {%0, %1}, [%2], %3;" : "=d"(r.x), "=d"(r.y) : "l"(ptr), "l"(pol));
@@ -341,19 +348,32 @@ __device__ __forceinline__ void tail_desc(const TailArgs& a, int4 d, int tid, ui
             orow = __ldg(a.out_rows + t);
             yp = a.y + orow;
         }
-        // Entry pairs: rows start at even positions and have even (padded)
-        // length, so lane l takes entries 2l, 2l+1, 2l+2G, ... as one 64-bit
-        // index and one 128-bit value load.  L1-allocating: the lanes of a
+        // Entry pairs (kTailVec = 2; or quads): rows start at even positions
+        // and have even (padded) length, so lane l takes entries 2l, 2l+1,
+        // 2l+2G, ... as one 64-bit index and one 128-bit value load.  L1-allocating: the lanes of a
         // row revisit each 32-byte sector on consecutive iterations.  The
         // padding entry (-1, +0.0) reads no x and adds nothing.
 #pragma unroll kTailUnroll
-        for (int32_t k = kb + 2 * lane; k < ke; k += 2 * G) {
-            const int2 c = ld_l1_i2(a.col + k, pol);
-            const double2 v = ld_l1_d2(a.val + k, pol);
-            const double x0 = gather_x<HALO>(a.x, a.x_halo, a.n_loc, c.x);
-            const double x1 = c.y >= 0 ? gather_x<HALO>(a.x, a.x_halo, a.n_loc, c.y) : 0.0;
-            acc = fma(v.x, x0, acc);
-            if (c.y >= 0) acc = fma(v.y, x1, acc);
+        for (int32_t k = kb + kTailVec * lane; k < ke; k += kTailVec * G) {
+            if constexpr (kTailVec == 2) {
+                const int2 c = ld_l1_i2(a.col + k, pol);
+                const double2 v = ld_l1_d2(a.val + k, pol);
+                const double x0 = gather_x<HALO>(a.x, a.x_halo, a.n_loc, c.x);
+                const double x1 = c.y >= 0 ? gather_x<HALO>(a.x, a.x_halo, a.n_loc, c.y) : 0.0;
+                acc = fma(v.x, x0, acc);
+                if (c.y >= 0) acc = fma(v.y, x1, acc);
+            } else {
+                const int4 c = ld_l1_i4(a.col + k, pol);
+                const double2 v0 = ld_l1_d2(a.val + k, pol), v1 = ld_l1_d2(a.val + k + 2, pol);
+                const double x0 = gather_x<HALO>(a.x, a.x_halo, a.n_loc, c.x);
+                const double x1 = c.y >= 0 ? gather_x<HALO>(a.x, a.x_halo, a.n_loc, c.y) : 0.0;
+                const double x2 = c.z >= 0 ? gather_x<HALO>(a.x, a.x_halo, a.n_loc, c.z) : 0.0;
+                const double x3 = c.w >= 0 ? gather_x<HALO>(a.x, a.x_halo, a.n_loc, c.w) : 0.0;
+                acc = fma(v0.x, x0, acc);
+                if (c.y >= 0) acc = fma(v0.y, x1, acc);
+                if (c.z >= 0) acc = fma(v1.x, x2, acc);
+                if (c.w >= 0) acc = fma(v1.y, x3, acc);
+            }
         }
     }
     if (lg <= 5) {
