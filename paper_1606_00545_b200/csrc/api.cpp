@@ -99,12 +99,14 @@ static void plan_chunks(hec_matrix_s* m, const HostHec& h, bool pipelined, std::
     // power-law 2^23 tail 8 > 4 > 2 > 1), worse for tiny ones (SPE10)
     int epl = h.tail_col.size() >= ((size_t)1 << 22) ? 8 : 2;
     if (const char* e = std::getenv("HEC_TAIL_EPL")) epl = std::max(1, std::min(16, std::atoi(e)));
+    int32_t super = kTailSuperRows;  // HEC_TAIL_SUPER (tuning)
+    if (const char* e = std::getenv("HEC_TAIL_SUPER")) super = std::max(256, std::atoi(e));
     int32_t t0 = 0;
     for (int c = 0; c < C; ++c) {
         int32_t t1 = t0;
         while (t1 < tr && h.tail_rows[t1] < m->chunk_row[c + 1]) ++t1;
-        for (int32_t sb = t0; sb < t1; sb += kTailSuperRows) {
-            const int32_t se = std::min(t1, sb + kTailSuperRows);
+        for (int32_t sb = t0; sb < t1; sb += super) {
+            const int32_t se = std::min(t1, sb + super);
             constexpr int NG = kTailMaxLg + 1;
             int32_t cnt[NG] = {}, pos[NG];
             for (int32_t t = sb; t < se; ++t) cnt[tail_lg_for(tp[t + 1] - tp[t], epl)]++;
