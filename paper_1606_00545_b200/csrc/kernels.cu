@@ -178,28 +178,6 @@ __device__ __forceinline__ double gather_x(const double* __restrict__ x,
     return __ldg(x + c);
 }
 
-#ifndef HEC_TAIL_XHINT
-#define HEC_TAIL_XHINT 0  // 1: the tail's x gathers carry an L2 evict_last policy (tuning)
-#endif
-__device__ __forceinline__ uint64_t policy_evict_last() {
-    uint64_t p;
-    asm("createpolicy.fractional.L2::evict_last.b64 %0, 1.0;" : "=l"(p));
-    return p;
-}
-
-template <bool HALO>
-__device__ __forceinline__ double gather_x_tail(const double* __restrict__ x, const double* __restrict__ xh,
-                                                int32_t n_loc, int32_t c, uint64_t xpol) {
-#if HEC_TAIL_XHINT
-    const double* p = (HALO && c >= n_loc) ? xh + (c - n_loc) : x + c;
-    double r;
-    asm("ld.global.nc.L2::cache_hint.f64 %0, [%1], %2;" : "=d"(r) : "l"(p), "l"(xpol));
-    return r;
-#else
-    (void)xpol;
-    return gather_x<HALO>(x, xh, n_loc, c);
-#endif
-}
 
 // ------------------------------------------------------------- ELL kernel --
 // W > 0: width known at compile time (fully unrolled); W == 0: runtime width.
@@ -367,7 +345,6 @@ __device__ __forceinline__ void tail_desc(const TailArgs& a, int4 d, int tid, ui
     if (active) {
         const int32_t t = d.x + grp;  // device position: the block's rows are contiguous
         const int32_t kb = __ldg(a.ptr + t), ke = __ldg(a.ptr + t + 1);
-        const uint64_t xpol = HEC_TAIL_XHINT ? policy_evict_last() : 0;
         if (lane == 0) {
             orow = __ldg(a.out_rows + t);
             yp = a.y + orow;
@@ -382,17 +359,17 @@ __device__ __forceinline__ void tail_desc(const TailArgs& a, int4 d, int tid, ui
             if constexpr (kTailVec == 2) {
                 const int2 c = ld_l1_i2(a.col + k, pol);
                 const double2 v = ld_l1_d2(a.val + k, pol);
-                const double x0 = gather_x_tail<HALO>(a.x, a.x_halo, a.n_loc, c.x, xpol);
-                const double x1 = c.y >= 0 ? gather_x_tail<HALO>(a.x, a.x_halo, a.n_loc, c.y, xpol) : 0.0;
+                const double x0 = gather_x<HALO>(a.x, a.x_halo, a.n_loc, c.x);
+                const double x1 = c.y >= 0 ? gather_x<HALO>(a.x, a.x_halo, a.n_loc, c.y) : 0.0;
                 acc = fma(v.x, x0, acc);
                 if (c.y >= 0) acc = fma(v.y, x1, acc);
             } else {
                 const int4 c = ld_l1_i4(a.col + k, pol);
                 const double2 v0 = ld_l1_d2(a.val + k, pol), v1 = ld_l1_d2(a.val + k + 2, pol);
-                const double x0 = gather_x_tail<HALO>(a.x, a.x_halo, a.n_loc, c.x, xpol);
-                const double x1 = c.y >= 0 ? gather_x_tail<HALO>(a.x, a.x_halo, a.n_loc, c.y, xpol) : 0.0;
-                const double x2 = c.z >= 0 ? gather_x_tail<HALO>(a.x, a.x_halo, a.n_loc, c.z, xpol) : 0.0;
-                const double x3 = c.w >= 0 ? gather_x_tail<HALO>(a.x, a.x_halo, a.n_loc, c.w, xpol) : 0.0;
+                const double x0 = gather_x<HALO>(a.x, a.x_halo, a.n_loc, c.x);
+                const double x1 = c.y >= 0 ? gather_x<HALO>(a.x, a.x_halo, a.n_loc, c.y) : 0.0;
+                const double x2 = c.z >= 0 ? gather_x<HALO>(a.x, a.x_halo, a.n_loc, c.z) : 0.0;
+                const double x3 = c.w >= 0 ? gather_x<HALO>(a.x, a.x_halo, a.n_loc, c.w) : 0.0;
                 acc = fma(v0.x, x0, acc);
                 if (c.y >= 0) acc = fma(v0.y, x1, acc);
                 if (c.z >= 0) acc = fma(v1.x, x2, acc);
