@@ -10,7 +10,7 @@ python -c "import __graft_entry__ as g; g.build(); g.smoke()" > $OUT/smoke.log 2
 timeout 1500 python -m pytest tests -m gpu -q -p no:cacheprovider > $OUT/pytest_gpu.log 2>&1; echo "pytest rc=$?" >> $OUT/pytest_gpu.log
 timeout 600 python bench.py > $OUT/bench.json 2> $OUT/bench.err
 timeout 600 python bench.py --impl reference --steps 5 --warmup 3 > $OUT/bench_reference.json 2>> $OUT/bench.err
-for cfg in poisson3d_128 spe10 powerlaw_8M poisson3d_150 poisson2d_64; do
+for cfg in poisson3d_128 spe10 powerlaw_8M poisson3d_150 poisson2d_64 powerlaw_8M_dsorted; do
   timeout 600 python bench.py --config $cfg --no-cpu-baseline > $OUT/bench_$cfg.json 2>> $OUT/bench.err
 done
 timeout 600 python bench.py --dist --steps 100 --warmup 5 --no-cpu-baseline > $OUT/bench_dist_n1.json 2>> $OUT/bench.err
