@@ -324,8 +324,8 @@ __global__ void __launch_bounds__(256, EPI == EPI_JACOBI ? HEC_JAC_MINB : 0) ell
 // The CSR part (Alg. 1 lines 5-7) for the rows that spill.  Rows
 // are regrouped by length inside super-blocks of consecutive tail rows
 // (plan_chunks, api.cpp): a CUDA block takes 256/G rows that all use G = 2^lg
-// lanes (G ~ half the spilled length, so each lane handles about two entries;
-// long rows loop).  The G lanes of a row read its contiguous entries, gather
+// lanes (G ~ spilled length / entries-per-lane target, 8 for big tails and 2
+// for small ones, capped at 256; longer rows loop).  The G lanes of a row read its contiguous entries, gather
 // x, reduce with __shfl_xor_sync and the first lane adds the row sum into the
 // ELL result (this kernel runs after ell_kernel on the same stream).
 // Blocks of one super-block run back to back, so its entries and the x window
