@@ -61,6 +61,8 @@ def parse():
                     help="experiment: FIXED ELL width instead of the BG3 rule (reading A1)")
     ap.add_argument("--transport", choices=["p2p", "nccl"], default="p2p",
                     help="N > 1 halo exchange: peer-memory push kernel over NVLink (default) or NCCL send/recv")
+    ap.add_argument("--partition", choices=["auto", "nnz", "cost"], default="auto",
+                    help="N > 1, non-grid matrices: CONTIG_NNZ (auto, reading A9) or CONTIG_COST (DESIGN §6)")
     ap.add_argument("--dist", action="store_true",
                     help="use the distributed path (hec_spmv_dist under torchrun) even with one GPU")
     return ap.parse_args()
@@ -405,7 +407,8 @@ def run_multi(args):
     torch.cuda.set_device(local)
     dist.init_process_group("nccl", device_id=torch.device(f"cuda:{local}"))
     A = hecgen.CONFIGS[args.config]()
-    kind = hec.PART_GRID if A.grid is not None else hec.PART_CONTIG_NNZ
+    kind = (hec.PART_GRID if A.grid is not None else
+            hec.PART_CONTIG_COST if args.partition == "cost" else hec.PART_CONTIG_NNZ)
     plan = hec.partition(A, world, kind, A.grid)
     obj = [hec.nccl_unique_id() if rank == 0 else None]
     dist.broadcast_object_list(obj, src=0)
@@ -509,7 +512,7 @@ def run_multi(args):
                 "warmup": args.warmup, "ms_per_step": round(ms_step, 5), "higher_is_better": True,
                 "scaling": "strong", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
                 "config": {"workload": args.config, "n_rows": A.n_rows, "nnz": A.nnz,
-                           "parallelism": f"row partition x{world} ({'GRID slabs' if kind == hec.PART_GRID else 'CONTIG_NNZ'}), "
+                           "parallelism": f"row partition x{world} ({'GRID slabs' if kind == hec.PART_GRID else 'CONTIG_COST' if kind == hec.PART_CONTIG_COST else 'CONTIG_NNZ'}), "
                                           + ("peer-memory halo push over NVLink" if transport == "p2p" else "NCCL halo exchange"),
                            "transport": transport if world > 1 else None,
                            "l2": ("L2 flushed (504 MiB write + 504 MiB read) before every step, outside the timed pair" if flush

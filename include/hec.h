@@ -224,7 +224,7 @@ void hec_free(hec_matrix A);
 
 /* ---------------------------------------------------------- partitions ---- */
 
-enum { HEC_PART_CONTIG_NNZ = 0, HEC_PART_CONTIG_ROWS = 1, HEC_PART_GRID = 2 };
+enum { HEC_PART_CONTIG_NNZ = 0, HEC_PART_CONTIG_ROWS = 1, HEC_PART_GRID = 2, HEC_PART_CONTIG_COST = 3 };
 
 typedef struct hec_plan_s* hec_plan;
 
@@ -237,6 +237,12 @@ typedef struct hec_plan_s* hec_plan;
  *   HEC_PART_CONTIG_ROWS: part_ptr[p] = floor(p*n/P).
  *   HEC_PART_CONTIG_NNZ: part_ptr[p] = lower_bound(row_ptr, ceil(p*nnz/P)),
  *     then max(., part_ptr[p-1]+1), then min(., n-(P-p)).
+ *   HEC_PART_CONTIG_COST (not in the paper): start from
+ *     CONTIG_NNZ; then 4 times (stopping early at a fixed point): with w_p =
+ *     the BG3 width (default options) of part p's rows, row i of part p costs
+ *     3 w_p + 4 max(len_i - w_p, 0) (padded ELL slots + tail entries, weights
+ *     from measured part times); part_ptr[p] = lower_bound(prefix cost,
+ *     ceil(p C / P)), clamped as for CONTIG_NNZ.
  * For every part: recv = sorted global columns referenced outside the part;
  * sends to peer q = sorted local indices of recv_q inside the part; boundary
  * rows = rows with any off-part column; interior = the rest.  Host-only,

@@ -8,7 +8,9 @@ provide" through a shared cache.  Readings:
   A9  GRID: part p owns planes [floor(p*nz/P), floor((p+1)*nz/P)) of the slowest
       axis with extent > 1; CONTIG_ROWS: floor(p*n/P); CONTIG_NNZ:
       lower_bound(row_ptr, ceil(p*nnz/P)) then clamped so every part is
-      non-empty.  The row permutation is the identity.
+      non-empty.  The row permutation is the identity.  CONTIG_COST (ours,
+      DESIGN.md §6): CONTIG_NNZ re-balanced on a padded-slots + tail-entries
+      cost under each part's own width.
   A10 recv_p sorted ascending by global column (hence grouped by owner);
       local column of halo entry g = n_loc + rank of g in recv_p; send lists
       are sorted local indices, concatenated over peers in rank order.
@@ -23,7 +25,7 @@ from dataclasses import dataclass, field
 
 import numpy as np
 
-KIND_CONTIG_NNZ, KIND_CONTIG_ROWS, KIND_GRID = 0, 1, 2
+KIND_CONTIG_NNZ, KIND_CONTIG_ROWS, KIND_GRID, KIND_CONTIG_COST = 0, 1, 2, 3
 
 
 def part_ptr_ref(A, n_parts: int, kind: int = KIND_CONTIG_NNZ, grid=None) -> np.ndarray:
@@ -60,6 +62,39 @@ def part_ptr_ref(A, n_parts: int, kind: int = KIND_CONTIG_NNZ, grid=None) -> np.
             r = max(r, pp[p - 1] + 1)
             r = min(r, n - (n_parts - p))
             pp[p] = r
+    elif kind == KIND_CONTIG_COST:
+        # not in the paper: modeled-cost balance.  Start from
+        # CONTIG_NNZ; then (at most 4 times, stopping at a fixed point) give row
+        # i of part p the cost 3 w_p + 4 max(len_i - w_p, 0), w_p = the BG3
+        # width (A1, cap 20) of part p's rows, and cut where the prefix cost
+        # first reaches ceil(p C / P), clamped as for CONTIG_NNZ.
+        from .hec_ref import width_bg3
+        lens = [int(A.row_ptr[i + 1]) - int(A.row_ptr[i]) for i in range(n)]
+        cur = [int(v) for v in part_ptr_ref(A, n_parts, KIND_CONTIG_NNZ)]
+        for _ in range(4):
+            cost = []
+            for p in range(n_parts):
+                w = width_bg3(np.array(lens[cur[p]:cur[p + 1]], dtype=np.int64), 20)
+                for i in range(cur[p], cur[p + 1]):
+                    cost.append(3 * w + 4 * max(lens[i] - w, 0))
+            prefix = [0]
+            for c in cost:
+                prefix.append(prefix[-1] + c)
+            C = prefix[-1]
+            nxt = [0] * (n_parts + 1)
+            nxt[n_parts] = n
+            for p in range(1, n_parts):
+                t = -((-p * C) // n_parts)           # ceil(p*C/P)
+                r = 0
+                while r < n and prefix[r] < t:      # lower_bound(prefix, t)
+                    r += 1
+                r = max(r, nxt[p - 1] + 1)
+                r = min(r, n - (n_parts - p))
+                nxt[p] = r
+            if nxt == cur:
+                break
+            cur = nxt
+        pp = cur
     else:
         raise ValueError("unknown partition kind")
     return np.array(pp, dtype=np.int32)

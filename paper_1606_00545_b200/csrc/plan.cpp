@@ -42,6 +42,47 @@ static hec_status make_part_ptr(const CsrView& A, int32_t P, int32_t kind, const
             r = std::min(r, n - (P - p));
             (*pp)[p] = r;
         }
+    } else if (kind == HEC_PART_CONTIG_COST) {
+        // Modeled-cost balance: row i of part p costs
+        // kCostSlot * w_p + kCostTail * max(len_i - w_p, 0) with w_p the part's
+        // own BG3 width (A1/A12: padded ELL slots + tail entries); start from
+        // CONTIG_NNZ and re-balance kCostIters times (fixed count: deterministic).
+        constexpr int64_t kCostSlot = 3, kCostTail = 4;
+        constexpr int kCostIters = 4;
+        std::vector<int32_t> cur;
+        hec_status st = make_part_ptr(A, P, HEC_PART_CONTIG_NNZ, nullptr, &cur);
+        if (st != HEC_OK) return st;
+        hec_opts o;
+        hec_opts_default(&o);
+        std::vector<int64_t> S((size_t)n + 1);
+        for (int it = 0; it < kCostIters; ++it) {
+            S[0] = 0;
+            for (int32_t p = 0; p < P; ++p) {
+                CsrView v;
+                v.n_rows = cur[p + 1] - cur[p];
+                v.n_cols = A.n_cols;
+                v.row_ptr = A.row_ptr + cur[p];  // lengths only (differences)
+                v.nnz = A.row_ptr[cur[p + 1]] - A.row_ptr[cur[p]];
+                const int64_t w = choose_width(v, o);
+                for (int32_t i = cur[p]; i < cur[p + 1]; ++i) {
+                    const int64_t len = A.row_ptr[i + 1] - A.row_ptr[i];
+                    S[i + 1] = S[i] + kCostSlot * w + kCostTail * std::max<int64_t>(len - w, 0);
+                }
+            }
+            std::vector<int32_t> nxt((size_t)P + 1, 0);
+            nxt[P] = n;
+            const int64_t C = S[n];
+            for (int32_t p = 1; p < P; ++p) {
+                const int64_t t = (p * C + P - 1) / P;  // ceil(p C / P)
+                int32_t r = (int32_t)(std::lower_bound(S.begin(), S.end(), t) - S.begin());
+                r = std::max(r, nxt[p - 1] + 1);
+                r = std::min(r, n - (P - p));
+                nxt[p] = r;
+            }
+            if (nxt == cur) break;
+            cur.swap(nxt);
+        }
+        *pp = cur;
     } else {
         return fail(HEC_ERR_ARG, "unknown partition kind");
     }

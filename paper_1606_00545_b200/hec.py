@@ -28,7 +28,7 @@ class HecError(RuntimeError):
 STATUS = {0: "HEC_OK", 1: "HEC_ERR_ARG", 2: "HEC_ERR_FORMAT", 3: "HEC_ERR_DIM", 4: "HEC_ERR_PARTS",
           5: "HEC_ERR_CUDA", 6: "HEC_ERR_NCCL", 7: "HEC_ERR_NOMEM", 8: "HEC_ERR_STATE", 9: "HEC_ERR_NODEV"}
 WIDTH_BG3, WIDTH_CAP, WIDTH_FIXED = 0, 1, 2
-PART_CONTIG_NNZ, PART_CONTIG_ROWS, PART_GRID = 0, 1, 2
+PART_CONTIG_NNZ, PART_CONTIG_ROWS, PART_GRID, PART_CONTIG_COST = 0, 1, 2, 3
 SUB_INTERIOR, SUB_BOUNDARY, SUB_ALL = 0, 1, 2
 NCCL_ID_BYTES = 128
 IPC_BYTES = 64

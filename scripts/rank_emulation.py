@@ -73,12 +73,16 @@ def main():
     ap.add_argument("configs", nargs="+")
     ap.add_argument("--parts", type=int, nargs="+", default=[1, 2, 4, 8])
     ap.add_argument("--reps", type=int, default=30)
+    ap.add_argument("--kind", choices=["auto", "nnz", "cost"], default="auto",
+                    help="partition of non-grid matrices: CONTIG_NNZ (auto) or CONTIG_COST")
     args = ap.parse_args()
     torch.cuda.set_device(0)
     for cfg in args.configs:
         A = hecgen.CONFIGS[cfg]()
-        kind = hec.PART_GRID if A.grid is not None else hec.PART_CONTIG_NNZ
-        out = {"config": cfg, "n_rows": A.n_rows, "nnz": A.nnz, "partition": "GRID" if A.grid else "CONTIG_NNZ",
+        kind = (hec.PART_GRID if A.grid is not None else
+                hec.PART_CONTIG_COST if args.kind == "cost" else hec.PART_CONTIG_NNZ)
+        kname = {hec.PART_GRID: "GRID", hec.PART_CONTIG_NNZ: "CONTIG_NNZ", hec.PART_CONTIG_COST: "CONTIG_COST"}[kind]
+        out = {"config": cfg, "n_rows": A.n_rows, "nnz": A.nnz, "partition": kname,
                "what": "compute-only projection on one GPU: each part's local HEC timed alone (median of reps, "
                        "L2 flushed when the part is < 4x L2); T_proj = max over parts", "P": {}}
         t1 = None
@@ -105,7 +109,7 @@ def main():
             if t1:
                 rec["E_proj"] = round(t1 / (P * tp), 4)
             out["P"][P] = rec
-            print(f"{cfg} P={P}: T_proj {tp:.4f} ms" + (f", E_proj {rec['E_proj']}" if t1 else ""), file=sys.stderr)
+            print(f"{cfg} [{kname}] P={P}: T_proj {tp:.4f} ms" + (f", E_proj {rec['E_proj']}" if t1 else ""), file=sys.stderr)
         print(json.dumps(out), flush=True)
 
 

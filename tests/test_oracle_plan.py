@@ -168,3 +168,54 @@ def test_local_csr_interior_boundary_split():
         # A12: width from all 256 local rows (halo columns count); 6x6x3 = 108 of
         # them have 7 entries and 3*108 >= 256, so w_p = 7 (BG3 closed form).
         assert PR.part_width(part, hecgen.Csr) == 7
+
+
+# ---------------------------------------------------------------- CONTIG_COST
+# Not in the paper: the partition is a heuristic, so it is
+# pinned by the properties that define it rather than by values.
+def _cost_prefix(A, pp):
+    from oracle.hec_ref import width_bg3
+    lens = np.diff(np.asarray(A.row_ptr, dtype=np.int64))
+    cost = np.zeros(A.n_rows, dtype=np.int64)
+    for p in range(len(pp) - 1):
+        w = width_bg3(lens[pp[p]:pp[p + 1]], 20)
+        seg = lens[pp[p]:pp[p + 1]]
+        cost[pp[p]:pp[p + 1]] = 3 * w + 4 * np.maximum(seg - w, 0)
+    return np.concatenate([[0], np.cumsum(cost)])
+
+
+@pytest.mark.parametrize("maker,P", [(lambda: hecgen.powerlaw(3000, seed=2), 4),
+                                     (lambda: hecgen.degree_sorted(hecgen.powerlaw(3000, seed=3)), 8),
+                                     (lambda: hecgen.spe10(10, 12, 6, seed=1), 3)])
+def test_contig_cost_is_a_balanced_fixed_point_or_capped(maker, P):
+    A = maker()
+    pp = PR.part_ptr_ref(A, P, PR.KIND_CONTIG_COST)
+    assert pp[0] == 0 and pp[-1] == A.n_rows and np.all(np.diff(pp) >= 1)
+    S = _cost_prefix(A, pp)
+    C = int(S[-1])
+    # where the iteration reached its fixed point, every cut is the first row
+    # whose prefix cost reaches ceil(p C / P) under the parts' own widths
+    fixed = all(pp[p] == max(pp[p - 1] + 1, min(int(np.searchsorted(S, -((-p * C) // P))), A.n_rows - (P - p)))
+                for p in range(1, P))
+    if fixed:
+        for p in range(1, P):
+            t = -((-p * C) // P)
+            assert S[pp[p]] >= t or pp[p] == A.n_rows - (P - p)
+            assert S[pp[p] - 1] < t or pp[p] == pp[p - 1] + 1
+
+
+def test_contig_cost_uniform_rows_equals_contig_rows():
+    # equal row lengths: every row costs the same, so the cuts are floor-free
+    # equal splits (P | n), identical to CONTIG_ROWS
+    B = hecgen.from_rows(48, [[(j, 1.0) for j in range(i % 4, i % 4 + 5)] for i in range(48)])
+    for P in (2, 3, 4, 6, 8):
+        assert PR.part_ptr_ref(B, P, PR.KIND_CONTIG_COST).tolist() == PR.part_ptr_ref(B, P, PR.KIND_CONTIG_ROWS).tolist()
+
+
+def test_contig_cost_reduces_the_modeled_maximum_on_degree_sorted():
+    A = hecgen.degree_sorted(hecgen.powerlaw(4000, seed=6))
+    for P in (4, 8):
+        def max_part(pp):
+            S = _cost_prefix(A, pp)
+            return max(int(S[pp[p + 1]] - S[pp[p]]) for p in range(P))
+        assert max_part(PR.part_ptr_ref(A, P, PR.KIND_CONTIG_COST)) < max_part(PR.part_ptr_ref(A, P, PR.KIND_CONTIG_NNZ))

@@ -54,6 +54,20 @@ def test_powerlaw_parts(P, kind):
     check_plan(hecgen.powerlaw(600, seed=P), P, kind)
 
 
+@pytest.mark.parametrize("P", [2, 3, 8])
+def test_contig_cost_parts(P):
+    check_plan(hecgen.powerlaw(600, seed=P), P, hec.PART_CONTIG_COST)
+
+
+@pytest.mark.parametrize("P", [4, 8])
+def test_contig_cost_degree_sorted(P):
+    check_plan(hecgen.degree_sorted(hecgen.powerlaw(2000, seed=5)), P, hec.PART_CONTIG_COST, check_sub=False)
+
+
+def test_contig_cost_p_equals_n():
+    check_plan(hecgen.random_csr(12, 12, 0.3, seed=4), 12, hec.PART_CONTIG_COST)
+
+
 def test_policies_and_units():
     A = hecgen.powerlaw(300, seed=4)
     for args in [(1, 20, 0, 32), (0, 5, 0, 256), (2, 0, 3, 64), (1, 0, 0, 256)]:
