@@ -58,6 +58,17 @@ def test_local_powerlaw_contig_nnz(P):
     assert run_local(B, xi, P, hec.PART_CONTIG_NNZ).tobytes() == oracle.csr_spmv(B, xi).tobytes()
 
 
+@pytest.mark.parametrize("P", [4, 8])
+def test_local_degree_sorted_contig_cost(P):
+    # the §8(d) stress variant under the cost-balanced partition
+    A = hecgen.degree_sorted(hecgen.powerlaw(1 << 15, seed=P))
+    x = hecgen.vector(A.n_cols, "uniform", seed=P)
+    assert_parity(A, x, run_local(A, x, P, hec.PART_CONTIG_COST))
+    B = hecgen.degree_sorted(hecgen.powerlaw(1 << 14, integer_values=True, seed=P))
+    xi = hecgen.vector(B.n_cols, "int", seed=P)
+    assert run_local(B, xi, P, hec.PART_CONTIG_COST).tobytes() == oracle.csr_spmv(B, xi).tobytes()
+
+
 def test_local_spe10_and_every_row_its_own_part():
     A = hecgen.spe10(20, 30, 10, seed=3)
     x = hecgen.vector(A.n_cols, "uniform", seed=3)
