@@ -532,10 +532,26 @@ static bool tail_pdl() {
     return v == 1;
 }
 
+// ELL CTA size: 128 threads for single-phase widths (w <= HEC_ELL_PHASE), 256
+// for the two-phase ones (measured, profiles/round1/ell_block/: 256^3 0.2467 ->
+// 0.2448 ms, 128^3 0.0349 -> 0.0346, SPE10 0.0223 -> 0.0219 with 128; power-law
+// w = 9 0.503 -> 0.519 ms with 128, so it keeps 256).  HEC_ELL_BLOCK (tuning)
+// forces 64/128/192/256 for every width.
+static int ell_block(int32_t width) {
+    static int forced = -1;
+    if (forced < 0) {
+        const char* e = std::getenv("HEC_ELL_BLOCK");
+        const int b = e ? std::atoi(e) : 0;
+        forced = (b == 64 || b == 128 || b == 192 || b == 256) ? b : 0;
+    }
+    if (forced) return forced;
+    return (width > 0 && width <= HEC_ELL_PHASE) ? 128 : 256;
+}
+
 template <bool HALO, bool ROWMAP, int EPI>
 static cudaError_t launch_ell_t(const EllArgs& a, cudaStream_t s) {
     const int64_t n_pairs = ((int64_t)a.n_rows + 1) >> 1;
-    const int threads = 256;
+    const int threads = ell_block(a.width);
     int64_t blocks = (n_pairs + threads - 1) / threads;
     // one row pair per thread, grid-stride only beyond 64 full waves (a
     // persistent grid of 5-40 blocks/SM was measured slower, r15; forcing
