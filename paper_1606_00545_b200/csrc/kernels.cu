@@ -602,23 +602,7 @@ cudaError_t launch_ell(const EllArgs& a, cudaStream_t s) {
     return rowmap ? launch_ell_t<false, true, EPI_NONE>(a, s) : launch_ell_t<false, false, EPI_NONE>(a, s);
 }
 
-// HEC_TAIL_CARVEOUT (tuning): the tail kernels' preferred shared-memory
-// carveout in percent (0 = as much L1 as possible for the x gathers)
-static void tail_carveout() {
-    static bool done = false;
-    if (done) return;
-    done = true;
-    const char* e = std::getenv("HEC_TAIL_CARVEOUT");
-    if (!e) return;
-    const int pct = std::atoi(e);
-    cudaFuncSetAttribute(tail_kernel<false, false>, cudaFuncAttributePreferredSharedMemoryCarveout, pct);
-    cudaFuncSetAttribute(tail_kernel<true, false>, cudaFuncAttributePreferredSharedMemoryCarveout, pct);
-    cudaFuncSetAttribute(tail_kernel<false, true>, cudaFuncAttributePreferredSharedMemoryCarveout, pct);
-    cudaGetLastError();
-}
-
 cudaError_t launch_tail(const TailArgs& a, cudaStream_t s) {
-    tail_carveout();
     const int64_t blocks = a.blk_end - a.blk_begin;
     if (blocks <= 0) return cudaSuccess;
     if (blocks > 0x7fffffff) return cudaErrorInvalidValue;
