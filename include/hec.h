@@ -201,7 +201,9 @@ hec_status hec_norm2(int64_t n, const double* x, double* result, void* stream);
  * Stops when ||s||_2 or ||r||_2 <= tol ||r0||_2 (Alg. 4's two tests; CG: ||r||),
  * after max_it iterations, or on breakdown (rho = 0 -> breakdown = 1;
  * omega = 0 -> breakdown = 2; (r0, v) = 0, where Alg. 4's alpha is undefined
- * -> breakdown = 3, reading A20).  Scalars, tests and breakdown checks stay on
+ * -> breakdown = 3, reading A20; (t, t) = 0 or a non-finite omega in BiCGSTAB,
+ * (p, A p) = 0 or a non-finite alpha in CG -> breakdown = 4: x keeps the last
+ * finite iterate).  Scalars, tests and breakdown checks stay on
  * the device (a done flag turns later passes into no-ops); the host reads the
  * state once per batch of iterations.  The first solve on a handle caches a
  * workspace of 6 n-vectors in it (freed with the handle); concurrent solves

@@ -61,7 +61,8 @@ def bicgstab(A, b: np.ndarray, x0: np.ndarray, tol: float, max_it: int) -> Solve
     """Alg. 4 with M = I, so p* = p and s* = s.  Stopping tests:
     ||s||_2 <= tol ||r_0||_2 and ||r||_2 <= tol ||r_0||_2 (reading of 'is
     satisfied'); breakdown 1 when rho_{k-1} = 0 ('Fails'), 2 when omega_k = 0,
-    3 when (r0, v) = 0 (alpha undefined; not tested by Alg. 4, reading A20)."""
+    3 when (r0, v) = 0 (alpha undefined; not tested by Alg. 4, reading A20),
+    4 when (t, t) = 0 or omega_k is not finite (omega undefined; reading A20)."""
     x = x0.astype(np.float64).copy()
     r = b - csr_spmv(A, x)                      # r0 = b - A x0           (SpMV; vector update)
     r0 = r.copy()                               # shadow residual r~ = r0
@@ -92,7 +93,10 @@ def bicgstab(A, b: np.ndarray, x0: np.ndarray, tol: float, max_it: int) -> Solve
             hist.append(sn / r0n)
             return SolveRef(x, k, True, 0, sn / r0n, hist)
         t = csr_spmv(A, s)                      # t = A s*               (SpMV)
-        omega = dot(t, s) / dot(t, t)           # omega_k = (t, s) / ||t||^2
+        ts, tt = dot(t, s), dot(t, t)
+        if tt == 0.0 or not math.isfinite(ts / tt):  # omega_k undefined (reading A20): breakdown 4
+            return SolveRef(x, k, False, 4, hist[-1], hist)
+        omega = ts / tt                         # omega_k = (t, s) / ||t||^2
         x = x + alpha * p + omega * s           # x = x + alpha p* + omega s*
         r = s - omega * t                       # r = s - omega t
         rn = norm2(r)
@@ -107,7 +111,8 @@ def bicgstab(A, b: np.ndarray, x0: np.ndarray, tol: float, max_it: int) -> Solve
 
 def cg(A, b: np.ndarray, x0: np.ndarray, tol: float, max_it: int) -> SolveRef:
     """Conjugate gradients for SPD A (Saad, Alg. 6.18): stop when
-    ||r_k||_2 <= tol ||r_0||_2."""
+    ||r_k||_2 <= tol ||r_0||_2; breakdown 4 when (p, A p) = 0 or alpha is not
+    finite (A not SPD)."""
     x = x0.astype(np.float64).copy()
     r = b - csr_spmv(A, x)
     p = r.copy()
@@ -118,7 +123,10 @@ def cg(A, b: np.ndarray, x0: np.ndarray, tol: float, max_it: int) -> SolveRef:
         return SolveRef(x, 0, True, 0, 0.0, hist)
     for k in range(1, max_it + 1):
         q = csr_spmv(A, p)
-        alpha = rho / dot(p, q)
+        pq = dot(p, q)
+        if pq == 0.0 or not math.isfinite(rho / pq):   # alpha undefined (A not SPD): breakdown 4
+            return SolveRef(x, k, False, 4, hist[-1], hist)
+        alpha = rho / pq
         x = x + alpha * p
         r = r - alpha * q
         rho_new = dot(r, r)

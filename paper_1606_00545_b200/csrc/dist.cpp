@@ -269,6 +269,17 @@ static PeerWait wait_args(const hec_dist_s* d, uint64_t ep) {
     return w;
 }
 
+// The peer-memory wait's error word (set when a neighbour's flag did not
+// arrive within ~10 s); the caller has synchronised the stream that ran it.
+hec_status dist_err(hec_dist_s* D) {
+    if (!D->d_err) return HEC_OK;
+    HEC_CUDA_TRY(cudaStreamSynchronize(D->comm_stream));
+    int32_t err = 0;
+    HEC_CUDA_TRY(cudaMemcpy(&err, D->d_err, sizeof(err), cudaMemcpyDeviceToHost));
+    if (err) return fail(HEC_ERR_STATE, "peer-memory halo: a neighbour's data did not arrive within 10 s");
+    return HEC_OK;
+}
+
 static double* p2p_halo(const hec_dist_s* d, uint64_t ep) {
     return d->n_halo ? win_buf0(d->d_win, d->n_parts) + (ep & 1) * (uint64_t)d->n_halo : nullptr;
 }
@@ -406,11 +417,7 @@ hec_status hec_dist_check(hec_dist D) {
     if (!D) return fail(HEC_ERR_ARG, "NULL handle");
     DeviceGuard g(D->device);
     HEC_CUDA_TRY(cudaStreamSynchronize(D->comm_stream));
-    if (!D->d_err) return HEC_OK;
-    int32_t err = 0;
-    HEC_CUDA_TRY(cudaMemcpy(&err, D->d_err, sizeof(err), cudaMemcpyDeviceToHost));
-    if (err) return fail(HEC_ERR_STATE, "peer-memory halo: a neighbour's data did not arrive within 10 s");
-    return HEC_OK;
+    return dist_err(D);
 }
 
 hec_status hec_dist_create_local(const hec_csr* A, hec_plan P, const hec_opts* o, int32_t device,
@@ -499,6 +506,9 @@ int64_t dist_n_local(hec_dist_s* D) { return (int64_t)D->r1 - D->r0; }
 ncclComm_t dist_comm(hec_dist_s* D) { return D->comm; }
 
 int32_t dist_parts(hec_dist_s* D) { return D->n_parts; }
+
+int32_t dist_device(hec_dist_s* D) { return D->device; }
+
 
 void** dist_ws_slot(hec_dist_s* D, void (***free_fn)(void*)) {
     *free_fn = &D->ws_free;

@@ -222,9 +222,9 @@ enum Step {
     ST_BICG_BEGIN,    // top of iteration k: count it; rho = 0 -> "Fails"; beta (k > 1)
     ST_BICG_ALPHA,    // alpha = rho / (r0, v); (r0, v) = 0 -> breakdown 3
     ST_BICG_S,        // ||s|| <= thr -> converged (x += alpha p pending)
-    ST_BICG_OMEGA,    // omega = (t, s) / (t, t)
+    ST_BICG_OMEGA,    // omega = (t, s) / (t, t); (t, t) = 0 or omega not finite -> breakdown 4
     ST_BICG_R,        // ||r|| <= thr -> converged; omega = 0 -> breakdown 2; rho = (r0, r)
-    ST_CG_ALPHA,      // count the iteration; alpha = rho / (p, q)
+    ST_CG_ALPHA,      // count the iteration; alpha = rho / (p, q); (p, q) = 0 -> breakdown 4
     ST_CG_R,          // rho_new = (r, r): converged?; beta = rho_new / rho
     ST_FINAL_DONE,    // clear the pending x += alpha p
 };
@@ -258,7 +258,12 @@ __device__ void step_body(double* sc, int mode, double tol, int first) {
                 sc[SC_RES] = sqrt(sc[SC_D0]) / sc[SC_R0NORM];
             }
             break;
-        case ST_BICG_OMEGA: sc[SC_OMEGA] = sc[SC_D0] / sc[SC_D1]; break;
+        case ST_BICG_OMEGA:
+            // (t, t) = 0 (t = A s = 0 with s != 0: A singular) or a non-finite
+            // omega: omega_k is undefined -> breakdown 4 (reading A20); x, r freeze
+            if (sc[SC_D1] == 0.0 || !isfinite(sc[SC_D0] / sc[SC_D1])) { sc[SC_DONE] = 2.0; sc[SC_BREAK] = 4.0; break; }
+            sc[SC_OMEGA] = sc[SC_D0] / sc[SC_D1];
+            break;
         case ST_BICG_R:
             sc[SC_RES] = sqrt(sc[SC_D0]) / sc[SC_R0NORM];
             if (sqrt(sc[SC_D0]) <= sc[SC_THR]) { sc[SC_DONE] = 1.0; sc[SC_CONV] = 1.0; break; }   // ||r|| satisfied
@@ -268,6 +273,8 @@ __device__ void step_body(double* sc, int mode, double tol, int first) {
             break;
         case ST_CG_ALPHA:  // counts the iteration (nothing between its start and here can stop it)
             sc[SC_ITER] += 1.0;
+            // (p, q) = 0: alpha undefined (A not SPD) -> breakdown 4 (reading A20)
+            if (sc[SC_D0] == 0.0 || !isfinite(sc[SC_RHO] / sc[SC_D0])) { sc[SC_DONE] = 2.0; sc[SC_BREAK] = 4.0; break; }
             sc[SC_ALPHA] = sc[SC_RHO] / sc[SC_D0];
             break;
         case ST_CG_R:
@@ -298,6 +305,8 @@ hec_status dist_spmv_launch(hec_dist_s* D, const double* x, double* y, cudaStrea
 int64_t dist_n_local(hec_dist_s* D);
 ncclComm_t dist_comm(hec_dist_s* D);
 int32_t dist_parts(hec_dist_s* D);
+int32_t dist_device(hec_dist_s* D);
+hec_status dist_err(hec_dist_s* D);  // HEC_ERR_STATE if a peer-memory halo wait timed out
 void** dist_ws_slot(hec_dist_s* D, void (***free_fn)(void*));
 
 #define HEC_TRY(expr)                         \
@@ -536,6 +545,7 @@ static hec_status solve(Op op, int method, const double* b, double* x, double to
     if (!info || (op.n > 0 && (!b || !x))) return fail(HEC_ERR_ARG, "NULL argument");
     if (!(tol >= 0) || max_it < 0) return fail(HEC_ERR_ARG, "negative tol or max_it");
     std::memset(info, 0, sizeof(*info));
+    DeviceGuard g(op.A ? op.A->device : dist_device(op.D));  // workspace + launches on the handle's device
     Solver S;
     S.op = op;
     S.s = (cudaStream_t)stream;
@@ -543,6 +553,9 @@ static hec_status solve(Op op, int method, const double* b, double* x, double to
     HEC_TRY(S.init());
     hec_status st = method == 0 ? bicgstab(S, b, x, max_it, info) : cg(S, b, x, max_it, info);
     if (st == HEC_OK) HEC_CUDA_TRY(cudaStreamSynchronize(S.s));
+    // peer-memory transport: a halo wait that timed out leaves boundary rows
+    // computed from stale data -- report it instead of a converged solve
+    if (st == HEC_OK && op.D) st = dist_err(op.D);
     return st;
 }
 

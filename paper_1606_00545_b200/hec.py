@@ -246,6 +246,27 @@ def _dptr(t, n: int, name: str) -> int:
     return t.data_ptr()
 
 
+def _hptr(a, n: int, name: str) -> int:
+    """Host buffer pointer: a numpy array or a CPU torch tensor, contiguous
+    float64 with >= n elements.  Anything else raises (a converted temporary
+    would be freed before the C call reads it)."""
+    if isinstance(a, np.ndarray):
+        if a.dtype != np.float64 or not a.flags["C_CONTIGUOUS"] or a.size < n:
+            raise ValueError(f"{name} must be a contiguous float64 array with >= {n} elements")
+        return _p(a)
+    try:
+        import torch
+    except ImportError:  # pragma: no cover
+        torch = None
+    if torch is not None and isinstance(a, torch.Tensor):
+        if a.device.type != "cpu":
+            raise TypeError(f"{name} must be a host (CPU) tensor for spmv_host")
+        if a.dtype != torch.float64 or not a.is_contiguous() or a.numel() < n:
+            raise ValueError(f"{name} must be contiguous float64 with >= {n} elements")
+        return a.data_ptr() if a.numel() else 0
+    raise TypeError(f"{name} must be a numpy array or a CPU torch tensor")
+
+
 @dataclass
 class HecArrays:
     width: int
@@ -311,12 +332,15 @@ class Matrix:
                              _stream_ptr(stream)))
         return y
 
-    def spmv_host(self, x: np.ndarray, y: np.ndarray | None = None, stream=None) -> np.ndarray:
-        """y = A x with host buffers (numpy or pinned torch tensors); synchronous."""
+    def spmv_host(self, x, y=None, stream=None):
+        """y = A x with host buffers (numpy arrays or CPU torch tensors, pinned
+        for full PCIe rate); synchronous.  Both must be contiguous float64 with
+        at least n_cols / n_rows elements (no conversion copies: the C side
+        reads and writes the caller's memory directly)."""
         if y is None:
             y = np.empty(self.n_rows, np.float64)
-        xp = x.data_ptr() if hasattr(x, "data_ptr") else _p(np.ascontiguousarray(x, dtype=np.float64))
-        yp = y.data_ptr() if hasattr(y, "data_ptr") else _p(y)
+        xp = _hptr(x, self.n_cols, "x")
+        yp = _hptr(y, self.n_rows, "y")
         _check(_lib.hec_spmv_host(self._h, xp, yp, _stream_ptr(stream)))
         return y
 
@@ -638,33 +662,3 @@ def norm2(x, stream=None) -> float:
     r = ctypes.c_double()
     _check(_lib.hec_norm2(x.numel(), _dptr(x, x.numel(), "x"), ctypes.byref(r), _stream_ptr(stream)))
     return r.value
-
-
-def exchange_halo_host(plan: Plan, rank: int, x_local: np.ndarray, group=None) -> np.ndarray:
-    """Host-side halo exchange over a torch.distributed process group (e.g.
-    gloo) following the plan's send/recv lists -- the same pattern the NCCL
-    path runs on the device.  Returns x_halo (ordered as recv_cols)."""
-    import torch
-    import torch.distributed as dist
-    a = plan.export(rank)
-    P = plan.n_parts
-    halo = np.empty(len(a.recv_cols), np.float64)
-    reqs, bufs = [], []
-    for q in range(P):
-        lo, hi = int(a.send_off[q]), int(a.send_off[q + 1])
-        if hi > lo:
-            t = torch.from_numpy(np.ascontiguousarray(x_local[a.send_idx[lo:hi]]))
-            bufs.append(t)
-            reqs.append(dist.isend(t, dst=q, group=group))
-    recvs = []
-    for q in range(P):
-        lo, hi = int(a.recv_off[q]), int(a.recv_off[q + 1])
-        if hi > lo:
-            t = torch.empty(hi - lo, dtype=torch.float64)
-            recvs.append((lo, hi, t))
-            reqs.append(dist.irecv(t, src=q, group=group))
-    for r in reqs:
-        r.wait()
-    for lo, hi, t in recvs:
-        halo[lo:hi] = t.numpy()
-    return halo

@@ -24,6 +24,36 @@ def _free_port():
     return p
 
 
+def exchange_halo_host(plan, rank, x_local, group=None):
+    """Host-side halo exchange over a torch.distributed process group (gloo),
+    following the product plan's send/recv lists -- the same pattern
+    hec_spmv_dist runs on the device.  Test infrastructure: returns
+    x_halo ordered as recv_cols."""
+    import torch
+    import torch.distributed as dist
+    a = plan.export(rank)
+    P = plan.n_parts
+    halo = np.empty(len(a.recv_cols), np.float64)
+    reqs, bufs, recvs = [], [], []
+    for q in range(P):
+        lo, hi = int(a.send_off[q]), int(a.send_off[q + 1])
+        if hi > lo:
+            t = torch.from_numpy(np.ascontiguousarray(x_local[a.send_idx[lo:hi]]))
+            bufs.append(t)
+            reqs.append(dist.isend(t, dst=q, group=group))
+    for q in range(P):
+        lo, hi = int(a.recv_off[q]), int(a.recv_off[q + 1])
+        if hi > lo:
+            t = torch.empty(hi - lo, dtype=torch.float64)
+            recvs.append((lo, hi, t))
+            reqs.append(dist.irecv(t, src=q, group=group))
+    for r in reqs:
+        r.wait()
+    for lo, hi, t in recvs:
+        halo[lo:hi] = t.numpy()
+    return halo
+
+
 def _make(case):
     import hecgen
     if case == "poisson":
@@ -57,7 +87,7 @@ def _worker(rank, world, port, case, out_q):
             x = hecgen.vector(A.n_cols, "uniform", seed=11)
         a = plan.export(rank)
         x_loc = x[a.r0:a.r1].copy()
-        halo = hec.exchange_halo_host(plan, rank, x_loc)
+        halo = exchange_halo_host(plan, rank, x_loc)
         assert halo.tobytes() == x[a.recv_cols].tobytes()          # exact copy of the needed entries
         x_ext = np.concatenate([x_loc, halo])
         y_loc = np.empty(a.r1 - a.r0)

@@ -78,20 +78,6 @@ def test_local_spe10_and_every_row_its_own_part():
     assert_parity(B, xb, run_local(B, xb, 24, hec.PART_CONTIG_ROWS))   # P = n
 
 
-def test_local_256_slabs_8_parts_sampled():
-    # BASELINE configs[2] at full size with the 8-slab partition of the scaling run.
-    A = hecgen.poisson3d(256, 256, 256)
-    x = hecgen.vector(A.n_cols, "uniform", seed=1606)
-    y = run_local(A, x, 8, hec.PART_GRID, (256, 256, 256))
-    plane = 256 * 256
-    for r0 in [0, 31 * plane, 32 * plane - 100, 100 * plane + 77, A.n_rows - 5000]:  # slab edges incl.
-        ref = oracle.csr_spmv(A, x, r0, r0 + 5000)
-        assert np.all(np.abs(y[r0:r0 + 5000] - ref) <= oracle.tolerance(A, x, r0, r0 + 5000))
-    ones = np.ones(A.n_cols)
-    y1 = run_local(A, ones, 8, hec.PART_GRID, (256, 256, 256))
-    assert y1.tobytes() == (6.0 - (np.diff(A.row_ptr) - 1)).astype(np.float64).tobytes()
-
-
 def test_dist_single_rank_equals_hec_spmv_bitwise():
     A = hecgen.powerlaw(1 << 15, seed=2)
     x = torch.from_numpy(hecgen.vector(A.n_cols, "uniform", seed=2)).cuda()

@@ -135,16 +135,17 @@ def test_bicgstab_matches_oracle(maker, tol):
         assert info.iterations == k
         assert abs(info.rel_residual - traj[k]) <= rel * traj[k], (k, info.rel_residual, traj[k])
     # (2) Converged solve: same outcome, a true residual within the tolerance
-    # and the oracle's solution.  The iteration count itself is rounding-
-    # chaotic past that point: the oracle over 12 random admissible summation
-    # orders of its dots and rows spans 173-185 on the power-law matrix (170
-    # in column order); the GPU takes 197 with the multi-warp tail rows and
-    # 180 with single-warp rows (HEC_TAIL_MAXLG=5).  Only a stall or a
-    # premature stop is an error: the count must lie within 1.5x either way.
+    # and the oracle's solution.  What A5 justifies stops at (1): past ~k = 40
+    # on the power-law matrix the trajectory is rounding-chaotic (any valid
+    # summation order is a different, equally correct run), so the iteration
+    # count there is NOT pinned.  On the well-conditioned Poisson matrix the
+    # gap stays small and the count is pinned to +-1.  A stall fails
+    # `converged`; a premature stop fails the true-residual bound.
     xd = torch.zeros(A.n_rows, dtype=torch.float64, device="cuda")
     info = M.bicgstab(dev(b), xd, tol, 2000)
     assert info.converged == ref.converged and info.breakdown == ref.breakdown == 0
-    assert ref.iterations / 1.5 <= info.iterations <= 1.5 * ref.iterations, (info.iterations, ref.iterations)
+    if A.grid is not None:
+        assert abs(info.iterations - ref.iterations) <= 1, (info.iterations, ref.iterations)
     x = xd.cpu().numpy()
     rel_true = np.linalg.norm(b - oracle.csr_spmv(A, x)) / np.linalg.norm(b)
     assert rel_true <= 5 * tol
@@ -162,6 +163,21 @@ def test_bicgstab_identity_one_step_and_breakdown():
     xd = torch.zeros(2, dtype=torch.float64, device="cuda")
     info = hec.from_csr(R).bicgstab(dev(np.array([1.0, 0.0])), xd, 1e-14, 10)
     assert (info.breakdown, info.iterations, info.converged) == (3, 1, 0)
+
+
+def test_breakdown_4_omega_and_cg_alpha_undefined():
+    # the oracle's pinned examples (tests/test_oracle_krylov.py): (t, t) = 0 in
+    # BiCGSTAB and (p, A p) = 0 in CG -> breakdown 4 at k = 1, x untouched
+    A = hecgen.from_dense(np.array([[1.0, -1.0], [0.0, 0.0]]))
+    xd = torch.zeros(2, dtype=torch.float64, device="cuda")
+    info = hec.from_csr(A).bicgstab(dev(np.array([0.5, -0.5])), xd, 1e-14, 10)
+    assert (info.breakdown, info.iterations, info.converged) == (4, 1, 0)
+    assert xd.cpu().numpy().tolist() == [0.0, 0.0]
+    B = hecgen.from_dense(np.array([[0.0, 1.0], [1.0, 0.0]]))
+    xd = torch.zeros(2, dtype=torch.float64, device="cuda")
+    info = hec.from_csr(B).cg(dev(np.array([1.0, 0.0])), xd, 1e-14, 10)
+    assert (info.breakdown, info.iterations, info.converged) == (4, 1, 0)
+    assert xd.cpu().numpy().tolist() == [0.0, 0.0]
 
 
 def test_dist_solvers_single_rank_equal_single_gpu_bitwise():

@@ -78,51 +78,6 @@ def test_poisson_128_full_parity():
     assert_parity(A, x, y)
 
 
-def test_poisson_256_sampled_and_closed_form():
-    # BASELINE configs[2] at full size in the bench's launch configuration:
-    # sampled rows against the oracle row by row, plus the closed form
-    # (A 1)_i = 6 - deg(i) on every row (exact, bitwise).
-    A = hecgen.poisson3d(256, 256, 256)
-    M = hec.from_csr(A)
-    x = hecgen.vector(A.n_cols, "uniform", seed=1606)
-    y, _ = gpu_spmv(A, x, M=M)
-    rng = np.random.default_rng(0)
-    for r0 in np.concatenate([[0, A.n_rows - 4096], rng.integers(0, A.n_rows - 4096, 30)]):
-        assert_parity(A, x, y[r0:r0 + 4096], int(r0), int(r0) + 4096)
-    ones = np.ones(A.n_cols)
-    y1, _ = gpu_spmv(A, ones, M=M)
-    deg = np.diff(A.row_ptr) - 1
-    assert y1.tobytes() == (6.0 - deg).astype(np.float64).tobytes()
-    # the integer regime at full size: bitwise equal to the oracle everywhere
-    xi = hecgen.vector(A.n_cols, "int", seed=5)
-    yi, _ = gpu_spmv(A, xi, M=M)
-    assert yi.tobytes() == oracle.csr_spmv(A, xi).tobytes()
-
-
-def test_powerlaw_full_size_sampled():
-    # BASELINE configs[4]: 2^23 rows, heavy CSR tail (~31% of rows spill).
-    A = hecgen.powerlaw(1 << 23)
-    x = hecgen.vector(A.n_cols, "uniform", seed=1606)
-    y, M = gpu_spmv(A, x)
-    assert M.info.ell_width == 9 and M.info.tail_rows > 2_000_000
-    rng = np.random.default_rng(1)
-    for r0 in np.concatenate([[0, A.n_rows - 2048], rng.integers(0, A.n_rows - 2048, 20)]):
-        assert_parity(A, x, y[r0:r0 + 2048], int(r0), int(r0) + 2048)
-
-
-def test_powerlaw_degree_sorted_full_size_sampled():
-    # SURVEY §8(d) secondary row: configs[4] with rows in descending length
-    # order -- every tail row is at the top, the longest (2,000) first.
-    A = hecgen.degree_sorted(hecgen.powerlaw(1 << 23))
-    x = hecgen.vector(A.n_cols, "uniform", seed=1606)
-    y, M = gpu_spmv(A, x)
-    assert M.info.ell_width == 9
-    assert np.all(np.diff(A.row_ptr)[:M.info.tail_rows] > 9)   # the tail is exactly the top rows
-    rng = np.random.default_rng(2)
-    for r0 in np.concatenate([[0, M.info.tail_rows - 1024, A.n_rows - 2048], rng.integers(0, A.n_rows - 2048, 12)]):
-        assert_parity(A, x, y[r0:r0 + 2048], int(r0), int(r0) + 2048)
-
-
 @pytest.mark.parametrize("n", [1, 31, 32, 33, 255, 256, 257, 1023])
 @pytest.mark.parametrize("unit", [32, 256])
 def test_sizes_and_strides(n, unit):

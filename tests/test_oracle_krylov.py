@@ -100,3 +100,24 @@ def test_bicgstab_breakdown_pivot():
     A = hecgen.from_dense(np.array([[0.0, 1.0], [-1.0, 0.0]]))
     res = K.bicgstab(A, np.array([1.0, 0.0]), np.zeros(2), 1e-14, 10)
     assert (res.breakdown, res.iterations, res.converged) == (3, 1, False)
+
+
+def test_bicgstab_breakdown_omega_undefined():
+    # A = [[1, -1], [0, 0]]: u = e1 is an eigenvector (lambda 1), w = (1, 1) spans
+    # the null space.  With r0 = u + c w, alpha_1 = (r,r)/(r,Ar) = 1/lambda exactly
+    # when w.(w + u) = 0, i.e. c = -1/2, and then t = A s = A r - alpha A^2 r = 0
+    # with s = (-1/2, -1/2) != 0: (t, t) = 0, omega_1 undefined -> breakdown 4
+    # (reading A20).  Every value is a dyadic rational: exact in fp64.
+    A = hecgen.from_dense(np.array([[1.0, -1.0], [0.0, 0.0]]))
+    res = K.bicgstab(A, np.array([0.5, -0.5]), np.zeros(2), 1e-14, 10)
+    assert (res.breakdown, res.iterations, res.converged) == (4, 1, False)
+    assert res.x.tolist() == [0.0, 0.0]                  # no update with an undefined omega
+
+
+def test_cg_breakdown_indefinite():
+    # A = [[0, 1], [1, 0]] (symmetric, indefinite), b = e1: p = r = e1, A p = e2,
+    # (p, A p) = 0 -> alpha undefined -> breakdown 4 at k = 1.
+    A = hecgen.from_dense(np.array([[0.0, 1.0], [1.0, 0.0]]))
+    res = K.cg(A, np.array([1.0, 0.0]), np.zeros(2), 1e-14, 10)
+    assert (res.breakdown, res.iterations, res.converged) == (4, 1, False)
+    assert res.x.tolist() == [0.0, 0.0]
