@@ -59,13 +59,32 @@ def parse():
                     help="NEXT-3: time damped-Jacobi sweeps (hec_jacobi) with this omega")
     ap.add_argument("--ell-width", type=int, default=None,
                     help="experiment: FIXED ELL width instead of the BG3 rule (reading A1)")
-    ap.add_argument("--transport", choices=["p2p", "nccl"], default="p2p",
-                    help="N > 1 halo exchange: peer-memory push kernel over NVLink (default) or NCCL send/recv")
+    ap.add_argument("--transport", choices=["p2p", "nccl", "both"], default="p2p",
+                    help="N > 1 halo exchange: peer-memory push kernel over NVLink (default), NCCL send/recv, "
+                         "or both timed in one run (NCCL first, then the same handle switched to p2p)")
+    ap.add_argument("--no-ncu", action="store_true",
+                    help="skip the in-run ncu pass that measures roofline.traffic (dram bytes per launch)")
+    ap.add_argument("--no-anchor", action="store_true",
+                    help="skip the paper-anchor leg (150^3 GPU / serial speedup beside Table 3's 13.63x)")
     ap.add_argument("--partition", choices=["auto", "nnz", "cost"], default="auto",
                     help="N > 1, non-grid matrices: CONTIG_NNZ (auto, reading A9) or CONTIG_COST (DESIGN §6)")
     ap.add_argument("--dist", action="store_true",
                     help="use the distributed path (hec_spmv_dist under torchrun) even with one GPU")
     return ap.parse_args()
+
+
+def workload_config(name, A, x_h, world: int = 1):
+    """The line's `config`: the workload's identity only (same keys and values
+    on the product arm and the reference arm), with the FNV-1a checksums of
+    the CSR arrays and x, and the GPU arm's L2 policy (flush iff a rank's
+    inputs are < 4x L2).  Run details go under the line's `run` key."""
+    alg = algorithmic_bytes(A.nnz, A.n_rows, A.n_cols) // max(1, world)
+    l2 = (f"inputs {alg / 1e9:.2f} GB per GPU > 4x the {L2_BYTES / 2**20:.0f} MiB L2: no flush between steps"
+          if alg >= 4 * L2_BYTES else
+          f"inputs {alg / 1e9:.3f} GB per GPU < 4x L2: GPU arm flushes L2 ({4 * L2_BYTES / 2**20:.0f} MiB write + read) "
+          f"before every step, outside the timed pair")
+    return {"workload": name, "n_rows": A.n_rows, "n_cols": A.n_cols, "nnz": A.nnz, "l2": l2,
+            "checksum": A.checksum(), "x_checksum": hecgen.fnv1a(x_h)}
 
 
 def grid_of(A):
@@ -86,17 +105,82 @@ def measured_peak():
         return 6650.0, "fallback (B200_PROFILING.md 6.65 TB/s)"
 
 
-def ncu_traffic(config: str):
-    """dram__bytes_read.sum + dram__bytes_write.sum per step (summed over the
-    step's kernels: ell_kernel, plus tail_kernel where the matrix has a tail)
-    from the committed ncu --set full captures (profiles/ncu_traffic.json), and
-    the per-kernel split; (None, None) if absent."""
+def csrc_hash() -> str:
+    """sha256[:16] over the product's native sources (csrc/ + include/): keys the
+    committed ncu traffic so a stale capture is never reported for new code."""
+    import glob
+    import hashlib
+    h = hashlib.sha256()
+    files = sorted(glob.glob(os.path.join(ROOT, "paper_1606_00545_b200", "csrc", "*")) +
+                   glob.glob(os.path.join(ROOT, "include", "*.h")))
+    for f in files:
+        h.update(os.path.basename(f).encode())
+        with open(f, "rb") as fh:
+            h.update(fh.read())
+    return h.hexdigest()[:16]
+
+
+def ncu_traffic_committed(config: str):
+    """Fallback: dram__bytes_read.sum + dram__bytes_write.sum per step from the
+    committed ncu captures (profiles/ncu_traffic.json), used ONLY when the
+    capture's csrc_sha matches the current native sources."""
     p = os.path.join(ROOT, "profiles", "ncu_traffic.json")
     try:
         d = json.load(open(p)).get(config, {})
-        return d.get("dram_bytes_per_step"), {k: v["dram_bytes_per_launch"] for k, v in d.get("kernels", {}).items()}
     except Exception:
-        return None, None
+        return None, None, "no committed capture"
+    if d.get("csrc_sha") != csrc_hash():
+        return None, None, f"committed capture is for csrc {d.get('csrc_sha')}, not {csrc_hash()} (stale: dropped)"
+    return (d.get("dram_bytes_per_step"), {k: v["dram_bytes_per_launch"] for k, v in d.get("kernels", {}).items()},
+            f"profiles/ncu_traffic.json (csrc {d.get('csrc_sha')})")
+
+
+def ncu_traffic_live(config: str, launches_per_step: int, timeout_s: float = 300.0):
+    """In-run measurement of roofline.traffic: re-runs this bench (--profile, 2
+    warm-up + 3 timed steps) under `ncu --metrics dram__bytes_read.sum,
+    dram__bytes_write.sum,gpu__time_duration.sum` restricted to the HEC
+    kernels, and takes the LAST step's launches (warm caches, the timed
+    configuration).  Returns (bytes per step, {kernel: bytes}, {kernel: ncu
+    ms}, source) or Nones with the reason."""
+    import csv
+    import shutil
+    import tempfile
+    ncu = shutil.which("ncu") or ("/usr/local/cuda/bin/ncu" if os.path.exists("/usr/local/cuda/bin/ncu") else None)
+    if ncu is None:
+        return None, None, None, "ncu not found"
+    log = tempfile.NamedTemporaryFile(prefix="hec_ncu_", suffix=".csv", delete=False).name
+    cmd = [ncu, "--metrics", "dram__bytes_read.sum,dram__bytes_write.sum,gpu__time_duration.sum",
+           "--clock-control", "none", "--csv", "--log-file", log, "-k", "regex:ell_kernel|tail_kernel",
+           sys.executable, os.path.abspath(__file__), "--profile", "--config", config,
+           "--steps", "3", "--warmup", "2"]
+    try:
+        r = subprocess.run(cmd, stdout=subprocess.DEVNULL, stderr=subprocess.PIPE, timeout=timeout_s, text=True)
+        rows = list(csv.reader(l for l in open(log) if l.startswith('"')))
+    except Exception as e:
+        return None, None, None, f"ncu pass failed: {str(e)[:120]}"
+    finally:
+        try:
+            os.unlink(log)
+        except OSError:
+            pass
+    if not rows or r.returncode != 0:
+        return None, None, None, f"ncu pass rc={r.returncode}: {r.stderr[-160:] if r.stderr else ''}"
+    hdr = rows[0]
+    iid, ik, im, iv = hdr.index("ID"), hdr.index("Kernel Name"), hdr.index("Metric Name"), hdr.index("Metric Value")
+    per = {}
+    for row in rows[1:]:
+        k = per.setdefault(int(row[iid]), {"kernel": row[ik]})
+        k[row[im]] = float(row[iv].replace(",", ""))
+    ids = sorted(per)[-launches_per_step:]
+    split, times = {}, {}
+    for i in ids:
+        k = per[i]
+        name = k["kernel"].split("<")[0].replace("void ", "").strip()
+        split[name] = int(k.get("dram__bytes_read.sum", 0) + k.get("dram__bytes_write.sum", 0))
+        times[name] = round(k.get("gpu__time_duration.sum", 0.0) * 1e-6, 5)  # ns -> ms
+    return (sum(split.values()), split, times,
+            f"measured in this run: ncu --metrics dram__bytes_read.sum,dram__bytes_write.sum (last of 5 steps, "
+            f"{launches_per_step} launch(es)/step)")
 
 
 class L2Flusher:
@@ -168,22 +252,66 @@ class ClockSampler:
 
 
 # --------------------------------------------------------- cpu baseline ----
-def cpu_oracle_rate(A, x, budget_s=12.0, max_s=30.0):
-    """The oracle O1 as it stands (serial C, one core), timed on the whole
-    matrix repeatedly until ~budget_s of CPU work; best-of and mean reported."""
+def host_description() -> dict:
+    """lscpu model name, sockets, cores, threads and NUMA nodes
+    of the host the CPU legs run on (read at run time)."""
+    info = {"logical_cpus": os.cpu_count(), "usable_cpus": len(os.sched_getaffinity(0))}
+    try:
+        out = subprocess.run(["lscpu"], capture_output=True, text=True, timeout=10).stdout
+        keys = {"Model name": "model", "Socket(s)": "sockets", "Core(s) per socket": "cores_per_socket",
+                "Thread(s) per core": "threads_per_core", "NUMA node(s)": "numa_nodes", "CPU max MHz": "max_mhz"}
+        for line in out.splitlines():
+            k, _, v = line.partition(":")
+            if k.strip() in keys and keys[k.strip()] not in info:
+                info[keys[k.strip()]] = v.strip()
+    except Exception as e:
+        info["lscpu_error"] = str(e)[:80]
+    return info
+
+
+class pinned_core:
+    """`taskset -c <core>` for the calling thread (Linux sched_setaffinity on
+    pid 0 applies to the calling thread), restored on exit: the serial oracle
+    leg runs on one pinned core (the paper's "CPU sequential
+    running time")."""
+
+    def __init__(self):
+        self.prev = os.sched_getaffinity(0)
+        self.core = min(self.prev)
+
+    def __enter__(self):
+        os.sched_setaffinity(0, {self.core})
+        return self
+
+    def __exit__(self, *a):
+        os.sched_setaffinity(0, self.prev)
+
+
+def serial_oracle_ms(A, x, budget_s: float, max_s: float = 30.0):
+    """The oracle O1 as it stands (serial C), whole matrix, on one pinned core:
+    1 warm-up, then repetitions until ~budget_s; (best ms, mean ms, reps, core)."""
     import oracle
-    oracle.csr_spmv(A, x, 0, min(A.n_rows, 1024))  # load/build the library
-    times = []
-    t_all = time.perf_counter()
-    while True:
-        t0 = time.perf_counter()
-        oracle.csr_spmv(A, x)
-        times.append(time.perf_counter() - t0)
-        el = time.perf_counter() - t_all
-        if el >= budget_s or el + times[-1] > max_s:
-            break
-    best = min(times)
-    # SURVEY §8(d) (ii): the same O1 rows over all host cores (OpenMP), bit-identical, ~3 s
+    oracle._load()                       # libgomp sizes its pool from the UNPINNED mask
+    with pinned_core() as pc:
+        oracle.csr_spmv(A, x)            # warm-up
+        times = []
+        t_all = time.perf_counter()
+        while True:
+            t0 = time.perf_counter()
+            oracle.csr_spmv(A, x)
+            times.append(time.perf_counter() - t0)
+            el = time.perf_counter() - t_all
+            if (el >= budget_s and len(times) >= 3) or el + times[-1] > max_s:
+                break
+    return min(times) * 1e3, sum(times) / len(times) * 1e3, len(times), pc.core
+
+
+def cpu_oracle_rate(A, x, budget_s=12.0, max_s=30.0):
+    """(i) the oracle O1 as it stands, serial, pinned to one core, on the whole
+    matrix repeated for ~budget_s; (ii) the same O1 rows over all host threads
+    (OpenMP, bit-identical), ~3 s.  Plus the lscpu record."""
+    import oracle
+    best, mean, reps, core = serial_oracle_ms(A, x, budget_s, max_s)
     par_times, threads = [], 1
     t_all = time.perf_counter()
     while time.perf_counter() - t_all < 3.0 and len(par_times) < 50:
@@ -191,13 +319,52 @@ def cpu_oracle_rate(A, x, budget_s=12.0, max_s=30.0):
         _, threads = oracle.csr_spmv_parallel(A, x)
         par_times.append(time.perf_counter() - t0)
     pbest = min(par_times)
-    return {"value": round(2 * A.nnz / best / 1e9, 4), "unit": "GFLOP/s", "cores": 1, "kind": "oracle",
-            "sample": f"whole {A.name} matrix ({A.n_rows} rows, {A.nnz} nnz), serial O1, "
-                      f"{len(times)} reps in {sum(times):.1f} s, best rep {best * 1e3:.1f} ms",
-            "mean_gflops": round(2 * A.nnz * len(times) / sum(times) / 1e9, 4),
+    alg = algorithmic_bytes(A.nnz, A.n_rows, A.n_cols)
+    return {"value": round(2 * A.nnz / (best * 1e-3) / 1e9, 4), "unit": "GFLOP/s", "cores": 1, "kind": "oracle",
+            "sample": f"whole {A.name} matrix ({A.n_rows} rows, {A.nnz} nnz), serial O1 pinned to core {core} "
+                      f"(taskset equivalent), 1 warm-up + {reps} reps, best {best:.1f} ms, mean {mean:.1f} ms",
+            "gbs": round(alg / (best * 1e-3) / 1e9, 2),
+            "mean_gflops": round(2 * A.nnz / (mean * 1e-3) / 1e9, 4),
+            "host": host_description(),
             "parallel": {"value": round(2 * A.nnz / pbest / 1e9, 4), "unit": "GFLOP/s", "cores": threads,
                          "kind": "oracle O1 rows over OpenMP threads (bit-identical)",
                          "sample": f"{len(par_times)} reps, best {pbest * 1e3:.1f} ms"}}
+
+
+def paper_anchor(dev: int, budget_s: float = 4.0):
+    """SURVEY §8(d) paper anchor (context, not a target): the paper's own
+    3D_Poisson 150^3 -- GPU hec_spmv time (cold L2, median of 30) and
+    the serial oracle on one pinned core -- and their ratio in the paper's
+    speedup definition (CPU sequential time / GPU time), beside Table 3's
+    HEC value for 3D_Poisson, 13.63x (Tesla C2050/C2070 vs a Xeon X5570
+    core, P:378-380) and "most ... over 10 and the highest ... 18" (P:413)."""
+    import torch
+    import paper_1606_00545_b200 as hec
+    A = hecgen.poisson3d(150, 150, 150)
+    x_h = hecgen.vector(A.n_cols, "uniform", seed=1606)
+    M = hec.from_csr(A, device=dev)
+    x = torch.from_numpy(x_h).to(f"cuda:{dev}")
+    y = torch.empty(A.n_rows, dtype=torch.float64, device=f"cuda:{dev}")
+    fl = L2Flusher(f"cuda:{dev}")
+    for _ in range(5):
+        M.spmv(x, y)
+    ev = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)) for _ in range(30)]
+    for a, b in ev:
+        fl()
+        a.record()
+        M.spmv(x, y)
+        b.record()
+    torch.cuda.synchronize()
+    gpu_ms = statistics.median(a.elapsed_time(b) for a, b in ev)
+    best, mean, reps, core = serial_oracle_ms(A, x_h, budget_s)
+    M.free()
+    return {"config": "poisson3d_150 (the paper's 3D_Poisson, P:406)", "gpu_ms": round(gpu_ms, 5),
+            "gpu_l2": "cold (flushed), median of 30", "serial_oracle_ms": round(best, 3),
+            "serial_sample": f"O1 pinned to core {core}, best of {reps}",
+            "speedup_vs_serial": round(best / gpu_ms, 1),
+            "paper_speedup_hec_3d_poisson": 13.63, "paper_claim": "most HEC speedups over 10, highest 18 (P:413)",
+            "paper_hardware": "NVIDIA Tesla C2050/C2070 vs Intel Xeon X5570 serial -O3 (P:378-382)",
+            "note": "context only: different hardware; the CPU side here is the oracle as it stands"}
 
 
 # ------------------------------------------------------------ reference ----
@@ -225,22 +392,23 @@ def run_reference(args):
         r0 = int(starts[k])
         oracle.csr_spmv(A, x, r0, r0 + rows)
     flops, total = 0, 0.0
-    for k in range(args.warmup, args.warmup + args.steps):
-        r0 = int(starts[k])
-        t0 = time.perf_counter()
-        oracle.csr_spmv(A, x, r0, r0 + rows)
-        total += time.perf_counter() - t0
-        flops += 2 * int(A.row_ptr[r0 + rows] - A.row_ptr[r0])
+    with pinned_core() as pc:
+        for k in range(args.warmup, args.warmup + args.steps):
+            r0 = int(starts[k])
+            t0 = time.perf_counter()
+            oracle.csr_spmv(A, x, r0, r0 + rows)
+            total += time.perf_counter() - t0
+            flops += 2 * int(A.row_ptr[r0 + rows] - A.row_ptr[r0])
     value = flops / total / 1e9
     sample = (f"{rows} contiguous rows of {A.name} per step ({'whole matrix' if rows == A.n_rows else 'bounded sample'}), "
-              f"serial O1 (spmv_oracle.c, -O2 -ffp-contract=off), 1 core")
+              f"serial O1 (spmv_oracle.c, -O2 -ffp-contract=off), pinned to core {pc.core}")
     line = {"metric": METRIC, "value": round(value, 4), "unit": "GFLOP/s", "n_gpus": args.gpus,
             "steps": args.steps, "warmup": args.warmup, "ms_per_step": round(total / args.steps * 1e3, 4),
             "higher_is_better": True, "scaling": "strong", "vs_baseline": None, "dtype": "f64",
             "data": "synthetic", "impl": "reference",
-            "config": {"workload": args.config, "n_rows": A.n_rows, "nnz": A.nnz},
+            "config": workload_config(args.config, A, x, max(1, args.gpus)),
             "cpu_baseline": {"value": round(value, 4), "unit": "GFLOP/s", "cores": 1, "kind": "oracle",
-                             "sample": sample},
+                             "sample": sample, "host": host_description()},
             "e2e": {"value": round(value, 4), "unit": "GFLOP/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
     print(json.dumps(line), flush=True)
     return 0
@@ -323,9 +491,8 @@ def run_single(args):
     # dominant kernel: the ELL kernel (the only launch per step when there is no tail)
     mean_launch_ms = statistics.mean(per)
     achieved = alg / (mean_launch_ms * 1e-3) / 1e9
-    traffic, traffic_split = ncu_traffic(args.config)
     roof = {"bound": "hbm", "achieved": round(achieved, 1), "peak": peak, "unit": "GB/s",
-            "frac": round(achieved / peak, 4), "traffic": traffic, "traffic_by_kernel": traffic_split,
+            "frac": round(achieved / peak, 4), "traffic": None, "traffic_by_kernel": None,
             "kernel": "ell_kernel" + ("" if launches_per_step == 1 else "+tail_kernel (step)"),
             "algorithmic_bytes_per_launch": alg, "format_bytes_per_launch": fmt_bytes,
             "peak_source": peak_src, "frac_of_8TBs_nominal": round(achieved / 8000.0, 4),
@@ -373,30 +540,95 @@ def run_single(args):
                "h2d_bytes_per_step": 8 * A.n_cols, "d2h_bytes_per_step": 8 * A.n_rows,
                "ms_per_step": round(dt * 1e3, 4), "steps": Ke, "api": "hec_spmv_host (pinned host x, y)"}
 
+    # roofline.traffic: dram bytes per launch measured by an ncu pass of this
+    # same bench (subprocess), else the committed capture if it is for these
+    # exact native sources, else null
+    if not args.profile:
+        if args.no_ncu or args.scramble is not None or args.reorder or args.ell_width is not None:
+            tr, split, ncu_ms, src = None, None, None, "skipped (--no-ncu or a non-default workload)"
+        else:
+            M.free()  # release the device copy while the ncu child builds its own
+            torch.cuda.empty_cache()
+            tr, split, ncu_ms, src = ncu_traffic_live(args.config, launches_per_step)
+            if tr is None:
+                reason = src
+                tr, split, src = ncu_traffic_committed(args.config)
+                src = f"{src} (live pass unavailable: {reason})"
+                ncu_ms = None
+        roof.update({"traffic": tr, "traffic_by_kernel": split, "traffic_source": src,
+                     "ncu_ms_by_kernel": ncu_ms, "csrc_sha": csrc_hash()})
+        if tr:
+            roof["traffic_over_algorithmic"] = round(tr / alg, 4)
+
     cpu = None
     if not args.no_cpu_baseline and not args.profile:
         cpu = cpu_oracle_rate(A, x_h)
+        cpu["gpu_speedup_vs_serial"] = round(2 * A.nnz / (ms_step * 1e-3) / 1e9 / cpu["value"], 1)
+    anchor = None
+    if not args.no_anchor and not args.profile:
+        anchor = paper_anchor(dev)
 
     line = {"metric": METRIC, "value": round(gflops, 2), "unit": "GFLOP/s", "n_gpus": 1, "steps": K,
             "warmup": args.warmup, "ms_per_step": round(ms_step, 5), "higher_is_better": True,
             "scaling": "strong", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
-            "config": {"workload": args.config, "n_rows": A.n_rows, "n_cols": A.n_cols, "nnz": A.nnz,
-                       "ell_width": inf.ell_width, "ell_stride": inf.ell_stride, "tail_rows": inf.tail_rows,
-                       "tail_nnz": inf.tail_nnz, "parallelism": "1 GPU",
-                       "width_policy": "BG3 (A1)" if args.ell_width is None else f"FIXED {args.ell_width} (experiment)",
-                       "l2": (f"inputs {alg / 1e9:.2f} GB > 4x {L2_BYTES / 2**20:.0f} MiB L2, no flush" if not flush
-                              else f"L2 flushed ({4 * L2_BYTES / 2**20:.0f} MiB write + read) before every step, outside the timed pair"),
-                       "checksum": A.checksum(), "x_checksum": hecgen.fnv1a(x_h), "setup_s": {"generate": round(t_gen, 2), "convert_upload": round(t_conv, 2)},
-                       "reorder": reorder_info},
+            "config": workload_config(args.config, A, x_h),
+            "run": {"parallelism": "1 GPU", "ell_width": inf.ell_width, "ell_stride": inf.ell_stride,
+                    "tail_rows": inf.tail_rows, "tail_nnz": inf.tail_nnz,
+                    "width_policy": "BG3 (A1)" if args.ell_width is None else f"FIXED {args.ell_width} (experiment)",
+                    "setup_s": {"generate": round(t_gen, 2), "convert_upload": round(t_conv, 2)},
+                    "reorder": reorder_info},
             "gbs": round(alg / (ms_step * 1e-3) / 1e9, 1),
             "roofline": roof, "gpu_launches": K * launches_per_step,
-            "e2e": e2e, "cpu_baseline": cpu,
+            "e2e": e2e, "cpu_baseline": cpu, "paper_anchor": anchor,
             "clocks": sampler.summary() if sampler else None}
     print(json.dumps(line), flush=True)
     return 0
 
 
 # ------------------------------------------------------------- multi GPU ----
+def time_dist_steps(D, x, y, stream, K, flusher, dist, torch):
+    """SURVEY §8(d) multi-GPU protocol, per repetition: every rank scrubs L2
+    (when its working set is < 4x L2), a tiny NCCL all-reduce aligns the ranks
+    on the device, then each rank times ONE hec_spmv_dist with CUDA events on
+    the launch stream.  T(P) of a repetition = the max over ranks (all-reduce
+    MAX of the per-repetition times).  Returns the per-repetition maxima (ms)
+    and the wall time between the bracketing barriers (s)."""
+    align = torch.zeros(1, dtype=torch.float32, device="cuda")
+    ev = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)) for _ in range(K)]
+    dist.barrier()
+    torch.cuda.synchronize()
+    t0 = time.perf_counter()
+    with torch.cuda.stream(stream):
+        for k in range(K):
+            if flusher:
+                flusher()  # outside the timed pair: evicts this rank's matrix from L2
+            dist.all_reduce(align)  # the stream waits until every rank got here
+            ev[k][0].record(stream)
+            D.spmv(x, y, stream)
+            ev[k][1].record(stream)
+    torch.cuda.synchronize()
+    dist.barrier()
+    wall = time.perf_counter() - t0
+    per = torch.tensor([a.elapsed_time(b) for a, b in ev], dtype=torch.float64, device="cuda")
+    dist.all_reduce(per, op=dist.ReduceOp.MAX)
+    return per.cpu().numpy(), wall
+
+
+def dist_parity(A, x_h, y, r0, r1, dist, torch):
+    """Every row of every rank against the serial C oracle O1 (tolerance
+    1e-12 (|A||x|)_i): each rank checks its own rows [r0, r1); the bad-row
+    counts are summed over ranks.  Makes the first N > 1 run self-proving."""
+    import oracle
+    got = y.cpu().numpy()
+    ref = oracle.csr_spmv(A, x_h, r0, r1)
+    tol = oracle.tolerance(A, x_h, r0, r1)
+    bad = torch.tensor([float(np.count_nonzero(~(np.abs(got - ref) <= tol))), float(r1 - r0)],
+                       dtype=torch.float64, device="cuda")
+    dist.all_reduce(bad)
+    return {"rows_checked": int(bad[1].item()), "bad_rows": int(bad[0].item()),
+            "vs": "oracle O1 (serial C), every row, |y - y_ref| <= 1e-12 (|A||x|)_i", "ok": bad[0].item() == 0}
+
+
 def run_multi(args):
     import torch
     import torch.distributed as dist
@@ -413,26 +645,7 @@ def run_multi(args):
     obj = [hec.nccl_unique_id() if rank == 0 else None]
     dist.broadcast_object_list(obj, src=0)
     D = hec.Dist(A, plan, rank, obj[0], local)
-    transport = "nccl"
-    if args.transport == "p2p" and world > 1:
-        # peer-memory transport (IPC windows exchanged over the handle's NCCL
-        # communicator); if any rank cannot map its peers, every rank falls
-        # back to a fresh NCCL-transport handle
-        ok = 1.0
-        try:
-            D.enable_p2p()
-        except hec.HecError as e:
-            print(f"rank {rank}: peer-memory transport unavailable ({e}); using NCCL", file=sys.stderr)
-            ok = 0.0
-        okt = torch.tensor([ok], device="cuda")
-        dist.all_reduce(okt, op=dist.ReduceOp.MIN)
-        if okt.item() > 0.5:
-            transport = "p2p"
-        else:
-            D.free()
-            obj = [hec.nccl_unique_id() if rank == 0 else None]
-            dist.broadcast_object_list(obj, src=0)
-            D = hec.Dist(A, plan, rank, obj[0], local)
+    comm_ranks, nccl_version = D.comm_size()
     x_h = hecgen.vector(A.n_cols, "uniform", seed=1606)
     r0, r1 = D.info.r0, D.info.r1
     x = torch.from_numpy(x_h[r0:r1].copy()).cuda()
@@ -441,95 +654,107 @@ def run_multi(args):
     # L2 policy: flush between steps unless this rank's working set is far larger than L2
     flush = D.info.algorithmic_bytes < 4 * L2_BYTES
     flusher = L2Flusher("cuda") if flush else None
-    with torch.cuda.stream(stream):
-        for _ in range(args.warmup):
-            D.spmv(x, y, stream)
-    torch.cuda.synchronize()
     K = args.steps
-    ev = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)) for _ in range(K)]
-    sampler = ClockSampler(local) if not args.profile else None
-    dist.barrier()
-    torch.cuda.synchronize()
-    if sampler:
-        sampler.__enter__()
-    with torch.cuda.stream(stream):
-        for k in range(K):
-            if flush:
-                flusher()  # outside the timed pair: evicts this rank's matrix from L2
-            ev[k][0].record(stream)
-            D.spmv(x, y, stream)
-            ev[k][1].record(stream)
-    torch.cuda.synchronize()
-    dist.barrier()
-    if sampler:
-        sampler.__exit__()
-    ms = sum(a.elapsed_time(b) for a, b in ev)  # device time of the K steps on this rank
-    t = torch.tensor([ms], dtype=torch.float64, device="cuda")
-    dist.all_reduce(t, op=dist.ReduceOp.MAX)
-    ms_max = float(t.item())
+    # transports to time: NCCL send/recv (the handle as created), then the
+    # peer-memory push (the same handle switched by hec_dist_enable_p2p)
+    order = {"p2p": ["p2p"], "nccl": ["nccl"], "both": ["nccl", "p2p"]}[args.transport] if world > 1 else ["none"]
+    results, sampler = {}, None
+    for t in order:
+        if t == "p2p":
+            ok = 1.0
+            try:
+                D.enable_p2p()
+            except hec.HecError as e:
+                print(f"rank {rank}: peer-memory transport unavailable ({e})", file=sys.stderr)
+                ok = 0.0
+            okt = torch.tensor([ok], device="cuda")
+            dist.all_reduce(okt, op=dist.ReduceOp.MIN)
+            if okt.item() < 0.5:
+                results[t] = {"unavailable": "hec_dist_enable_p2p failed on some rank (see stderr)"}
+                if len(order) == 1:  # fall back to the NCCL transport on a fresh handle
+                    D.free()
+                    obj = [hec.nccl_unique_id() if rank == 0 else None]
+                    dist.broadcast_object_list(obj, src=0)
+                    D = hec.Dist(A, plan, rank, obj[0], local)
+                    t = "nccl"
+                else:
+                    continue
+        with torch.cuda.stream(stream):
+            for _ in range(args.warmup):
+                D.spmv(x, y, stream)
+        torch.cuda.synchronize()
+        sampler = ClockSampler(local) if not args.profile else None
+        if sampler:
+            sampler.__enter__()
+        per, wall = time_dist_steps(D, x, y, stream, K, flusher, dist, torch)
+        if sampler:
+            sampler.__exit__()
+        D.check()  # raises if a peer-memory halo wait timed out (the results would be garbage)
+        par = dist_parity(A, x_h, y, r0, r1, dist, torch)
+        ms_mean = float(np.mean(per))
+        results[t] = {"ms_per_step": round(ms_mean, 5), "median_ms": round(float(np.median(per)), 5),
+                      "p10_ms": round(float(np.percentile(per, 10)), 5),
+                      "p90_ms": round(float(np.percentile(per, 90)), 5),
+                      "gflops": round(2 * A.nnz / (ms_mean * 1e-3) / 1e9, 2),
+                      "wall_s_between_barriers": round(wall, 4), "parity": par,
+                      "launches_per_step": D.info.launches, "clocks": sampler.summary() if sampler else None}
+    head = "p2p" if "p2p" in results and "ms_per_step" in results["p2p"] else \
+        ("nccl" if "nccl" in results else order[-1])
+    hr = results[head]
     alg_loc = torch.tensor([float(D.info.algorithmic_bytes)], dtype=torch.float64, device="cuda")
     dist.all_reduce(alg_loc)
-    # oracle-free parity spot check: for the Laplacians (A 1)_i = diag - deg(i)
-    ok = bool(torch.isfinite(y).all().item())
-    if A.grid is not None:
-        ones = torch.ones(r1 - r0, dtype=torch.float64, device="cuda")
-        with torch.cuda.stream(stream):
-            D.spmv(ones, y, stream)
-        torch.cuda.synchronize()
-        lens = np.diff(A.row_ptr[r0:r1 + 1]).astype(np.float64)
-        diag = 6.0 if A.grid[2] > 1 else 4.0
-        ok = ok and bool(np.array_equal(y.cpu().numpy(), diag - (lens - 1)))
-    okt = torch.tensor([1.0 if ok else 0.0], device="cuda")
-    dist.all_reduce(okt, op=dist.ReduceOp.MIN)
-    # end to end through the public API: pinned host x slice -> device, SpMV, y slice -> host
+    # end to end through the public C ABI with HOST buffers: hec_spmv_dist_host
+    # (H2D of this rank's x slice, the distributed product, D2H of its y slice)
     e2e = None
     if not args.no_e2e and not args.profile:
         xp = torch.from_numpy(x_h[r0:r1].copy()).pin_memory()
         yp = torch.empty(r1 - r0, dtype=torch.float64).pin_memory()
-        xd = torch.empty_like(x)
         Ke = max(3, min(K, 50))
+        for _ in range(2):
+            D.spmv_host(xp, yp, stream)
         dist.barrier()
-        torch.cuda.synchronize()
         t0 = time.perf_counter()
-        with torch.cuda.stream(stream):
-            for _ in range(Ke):
-                xd.copy_(xp, non_blocking=True)
-                D.spmv(xd, y, stream)
-                yp.copy_(y, non_blocking=True)
-                stream.synchronize()
+        for _ in range(Ke):
+            D.spmv_host(xp, yp, stream)
         dt = torch.tensor([(time.perf_counter() - t0) / Ke], dtype=torch.float64, device="cuda")
         dist.all_reduce(dt, op=dist.ReduceOp.MAX)
         e2e = {"value": round(2 * A.nnz / float(dt.item()) / 1e9, 3), "unit": "GFLOP/s",
                "h2d_bytes_per_step": 8 * A.n_cols, "d2h_bytes_per_step": 8 * A.n_rows,
                "ms_per_step": round(float(dt.item()) * 1e3, 4), "steps": Ke,
-               "api": "hec_spmv_dist with pinned host slices (H2D + D2H inside each step), max over ranks"}
+               "api": "hec_spmv_dist_host (pinned host slices; H2D + product + D2H per step), max over ranks"}
     if rank == 0:
-        ms_step = ms_max / K
+        ms_step = hr["ms_per_step"]
         gflops = 2 * A.nnz / (ms_step * 1e-3) / 1e9
         peak, peak_src = measured_peak()
         achieved = float(alg_loc.item()) / world / (ms_step * 1e-3) / 1e9
+        pname = 'GRID slabs' if kind == hec.PART_GRID else 'CONTIG_COST' if kind == hec.PART_CONTIG_COST else 'CONTIG_NNZ'
         line = {"metric": METRIC, "value": round(gflops, 2), "unit": "GFLOP/s", "n_gpus": world, "steps": K,
                 "warmup": args.warmup, "ms_per_step": round(ms_step, 5), "higher_is_better": True,
                 "scaling": "strong", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
-                "config": {"workload": args.config, "n_rows": A.n_rows, "nnz": A.nnz,
-                           "parallelism": f"row partition x{world} ({'GRID slabs' if kind == hec.PART_GRID else 'CONTIG_COST' if kind == hec.PART_CONTIG_COST else 'CONTIG_NNZ'}), "
-                                          + ("peer-memory halo push over NVLink" if transport == "p2p" else "NCCL halo exchange"),
-                           "transport": transport if world > 1 else None,
+                "config": workload_config(args.config, A, x_h, world),
+                "run": {"parallelism": f"row partition x{world} ({pname}), "
+                                          + {"p2p": "peer-memory halo push over NVLink",
+                                             "nccl": "NCCL send/recv halo exchange",
+                                             "none": "single rank (no exchange)"}[head],
+                           "transport": head,
+                           "timing": "per repetition: L2 scrub (if needed), NCCL all-reduce alignment, event pair "
+                                     "around one hec_spmv_dist; T = max over ranks per repetition; value from the mean",
                            "l2": ("L2 flushed (504 MiB write + 504 MiB read) before every step, outside the timed pair" if flush
                                   else "per-rank inputs > 4x L2, no flush")},
                 "gbs": round(float(alg_loc.item()) / (ms_step * 1e-3) / 1e9, 1),
                 "roofline": {"bound": "hbm", "achieved": round(achieved, 1), "peak": peak, "unit": "GB/s",
                              "frac": round(achieved / peak, 4), "traffic": None,
                              "kernel": "whole step per rank (interior + boundary SpMV, halo exchange)",
-                             "peak_source": peak_src},
-                "gpu_launches": K * D.info.launches, "e2e": e2e, "cpu_baseline": None,
-                "clocks": sampler.summary() if sampler else None,
-                "parity_closed_form": bool(okt.item() > 0.5) if A.grid is not None else None}
+                             "peak_source": peak_src, "median_step_ms": hr["median_ms"]},
+                "parity": hr["parity"], "transports": results,
+                "nccl": {"version": nccl_version, "comm_ranks": comm_ranks},
+                "gpu_launches": K * hr["launches_per_step"], "e2e": e2e, "cpu_baseline": None,
+                "clocks": hr["clocks"]}
         print(json.dumps(line), flush=True)
     D.free()
     dist.barrier()
     dist.destroy_process_group()
-    return 0
+    return 0 if all(r.get("parity", {}).get("ok", True) for r in results.values()) else 3
 
 
 def run_solver(args):

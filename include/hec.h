@@ -335,6 +335,17 @@ hec_status hec_dist_create_local(const hec_csr* A, hec_plan P, const hec_opts* o
  * Asynchronous; ordered after prior work on `stream` and before later work on it. */
 hec_status hec_spmv_dist(hec_dist D, const double* x_local, double* y_local, void* stream);
 
+/* COLLECTIVE, end to end with HOST buffers (the distributed analogue of
+ * hec_spmv_host): copies x_host_local (n_loc doubles, pageable or pinned) to a
+ * device staging buffer on `stream`, runs hec_spmv_dist, copies y back into
+ * y_host_local (n_loc doubles) and synchronises `stream`.  Staging buffers are
+ * allocated by the first call and kept in the handle. */
+hec_status hec_spmv_dist_host(hec_dist D, const double* x_host_local, double* y_host_local, void* stream);
+
+/* The handle's NCCL communicator: *nranks = ncclCommCount (0 when the handle
+ * has none: P = 1 or a peer-memory-only handle), *version = ncclGetVersion. */
+hec_status hec_dist_comm_size(hec_dist D, int32_t* nranks, int32_t* version);
+
 /* ---- peer-memory halo transport ----
  * The export of P:158 without NCCL: every rank exposes a receive window (its
  * arrival flags and two halo buffers, alternating by call parity) through CUDA

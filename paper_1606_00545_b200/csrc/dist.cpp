@@ -13,6 +13,7 @@
 #include <memory>
 
 #include <nccl.h>
+#include <nvtx3/nvToolsExt.h>  // header-only NVTX v3: host ranges around each phase's enqueue (nsys)
 
 #include "hec_internal.h"
 
@@ -48,6 +49,8 @@ struct hec_dist_s {
     uint64_t epoch = 0;
     void* ws = nullptr;                 // Krylov workspace (krylov.cu), freed through ws_free
     void (*ws_free)(void*) = nullptr;
+    double* d_stage_x = nullptr;        // hec_spmv_dist_host staging (first call)
+    double* d_stage_y = nullptr;
 };
 
 namespace hec {
@@ -82,6 +85,8 @@ static void dist_release(hec_dist_s* d) {
     if (d->d_send_idx) cudaFree(d->d_send_idx);
     if (d->d_sendbuf) cudaFree(d->d_sendbuf);
     if (d->d_x_halo) cudaFree(d->d_x_halo);
+    if (d->d_stage_x) cudaFree(d->d_stage_x);
+    if (d->d_stage_y) cudaFree(d->d_stage_y);
     hec_free(d->interior);
     hec_free(d->boundary);
     cudaSetDevice(cur);
@@ -444,7 +449,15 @@ namespace hec {
 // stream waits for the exchange before the boundary rows AND before returning
 // control of `s`, so every later NCCL call issued on `s` (e.g. the Krylov
 // all-reduces) is ordered after this exchange on every rank.
+// Host-side NVTX range for the scope (one phase of hec_spmv_dist's enqueue);
+// an nsys timeline lines the ranges up with the kernels they launch.
+struct NvtxRange {
+    explicit NvtxRange(const char* name) { nvtxRangePushA(name); }
+    ~NvtxRange() { nvtxRangePop(); }
+};
+
 hec_status dist_spmv_launch(hec_dist_s* D, const double* x_local, double* y_local, cudaStream_t s) {
+    NvtxRange all("hec_spmv_dist");
     if (D->p2p && !D->nbr.empty()) {
         // peer-memory transport: fused pack + NVLink stores + flag release on
         // the comm stream, then wait for the neighbours' flags and run the
@@ -452,15 +465,22 @@ hec_status dist_spmv_launch(hec_dist_s* D, const double* x_local, double* y_loca
         const uint64_t ep = ++D->epoch;
         HEC_CUDA_TRY(cudaEventRecord(D->ev_start, s));
         HEC_CUDA_TRY(cudaStreamWaitEvent(D->comm_stream, D->ev_start, 0));
-        HEC_CUDA_TRY(launch_push(push_args(D, x_local, ep), D->comm_stream));
+        {
+            NvtxRange r("hec.push (pack + NVLink stores + release)");
+            HEC_CUDA_TRY(launch_push(push_args(D, x_local, ep), D->comm_stream));
+        }
         const PeerWait w = wait_args(D, ep);
-        if (D->n_boundary > 0) {
-            hec_status st = launch_spmv_peer(D->boundary, x_local, p2p_halo(D, ep), y_local, D->comm_stream, w);
-            if (st != HEC_OK) return st;
-        } else {
-            HEC_CUDA_TRY(launch_peer_wait(w, D->comm_stream));
+        {
+            NvtxRange r("hec.wait + boundary");
+            if (D->n_boundary > 0) {
+                hec_status st = launch_spmv_peer(D->boundary, x_local, p2p_halo(D, ep), y_local, D->comm_stream, w);
+                if (st != HEC_OK) return st;
+            } else {
+                HEC_CUDA_TRY(launch_peer_wait(w, D->comm_stream));
+            }
         }
         HEC_CUDA_TRY(cudaEventRecord(D->ev_halo, D->comm_stream));
+        NvtxRange r("hec.interior");
         hec_status st = launch_spmv(D->interior, x_local, nullptr, y_local, s);
         if (st != HEC_OK) return st;
         HEC_CUDA_TRY(cudaStreamWaitEvent(s, D->ev_halo, 0));
@@ -473,6 +493,7 @@ hec_status dist_spmv_launch(hec_dist_s* D, const double* x_local, double* y_loca
         // comm stream: pack + grouped send/recv, overlapped with the interior SpMV
         HEC_CUDA_TRY(cudaEventRecord(D->ev_start, s));
         HEC_CUDA_TRY(cudaStreamWaitEvent(D->comm_stream, D->ev_start, 0));
+        NvtxRange rx("hec.pack + ncclSend/ncclRecv + boundary");
         HEC_CUDA_TRY(launch_pack(D->d_send_idx, D->n_send, x_local, D->d_sendbuf, D->comm_stream));
         ncclResult_t r = ncclGroupStart();
         for (int32_t q = 0; q < D->n_parts && r == ncclSuccess; ++q) {
@@ -494,6 +515,7 @@ hec_status dist_spmv_launch(hec_dist_s* D, const double* x_local, double* y_loca
         }
         HEC_CUDA_TRY(cudaEventRecord(D->ev_halo, D->comm_stream));
     }
+    NvtxRange ri("hec.interior");
     hec_status st = launch_spmv(D->interior, x_local, nullptr, y_local, s);  // interior rows
     if (st != HEC_OK) return st;
     if (ex) HEC_CUDA_TRY(cudaStreamWaitEvent(s, D->ev_halo, 0));
@@ -532,6 +554,42 @@ hec_status hec_spmv_dist(hec_dist D, const double* x_local, double* y_local, voi
     hec_status st = dist_spmv_launch(D, x_local, y_local, (cudaStream_t)stream);
     if (prev != D->device) cudaSetDevice(prev);
     return st;
+}
+
+hec_status hec_spmv_dist_host(hec_dist D, const double* x_host_local, double* y_host_local, void* stream) {
+    if (!D) return fail(HEC_ERR_ARG, "NULL handle");
+    if (D->local) return fail(HEC_ERR_STATE, "local-emulation handle: use hec_spmv_dist_local");
+    const int32_t n_loc = D->r1 - D->r0;
+    if (n_loc > 0 && (!x_host_local || !y_host_local)) return fail(HEC_ERR_ARG, "NULL host vector");
+    DeviceGuard g(D->device);
+    cudaStream_t s = (cudaStream_t)stream;
+    const size_t nb = sizeof(double) * (size_t)(n_loc > 0 ? n_loc : 1);
+    if (!D->d_stage_x) {
+        HEC_CUDA_TRY(cudaMalloc(&D->d_stage_x, nb));
+        HEC_CUDA_TRY(cudaMalloc(&D->d_stage_y, nb));
+        D->device_bytes += 2 * (int64_t)nb;
+    }
+    if (n_loc > 0)
+        HEC_CUDA_TRY(cudaMemcpyAsync(D->d_stage_x, x_host_local, sizeof(double) * n_loc, cudaMemcpyHostToDevice, s));
+    hec_status st = dist_spmv_launch(D, D->d_stage_x, D->d_stage_y, s);
+    if (st != HEC_OK) return st;
+    if (n_loc > 0)
+        HEC_CUDA_TRY(cudaMemcpyAsync(y_host_local, D->d_stage_y, sizeof(double) * n_loc, cudaMemcpyDeviceToHost, s));
+    HEC_CUDA_TRY(cudaStreamSynchronize(s));
+    return HEC_OK;
+}
+
+hec_status hec_dist_comm_size(hec_dist D, int32_t* nranks, int32_t* version) {
+    if (!D || !nranks || !version) return fail(HEC_ERR_ARG, "NULL argument");
+    int v = 0, c = 0;
+    ncclGetVersion(&v);
+    if (D->comm) {
+        ncclResult_t r = ncclCommCount(D->comm, &c);
+        if (r != ncclSuccess) return nccl_fail(r, "ncclCommCount");
+    }
+    *nranks = c;
+    *version = v;
+    return HEC_OK;
 }
 
 hec_status hec_spmv_dist_local(hec_dist* D, int32_t n, const double* const* x_locals,

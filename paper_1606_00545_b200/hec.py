@@ -84,6 +84,7 @@ EXPORTED = [
     "hec_dist_enable_p2p", "hec_dist_p2p_connect_local", "hec_dist_check",
     "hec_spmv_axpby", "hec_diag", "hec_jacobi", "hec_axpby", "hec_axpbyz", "hec_dot", "hec_norm2", "hec_bicgstab", "hec_cg",
     "hec_bicgstab_dist", "hec_cg_dist", "hec_from_csr_hyb", "hec_reorder_rcm", "hec_permute",
+    "hec_spmv_dist_host", "hec_dist_comm_size",
 ]
 
 
@@ -156,6 +157,10 @@ def load(build: bool = True):
     L.hec_dist_create_local.argtypes = [ctypes.POINTER(CsrT), vp, ctypes.POINTER(OptsT), i32, vp]
     L.hec_spmv_dist.restype = st
     L.hec_spmv_dist.argtypes = [vp, vp, vp, vp]
+    L.hec_spmv_dist_host.restype = st
+    L.hec_spmv_dist_host.argtypes = [vp, vp, vp, vp]
+    L.hec_dist_comm_size.restype = st
+    L.hec_dist_comm_size.argtypes = [vp, ctypes.POINTER(i32), ctypes.POINTER(i32)]
     L.hec_spmv_dist_local.restype = st
     L.hec_spmv_dist_local.argtypes = [vp, i32, vp, vp, vp]
     L.hec_dist_get_info.restype = st
@@ -553,6 +558,21 @@ class Dist:
         _check(_lib.hec_spmv_dist(self._h, _dptr(x_local, self.n_loc, "x_local"),
                                   _dptr(y_local, self.n_loc, "y_local"), _stream_ptr(stream)))
         return y_local
+
+    def spmv_host(self, x_local, y_local=None, stream=None):
+        """COLLECTIVE y_local = (A x)[r0:r1] with HOST buffers (hec_spmv_dist_host):
+        H2D of x_local, the distributed product, D2H of y_local; synchronous."""
+        if y_local is None:
+            y_local = np.empty(self.n_loc, np.float64)
+        _check(_lib.hec_spmv_dist_host(self._h, _hptr(x_local, self.n_loc, "x_local"),
+                                       _hptr(y_local, self.n_loc, "y_local"), _stream_ptr(stream)))
+        return y_local
+
+    def comm_size(self) -> tuple[int, int]:
+        """(ncclCommCount of the handle's communicator or 0, ncclGetVersion)."""
+        n, v = i32(), i32()
+        _check(_lib.hec_dist_comm_size(self._h, ctypes.byref(n), ctypes.byref(v)))
+        return n.value, v.value
 
     def bicgstab(self, b_local, x_local, tol: float = 1e-8, max_it: int = 1000, stream=None) -> SolveInfoT:
         inf = SolveInfoT()
