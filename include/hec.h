@@ -103,7 +103,7 @@ typedef struct {
     int64_t tail_nnz;
     int64_t device_bytes;  /* bytes of device arrays owned by the handle */
     int32_t device;        /* CUDA device ordinal, or -1 for a host-only handle */
-    int32_t reserved;
+    int32_t tail_fused;    /* 1: hec_spmv runs the (small) CSR tail inside the ELL launch */
 } hec_matrix_info;
 
 /* Caller-allocated export buffers, sized from hec_matrix_info:
@@ -226,7 +226,8 @@ void hec_free(hec_matrix A);
 
 /* ---------------------------------------------------------- partitions ---- */
 
-enum { HEC_PART_CONTIG_NNZ = 0, HEC_PART_CONTIG_ROWS = 1, HEC_PART_GRID = 2, HEC_PART_CONTIG_COST = 3 };
+enum { HEC_PART_CONTIG_NNZ = 0, HEC_PART_CONTIG_ROWS = 1, HEC_PART_GRID = 2, HEC_PART_CONTIG_COST = 3,
+       HEC_PART_EXPLICIT = 4 };
 
 typedef struct hec_plan_s* hec_plan;
 
@@ -249,6 +250,9 @@ typedef struct hec_plan_s* hec_plan;
  * sends to peer q = sorted local indices of recv_q inside the part; boundary
  * rows = rows with any off-part column; interior = the rest.  Host-only,
  * deterministic, immutable. */
+/*   HEC_PART_EXPLICIT: grid = part_ptr[n_parts + 1] given by the caller
+ *     (0 = part_ptr[0] < part_ptr[1] < ... < part_ptr[n_parts] = n), e.g. from
+ *     hec_partition_order after B = P A P^T. */
 hec_status hec_partition(const hec_csr* A, int32_t n_parts, int32_t kind, const int32_t* grid,
                          hec_plan* out);
 
@@ -301,6 +305,23 @@ void hec_plan_free(hec_plan P);
  *     val_out[nnz].  Vectors follow with x_new[i] = x[perm[i]].
  * Square A only (HEC_ERR_DIM); perm must be a permutation (HEC_ERR_ARG). */
 hec_status hec_reorder_rcm(const hec_csr* A, int32_t* perm);
+
+/* Partitioning orders for irregular matrices (NEXT-4; the contract of SPEC's
+ * partition_rows, implementation per S:188 -- METIS is out of
+ * reach offline, reading A21).  Graph = pattern of A + A^T without the
+ * diagonal, edge weight = stored entries it stands for (1 or 2).
+ *   HEC_ORDER_BISECT: recursive bisection by BFS level sets from a
+ *     pseudo-peripheral vertex (George-Liu), lowest index first; parts
+ *     balanced by rows (sizes within 1 when n_parts | n on connected graphs).
+ *   HEC_ORDER_MULTILEVEL: multilevel k-way (heavy-edge matching, weighted
+ *     level-set bisection of the coarsest graph, greedy boundary refinement
+ *     at every level); parts balanced by nonzeros within 3%.
+ * Outputs (caller-allocated): perm[n] with perm[new] = old, the parts
+ * contiguous in the new order, and part_ptr[n_parts + 1].  Partition B =
+ * P A P^T (hec_permute) with HEC_PART_EXPLICIT and part_ptr.  Deterministic.
+ * Square A only (HEC_ERR_DIM); 1 <= n_parts <= n (HEC_ERR_PARTS). */
+enum { HEC_ORDER_BISECT = 0, HEC_ORDER_MULTILEVEL = 1 };
+hec_status hec_partition_order(const hec_csr* A, int32_t n_parts, int32_t method, int32_t* perm, int32_t* part_ptr);
 hec_status hec_permute(const hec_csr* A, const int32_t* perm, int32_t* row_ptr_out, int32_t* col_out,
                        double* val_out);
 
@@ -410,6 +431,18 @@ hec_status hec_bicgstab_dist(hec_dist D, const double* b_local, double* x_local,
                              void* stream, hec_solve_info* info);
 hec_status hec_cg_dist(hec_dist D, const double* b_local, double* x_local, double tol, int32_t max_it,
                        void* stream, hec_solve_info* info);
+/* The same two solvers over ALL n ranks of a local emulation
+ * (hec_dist_create_local, handles in rank order) on one device and one
+ * stream: SpMVs are hec_spmv_dist_local; each rank's dot partials are reduced
+ * in its fixed order and the per-rank results summed in rank order (a
+ * stand-in for ncclAllReduce -- one valid order of the same sum), so the
+ * distributed solvers' P > 1 logic runs without P GPUs.  b_locals[p] /
+ * x_locals[p]: rank p's device segments (n_loc(p) doubles); x holds x0 on
+ * entry.  Synchronises `stream`. */
+hec_status hec_bicgstab_dist_local(hec_dist* D, int32_t n, const double* const* b_locals, double* const* x_locals,
+                                   double tol, int32_t max_it, void* stream, hec_solve_info* info);
+hec_status hec_cg_dist_local(hec_dist* D, int32_t n, const double* const* b_locals, double* const* x_locals,
+                             double tol, int32_t max_it, void* stream, hec_solve_info* info);
 void hec_dist_free(hec_dist D);
 
 #ifdef __cplusplus

@@ -30,8 +30,8 @@ static void release(hec_matrix_s* m) {
         cudaGetDevice(&cur);
         cudaSetDevice(m->device);
         if (m->ws && m->ws_free) m->ws_free(m->ws);
-        void* ptrs[] = {m->d_ell_col, m->d_ell_val, m->d_tail_out, m->d_tail_blk,
-                        m->d_tail_ptr, m->d_tail_col, m->d_tail_val, m->d_rowmap, m->d_coo_row, m->d_stage_x,
+        void* ptrs[] = {m->d_ell_col, m->d_ell_val, m->d_tail_out, m->d_tail_blk, m->d_fuse,
+                        m->d_tail_warp, m->d_tail_col, m->d_tail_val, m->d_rowmap, m->d_coo_row, m->d_stage_x,
                         m->d_stage_y};
         for (void* p : ptrs)
             if (p) cudaFree(p);
@@ -48,7 +48,7 @@ static void release(hec_matrix_s* m) {
 // Row chunks (for hec_spmv_host; one chunk for sub-matrices and small
 // matrices), the x prefix each chunk reads, and the tail-kernel work list.
 static void plan_chunks(hec_matrix_s* m, const HostHec& h, bool pipelined, std::vector<int32_t>* order,
-                        std::vector<int4>* blk) {
+                        std::vector<int4>* blk, std::vector<int4>* warp, int64_t* entries) {
     const int32_t n = h.n_rows;
     // ~1M-row chunks, at most 16 (32 chunks measured slower: 3.62 vs 3.41 ms on
     // 256^3; smaller first/last chunks too: 3.36 vs 3.31 ms; the floor is the
@@ -85,20 +85,23 @@ static void plan_chunks(hec_matrix_s* m, const HostHec& h, bool pipelined, std::
     }
     // Tail rows of each chunk (contiguous: tail rows are ascending), cut into
     // super-blocks of kTailSuperRows consecutive tail rows; inside a
-    // super-block the rows are regrouped by lanes-per-row G = 2^lg (stable), and
-    // each CUDA block takes 256/G rows of one group.  Consecutive blocks cover
+    // super-block the rows are sorted by (lanes-per-row G = 2^lg, length),
+    // and each CUDA block takes 256/G rows of one G.  Consecutive blocks cover
     // one super-block, so its entries and x window are still reused in L2
-    // while every group gets a row width that keeps its lanes busy.
+    // while every group gets a row width that keeps its lanes busy; sorting
+    // by length keeps the rows sharing a warp (G < 32) nearly equally long,
+    // so the warp-chunk layout (hec_internal.h) pads little.
     const int32_t tr = (int32_t)h.tail_rows.size();
     const int32_t* tp = h.tail_ptr.data();
     order->assign(tr, 0);
     blk->clear();
+    warp->clear();
+    *entries = 0;
     m->chunk_blk.assign(C + 1, 0);
     // target entries per lane: more entries per lane = more loads in flight per
     // row and fewer rows in flight -- better for big tails (measured r11:
     // power-law 2^23 tail 8 > 4 > 2 > 1), worse for tiny ones (SPE10)
-    int epl = h.tail_col.size() >= ((size_t)1 << 22) ? 8 : 2;
-    if (const char* e = std::getenv("HEC_TAIL_EPL")) epl = std::max(1, std::min(16, std::atoi(e)));
+    const int epl = tail_epl(h.tail_col.size());
     int32_t super = kTailSuperRows;  // HEC_TAIL_SUPER (tuning)
     if (const char* e = std::getenv("HEC_TAIL_SUPER")) super = std::max(256, std::atoi(e));
     int32_t t0 = 0;
@@ -107,20 +110,61 @@ static void plan_chunks(hec_matrix_s* m, const HostHec& h, bool pipelined, std::
         while (t1 < tr && h.tail_rows[t1] < m->chunk_row[c + 1]) ++t1;
         for (int32_t sb = t0; sb < t1; sb += super) {
             const int32_t se = std::min(t1, sb + super);
-            constexpr int NG = kTailMaxLg + 1;
-            int32_t cnt[NG] = {}, pos[NG];
-            for (int32_t t = sb; t < se; ++t) cnt[tail_lg_for(tp[t + 1] - tp[t], epl)]++;
-            pos[0] = sb;
-            for (int g = 1; g < NG; ++g) pos[g] = pos[g - 1] + cnt[g - 1];
-            for (int g = 0; g < NG; ++g) {
-                const int32_t per_blk = 256 >> g;
-                for (int32_t f = pos[g]; f < pos[g] + cnt[g]; f += per_blk)
-                    blk->push_back(make_int4(f, std::min(per_blk, pos[g] + cnt[g] - f), g, 0));
+            for (int32_t t = sb; t < se; ++t) (*order)[t] = t;
+            auto key = [&](int32_t t) {
+                const int32_t L = tp[t + 1] - tp[t];
+                return std::make_pair(tail_lg_for(L, epl), L);
+            };
+            std::stable_sort(order->begin() + sb, order->begin() + se,
+                             [&](int32_t a, int32_t b) { return key(a) < key(b); });
+            for (int32_t f = sb; f < se;) {
+                const int g = key((*order)[f]).first, G = 1 << g, per_blk = 256 >> g;
+                int32_t cnt = 0;
+                while (cnt < per_blk && f + cnt < se && key((*order)[f + cnt]).first == g) ++cnt;
+                blk->push_back(make_int4(f, cnt, g, (int32_t)warp->size()));
+                // the descriptor's 8 warps: thread tid = 32 w + l serves row tid >> g
+                for (int w = 0; w < 8; ++w) {
+                    int32_t iters = 0;
+                    const int32_t r_lo = (32 * w) >> g, r_hi = std::min(cnt, ((32 * w + 31) >> g) + 1);
+                    for (int32_t r = r_lo; r < r_hi; ++r) {
+                        const int32_t t = (*order)[f + r];
+                        iters = std::max(iters, (tp[t + 1] - tp[t] + 2 * G - 1) / (2 * G));
+                    }
+                    warp->push_back(make_int4((int32_t)std::min<int64_t>(*entries, INT32_MAX), iters, f, (cnt << 8) | g));
+                    *entries += (int64_t)iters * kTailChunk;
+                }
+                f += cnt;
             }
-            for (int32_t t = sb; t < se; ++t) (*order)[pos[tail_lg_for(tp[t + 1] - tp[t], epl)]++] = t;
         }
         m->chunk_blk[c + 1] = (int64_t)blk->size();
         t0 = t1;
+    }
+}
+
+// Every stored tail entry's device position in the warp-chunk layout:
+// f(position, index of the entry in the host tail arrays).  Thread tid =
+// 32 w + l of a descriptor serves row tid >> lg as lane lr = tid & (G - 1);
+// in iteration i it reads its row's entries 2 (i G + lr) + e, e = 0, 1, at
+// position base_w + 64 i + 2 l + e.
+template <typename F>
+static void for_each_tail_entry(const std::vector<int4>& blk, const std::vector<int4>& warp,
+                                const std::vector<int32_t>& order, const std::vector<int32_t>& tail_ptr, F f) {
+    for (const int4& d : blk) {
+        const int g = d.z, G = 1 << g;
+        for (int w = 0; w < 8; ++w) {
+            const int4 wm = warp[(size_t)d.w + w];
+            for (int l = 0; l < 32; ++l) {
+                const int tid = 32 * w + l, r = tid >> g, lr = tid & (G - 1);
+                if (r >= d.y) continue;
+                const int32_t t = order[(size_t)d.x + r];
+                const int32_t b = tail_ptr[t], L = tail_ptr[t + 1] - b;
+                for (int32_t i = 0; i < wm.y; ++i)
+                    for (int e = 0; e < 2; ++e) {
+                        const int32_t idx = 2 * (i * G + lr) + e;
+                        if (idx < L) f((int64_t)wm.x + (int64_t)kTailChunk * i + 2 * l + e, b + idx);
+                    }
+            }
+        }
     }
 }
 
@@ -153,8 +197,9 @@ hec_status make_matrix(HostHec&& h, int32_t device, cudaStream_t s, const int32_
     DeviceGuard g(device);
     m->tail_coo = coo_tail;
     std::vector<int32_t> order;
-    std::vector<int4> blk;
-    plan_chunks(m.get(), h, n_loc < 0 && !rowmap && !coo_tail, &order, &blk);
+    std::vector<int4> blk, warp;
+    int64_t entries = 0;
+    plan_chunks(m.get(), h, n_loc < 0 && !rowmap && !coo_tail, &order, &blk, &warp, &entries);
     int64_t bytes = 0;
     hec_status st;
     if ((st = dmalloc_copy(&m->d_ell_col, h.ell_col.data(), h.ell_col.size(), s, &bytes))) return st;
@@ -175,36 +220,87 @@ hec_status make_matrix(HostHec&& h, int32_t device, cudaStream_t s, const int32_
     }
     if ((st = dmalloc_copy(&m->d_ell_val, h.ell_val.data(), h.ell_val.size(), s, &bytes))) return st;
     if (!h.tail_rows.empty()) {
-        // Device copy of the CSR tail in the kernel's order (rows regrouped
-        // inside super-blocks, plan_chunks): a block's rows and their entries
-        // are contiguous, and the kernel needs no indirection.  hec_export
-        // undoes the permutation with m->h_tail_order.
-        // Every row starts at a multiple of kTailVec (rows are padded with
-        // (-1, +0.0) entries, reading A4's convention) so the kernel reads
-        // kTailVec entries per lane as vector index / value loads.
+        // Device copy of the CSR tail in the warp-chunk layout (hec_internal.h):
+        // every entry goes to the position its lane reads it from, gaps are
+        // (-1, +0.0) padding (reading A4).  hec_export walks the same map back.
+        if (entries > INT32_MAX) return fail(HEC_ERR_DIM, "padded CSR tail exceeds int32 positions");
         const size_t tr = h.tail_rows.size();
-        std::vector<int32_t> dptr(tr + 1), dout(tr);
-        int64_t padded = 0;
-        for (size_t t = 0; t < tr; ++t) padded += (h.tail_ptr[t + 1] - h.tail_ptr[t] + kTailVec - 1) / kTailVec * kTailVec;
-        if (padded > INT32_MAX) return fail(HEC_ERR_DIM, "padded CSR tail exceeds int32 positions");
-        std::vector<int32_t> dcol((size_t)padded, -1);
-        std::vector<double> dval((size_t)padded, 0.0);
-        dptr[0] = 0;
-        for (size_t p = 0; p < tr; ++p) {
-            const int32_t t = order[p];
-            const int32_t b = h.tail_ptr[t], e = h.tail_ptr[t + 1];
-            std::copy(h.tail_col.begin() + b, h.tail_col.begin() + e, dcol.begin() + dptr[p]);
-            std::copy(h.tail_val.begin() + b, h.tail_val.begin() + e, dval.begin() + dptr[p]);
-            dptr[p + 1] = dptr[p] + (e - b + kTailVec - 1) / kTailVec * kTailVec;
-            dout[p] = rowmap ? rowmap[h.tail_rows[t]] : row_off + h.tail_rows[t];
-        }
+        std::vector<int32_t> dcol((size_t)entries, -1), dout(tr);
+        std::vector<double> dval((size_t)entries, 0.0);
+        for_each_tail_entry(blk, warp, order, h.tail_ptr, [&](int64_t pos, int32_t k) {
+            dcol[(size_t)pos] = h.tail_col[k];
+            dval[(size_t)pos] = h.tail_val[k];
+        });
+        for (size_t p = 0; p < tr; ++p) dout[p] = rowmap ? rowmap[h.tail_rows[order[p]]] : row_off + h.tail_rows[order[p]];
         m->h_tail_order = order;
+        m->h_tail_ptr = h.tail_ptr;
+        m->h_tail_blk = blk;
+        m->h_tail_warp = warp;
+        m->tail_entries = entries;
         if ((st = dmalloc_copy(&m->d_tail_out, dout.data(), dout.size(), s, &bytes))) return st;
         if ((st = dmalloc_copy(&m->d_tail_blk, blk.data(), blk.size(), s, &bytes))) return st;
-        if ((st = dmalloc_copy(&m->d_tail_ptr, dptr.data(), dptr.size(), s, &bytes))) return st;
+        if ((st = dmalloc_copy(&m->d_tail_warp, warp.data(), warp.size(), s, &bytes))) return st;
         if ((st = dmalloc_copy(&m->d_tail_col, dcol.data(), dcol.size(), s, &bytes))) return st;
         if ((st = dmalloc_copy(&m->d_tail_val, dval.data(), dval.size(), s, &bytes))) return st;
         HEC_CUDA_TRY(cudaStreamSynchronize(s));  // host vectors die after return
+    }
+    // Small tails fused into the ELL launch (one launch per hec_spmv instead of
+    // two): whole matrices only, every ELL CTA one tile of rows (no grid
+    // stride), <= kFuseMaxRowsPerCta tail rows per tile.  HEC_FUSE_TAIL=0
+    // disables; HEC_FUSE_TAIL_MAX = most tail entries fused (default 65536).
+    if (!h.tail_rows.empty() && n_loc < 0 && !rowmap && row_off == 0) {
+        int64_t fmax = 65536;
+        if (const char* e = std::getenv("HEC_FUSE_TAIL_MAX")) fmax = std::atol(e);
+        bool fuse = (int64_t)h.tail_col.size() <= fmax;
+        if (const char* e = std::getenv("HEC_FUSE_TAIL")) fuse = fuse && std::atoi(e) != 0;
+        const int32_t T = 2 * ell_block_threads(h.width);
+        const int64_t n_cta = ((int64_t)h.n_rows + T - 1) / T;
+        if (fuse && n_cta <= ell_grid_cap()) {
+            const size_t tr = h.tail_rows.size();
+            std::vector<int32_t> cta((size_t)n_cta + 1, 0), frow(tr), fptr(tr + 1), flg(tr), fcol;
+            std::vector<double> fval;
+            const int epl = tail_epl(h.tail_col.size());  // as plan_chunks: same lanes per row
+            for (size_t t = 0; t < tr; ++t) {
+                cta[(size_t)(h.tail_rows[t] / T) + 1]++;
+                const int32_t b = h.tail_ptr[t], e = h.tail_ptr[t + 1];
+                frow[t] = h.tail_rows[t];
+                flg[t] = tail_lg_for(e - b, epl);
+                fptr[t] = (int32_t)fcol.size();
+                fcol.insert(fcol.end(), h.tail_col.begin() + b, h.tail_col.begin() + e);
+                fval.insert(fval.end(), h.tail_val.begin() + b, h.tail_val.begin() + e);
+                if ((e - b) & 1) { fcol.push_back(-1); fval.push_back(0.0); }  // rows start even: pair loads
+            }
+            fptr[tr] = (int32_t)fcol.size();
+            int32_t most = 0;
+            for (int64_t c = 0; c < n_cta; ++c) {
+                most = std::max(most, cta[(size_t)c + 1]);
+                cta[(size_t)c + 1] += cta[(size_t)c];
+            }
+            if (most <= kFuseMaxRowsPerCta && !fcol.empty()) {
+                // one allocation: the int32 arrays, the column indices from an
+                // 8-byte boundary (int2 pair loads), the values from a 16-byte
+                // boundary (double2 pair loads)
+                const size_t nmeta = cta.size() + 3 * tr + 1, ocol = (nmeta + 1) & ~(size_t)1;
+                const size_t ni2 = (ocol + fcol.size() + 3) & ~(size_t)3;
+                std::vector<int32_t> buf(ni2 + 2 * fval.size(), 0);
+                size_t o = 0;
+                for (auto* v : {&cta, &frow, &fptr, &flg}) {
+                    std::copy(v->begin(), v->end(), buf.begin() + o);
+                    o += v->size();
+                }
+                std::copy(fcol.begin(), fcol.end(), buf.begin() + ocol);
+                std::memcpy(buf.data() + ni2, fval.data(), fval.size() * sizeof(double));
+                if ((st = dmalloc_copy(&m->d_fuse, buf.data(), buf.size(), s, &bytes))) return st;
+                HEC_CUDA_TRY(cudaStreamSynchronize(s));  // buf dies after this scope
+                m->d_fuse_cta = m->d_fuse;
+                m->d_fuse_row = m->d_fuse_cta + cta.size();
+                m->d_fuse_ptr = m->d_fuse_row + tr;
+                m->d_fuse_lg = m->d_fuse_ptr + tr + 1;
+                m->d_fuse_col = m->d_fuse + ocol;
+                m->d_fuse_val = reinterpret_cast<const double*>(m->d_fuse + ni2);
+                m->fuse_tile = T;
+            }
+        }
     }
     if (rowmap)
         if ((st = dmalloc_copy(&m->d_rowmap, rowmap, (size_t)n_rowmap, s, &bytes))) return st;
@@ -240,6 +336,17 @@ static hec_status launch_chunks(const hec_matrix_s* A, int c, const double* x, c
     e.diag = jd;  // Jacobi epilogue (whole matrix only: c < 0)
     e.b = jb;
     e.omega = omega;
+    // plain whole-matrix product: the small tail rides in the ELL launch
+    const bool fused = A->fuse_tile > 0 && c < 0 && !pw && !jd && alpha == 1.0 && beta == 0.0 && !x_halo &&
+                       A->fuse_tile == 2 * ell_block_threads(A->width);
+    if (fused) {
+        e.fuse_cta = A->d_fuse_cta;
+        e.fuse_row = A->d_fuse_row;
+        e.fuse_ptr = A->d_fuse_ptr;
+        e.fuse_lg = A->d_fuse_lg;
+        e.fuse_col = A->d_fuse_col;
+        e.fuse_val = A->d_fuse_val;
+    }
     if (pw) {  // peer-memory transport: wait for the peers' flags, boundary ELL as its dependent
         cudaError_t we = launch_peer_wait(*pw, s);
         if (we != cudaSuccess) return cuda_fail(we, "peer_wait_kernel launch");
@@ -247,6 +354,7 @@ static hec_status launch_chunks(const hec_matrix_s* A, int c, const double* x, c
     }
     cudaError_t err = launch_ell(e, s);  // Alg. 1 lines 1-3: ELL first
     if (err != cudaSuccess) return cuda_fail(err, "ell_kernel launch");
+    if (fused) return HEC_OK;            // lines 5-7 ran in the same launch
     if (A->tail_coo) {                   // HYB comparison variant: COO remainder
         CooArgs k;
         k.nnz = A->tail_nnz;
@@ -266,10 +374,10 @@ static hec_status launch_chunks(const hec_matrix_s* A, int c, const double* x, c
     if (A->tail_rows > 0 && b1 > b0) {  // Alg. 1 lines 5-7: then the CSR part
         TailArgs t;
         t.blk = A->d_tail_blk;
+        t.warp = A->d_tail_warp;
         t.blk_begin = b0;
         t.blk_end = b1;
         t.out_rows = A->d_tail_out;
-        t.ptr = A->d_tail_ptr;
         t.col = A->d_tail_col;
         t.val = A->d_tail_val;
         t.x = x;
@@ -360,7 +468,7 @@ hec_status hec_info(hec_matrix A, hec_matrix_info* o) {
     o->tail_nnz = A->tail_nnz;
     o->device_bytes = A->device_bytes;
     o->device = A->device;
-    o->reserved = 0;
+    o->tail_fused = A->fuse_tile > 0 ? 1 : 0;
     return HEC_OK;
 }
 
@@ -391,27 +499,17 @@ hec_status hec_export(hec_matrix A, hec_host_arrays* o) {
         if (o->tail_val) HEC_CUDA_TRY(cudaMemcpy(o->tail_val, A->d_tail_val, A->tail_nnz * sizeof(double), cudaMemcpyDeviceToHost));
         return HEC_OK;
     }
-    // the device tail is stored in kernel order (see make_matrix): undo it
-    const size_t tr = (size_t)A->tail_rows;
-    std::vector<int32_t> dptr(tr + 1);
-    HEC_CUDA_TRY(cudaMemcpy(dptr.data(), A->d_tail_ptr, (tr + 1) * sizeof(int32_t), cudaMemcpyDeviceToHost));
-    std::vector<int32_t> dcol((size_t)dptr[tr]);  // padded to even row lengths (make_matrix)
-    std::vector<double> dval((size_t)dptr[tr]);
+    // the device tail is stored in the warp-chunk layout (make_matrix): read it
+    // back and walk the same position map to the host CSR order
+    std::vector<int32_t> dcol((size_t)A->tail_entries);
+    std::vector<double> dval((size_t)A->tail_entries);
     HEC_CUDA_TRY(cudaMemcpy(dcol.data(), A->d_tail_col, dcol.size() * sizeof(int32_t), cudaMemcpyDeviceToHost));
     HEC_CUDA_TRY(cudaMemcpy(dval.data(), A->d_tail_val, dval.size() * sizeof(double), cudaMemcpyDeviceToHost));
-    std::vector<int32_t> where(tr);  // tail row t -> device position
-    for (size_t p = 0; p < tr; ++p) where[A->h_tail_order[p]] = (int32_t)p;
-    int32_t k = 0;
-    for (size_t t = 0; t < tr; ++t) {
-        const int32_t p = where[t], b = dptr[p];
-        int32_t e = dptr[p + 1];
-        while (e > b && dcol[e - 1] < 0) --e;  // drop the padding entries
-        if (o->tail_ptr) o->tail_ptr[t] = k;
-        if (o->tail_col) std::copy(dcol.begin() + b, dcol.begin() + e, o->tail_col + k);
-        if (o->tail_val) std::copy(dval.begin() + b, dval.begin() + e, o->tail_val + k);
-        k += e - b;
-    }
-    if (o->tail_ptr) o->tail_ptr[tr] = k;
+    if (o->tail_ptr) std::memcpy(o->tail_ptr, A->h_tail_ptr.data(), A->h_tail_ptr.size() * sizeof(int32_t));
+    for_each_tail_entry(A->h_tail_blk, A->h_tail_warp, A->h_tail_order, A->h_tail_ptr, [&](int64_t pos, int32_t k) {
+        if (o->tail_col) o->tail_col[k] = dcol[(size_t)pos];
+        if (o->tail_val) o->tail_val[k] = dval[(size_t)pos];
+    });
     return HEC_OK;
 }
 
@@ -564,6 +662,7 @@ hec_status hec_spmv_host(hec_matrix A, const double* x_host, double* y_host, voi
 
 int32_t hec_spmv_launches(hec_matrix A) {
     if (!A || A->n_rows == 0) return 0;
+    if (A->fuse_tile > 0 && A->fuse_tile == 2 * ell_block_threads(A->width)) return 1;
     return 1 + (A->tail_rows > 0 ? 1 : 0);
 }
 

@@ -523,7 +523,59 @@ hec_status dist_spmv_launch(hec_dist_s* D, const double* x_local, double* y_loca
     return st;
 }
 
+// Local emulation of one distributed product over all n ranks on one device
+// and one stream (device current, handles validated by the caller).
+hec_status dist_local_spmv_launch(hec_dist_s** D, int32_t n, const double* const* x_locals,
+                                  double* const* y_locals, cudaStream_t s) {
+    if (D[0]->p2p) {
+        // peer-memory transport emulated on one device and one stream: every
+        // rank's push kernel (stores into the other ranks' windows + flag
+        // release), then every rank's interior rows and flag wait + boundary
+        // rows (the flags are already set, so no wait ever spins)
+        for (int32_t p = 0; p < n; ++p) {
+            const uint64_t ep = ++D[p]->epoch;
+            cudaError_t e = D[p]->nbr.empty() ? cudaSuccess : launch_push(push_args(D[p], x_locals[p], ep), s);
+            if (e != cudaSuccess) return cuda_fail(e, "push kernel");
+        }
+        for (int32_t p = 0; p < n; ++p) {
+            const uint64_t ep = D[p]->epoch;
+            hec_status st = launch_spmv(D[p]->interior, x_locals[p], nullptr, y_locals[p], s);
+            if (st == HEC_OK && D[p]->n_boundary > 0) {
+                st = D[p]->nbr.empty()
+                         ? launch_spmv(D[p]->boundary, x_locals[p], p2p_halo(D[p], ep), y_locals[p], s)
+                         : launch_spmv_peer(D[p]->boundary, x_locals[p], p2p_halo(D[p], ep), y_locals[p], s,
+                                            wait_args(D[p], ep));
+            }
+            if (st != HEC_OK) return st;
+        }
+        return HEC_OK;
+    }
+    for (int32_t p = 0; p < n; ++p) {
+        cudaError_t e = launch_pack(D[p]->d_send_idx, D[p]->n_send, x_locals[p], D[p]->d_sendbuf, s);
+        if (e != cudaSuccess) return cuda_fail(e, "halo pack");
+    }
+    for (int32_t p = 0; p < n; ++p)          // the "exchange": sender p -> receiver q
+        for (int32_t q = 0; q < n; ++q) {
+            const int32_t sc = D[p]->send_off[q + 1] - D[p]->send_off[q];
+            if (sc <= 0) continue;
+            const int32_t rc = D[q]->recv_off[p + 1] - D[q]->recv_off[p];
+            if (rc != sc) return fail(HEC_ERR_STATE, "send/recv count mismatch");
+            cudaError_t e = cudaMemcpyAsync(D[q]->d_x_halo + D[q]->recv_off[p], D[p]->d_sendbuf + D[p]->send_off[q],
+                                            sizeof(double) * sc, cudaMemcpyDeviceToDevice, s);
+            if (e != cudaSuccess) return cuda_fail(e, "local exchange");
+        }
+    for (int32_t p = 0; p < n; ++p) {
+        hec_status st = launch_spmv(D[p]->interior, x_locals[p], nullptr, y_locals[p], s);
+        if (st == HEC_OK && D[p]->n_boundary > 0)
+            st = launch_spmv(D[p]->boundary, x_locals[p], D[p]->d_x_halo, y_locals[p], s);
+        if (st != HEC_OK) return st;
+    }
+    return HEC_OK;
+}
+
 int64_t dist_n_local(hec_dist_s* D) { return (int64_t)D->r1 - D->r0; }
+
+bool dist_is_local(hec_dist_s* D) { return D->local; }
 
 ncclComm_t dist_comm(hec_dist_s* D) { return D->comm; }
 
@@ -598,56 +650,8 @@ hec_status hec_spmv_dist_local(hec_dist* D, int32_t n, const double* const* x_lo
     for (int32_t p = 0; p < n; ++p)
         if (!D[p] || !D[p]->local || D[p]->rank != p || D[p]->n_parts != n)
             return fail(HEC_ERR_STATE, "handles must be the n ranks from hec_dist_create_local");
-    cudaStream_t s = (cudaStream_t)stream;
-    int prev = 0;
-    cudaGetDevice(&prev);
-    cudaSetDevice(D[0]->device);
-    if (D[0]->p2p) {
-        // peer-memory transport emulated on one device and one stream: every
-        // rank's push kernel (stores into the other ranks' windows + flag
-        // release), then every rank's interior rows and flag wait + boundary
-        // rows (the flags are already set, so no wait ever spins)
-        for (int32_t p = 0; p < n; ++p) {
-            const uint64_t ep = ++D[p]->epoch;
-            cudaError_t e = D[p]->nbr.empty() ? cudaSuccess : launch_push(push_args(D[p], x_locals[p], ep), s);
-            if (e != cudaSuccess) { cudaSetDevice(prev); return cuda_fail(e, "push kernel"); }
-        }
-        for (int32_t p = 0; p < n; ++p) {
-            const uint64_t ep = D[p]->epoch;
-            hec_status st = launch_spmv(D[p]->interior, x_locals[p], nullptr, y_locals[p], s);
-            if (st == HEC_OK && D[p]->n_boundary > 0) {
-                st = D[p]->nbr.empty()
-                         ? launch_spmv(D[p]->boundary, x_locals[p], p2p_halo(D[p], ep), y_locals[p], s)
-                         : launch_spmv_peer(D[p]->boundary, x_locals[p], p2p_halo(D[p], ep), y_locals[p], s,
-                                            wait_args(D[p], ep));
-            }
-            if (st != HEC_OK) { cudaSetDevice(prev); return st; }
-        }
-        cudaSetDevice(prev);
-        return HEC_OK;
-    }
-    for (int32_t p = 0; p < n; ++p) {
-        cudaError_t e = launch_pack(D[p]->d_send_idx, D[p]->n_send, x_locals[p], D[p]->d_sendbuf, s);
-        if (e != cudaSuccess) { cudaSetDevice(prev); return cuda_fail(e, "halo pack"); }
-    }
-    for (int32_t p = 0; p < n; ++p)          // the "exchange": sender p -> receiver q
-        for (int32_t q = 0; q < n; ++q) {
-            const int32_t sc = D[p]->send_off[q + 1] - D[p]->send_off[q];
-            if (sc <= 0) continue;
-            const int32_t rc = D[q]->recv_off[p + 1] - D[q]->recv_off[p];
-            if (rc != sc) { cudaSetDevice(prev); return fail(HEC_ERR_STATE, "send/recv count mismatch"); }
-            cudaError_t e = cudaMemcpyAsync(D[q]->d_x_halo + D[q]->recv_off[p], D[p]->d_sendbuf + D[p]->send_off[q],
-                                            sizeof(double) * sc, cudaMemcpyDeviceToDevice, s);
-            if (e != cudaSuccess) { cudaSetDevice(prev); return cuda_fail(e, "local exchange"); }
-        }
-    for (int32_t p = 0; p < n; ++p) {
-        hec_status st = launch_spmv(D[p]->interior, x_locals[p], nullptr, y_locals[p], s);
-        if (st == HEC_OK && D[p]->n_boundary > 0)
-            st = launch_spmv(D[p]->boundary, x_locals[p], D[p]->d_x_halo, y_locals[p], s);
-        if (st != HEC_OK) { cudaSetDevice(prev); return st; }
-    }
-    cudaSetDevice(prev);
-    return HEC_OK;
+    DeviceGuard g(D[0]->device);
+    return dist_local_spmv_launch(D, n, x_locals, y_locals, (cudaStream_t)stream);
 }
 
 hec_status hec_dist_get_info(hec_dist D, hec_dist_info* o) {

@@ -64,13 +64,16 @@ hec_status check_opts(const hec_opts& o);
 int32_t choose_width(const CsrView& A, const hec_opts& o);
 // CSR -> HEC fill with a given width (readings A2-A4, A15).
 hec_status convert(const CsrView& A, int32_t width, int32_t stride_unit, HostHec* out);
-// CSR-tail work unit: at most this many spilled entries start rows owned by
-// one warp (see plan_chunks in api.cpp), so a unit owns <= 256 rows.
-#ifndef HEC_TAIL_VEC
-#define HEC_TAIL_VEC 2  // tail entries per lane load (2: int2/double2; 4: int4 + 2 double2)
-#endif
-constexpr int kTailVec = HEC_TAIL_VEC;  // device tail rows padded to a multiple of this
-static_assert(kTailVec == 2 || kTailVec == 4, "HEC_TAIL_VEC must be 2 or 4");
+// Device layout of the CSR tail ("warp chunks", plan_chunks in api.cpp): the
+// tail rows are cut into super-blocks of consecutive tail rows; inside one
+// they are sorted by (lanes per row G = 2^lg, spilled length) and every CUDA
+// block descriptor takes 256/G rows of one G.  Lane l of warp w of a
+// descriptor reads, in iteration i, the entry pair at base_w + 64 i + 2 l:
+// every warp-wide load is one aligned 256-byte (index) and 512-byte (value)
+// segment, whatever the row lengths.  Padding entries are (-1, +0.0)
+// (reading A4).  A lane's pairs are its row's entries 2(iG + lr), +1 in
+// order, lr = its lane within the row.
+constexpr int kTailChunk = 64;         // entries per warp per iteration (32 lanes x a pair)
 constexpr int kTailSuperRows = 4096;   // tail rows regrouped by length within blocks of this many
 
 // Lanes per tail row: the smallest power of two >= ceil(L / epl), capped at
@@ -78,6 +81,10 @@ constexpr int kTailSuperRows = 4096;   // tail rows regrouped by length within b
 // lives in one warp (shuffle reduction); 64-256 lanes span 2-8 warps of one
 // CTA (shuffle, then the warps' partials combined through shared memory).
 constexpr int kTailMaxLg = 8;
+#ifndef HEC_TAIL_EPL_BIG
+#define HEC_TAIL_EPL_BIG 32  // measured with the batched tail loop: 8 -> 316/335 us, 16 -> 274, 32 -> 262
+#endif
+constexpr int kTailEplBig = HEC_TAIL_EPL_BIG;  // entries per lane for tails of >= 2^22 entries
 inline int tail_max_lg() {             // HEC_TAIL_MAXLG (tuning): 5..8
     static int v = -1;
     if (v < 0) {
@@ -85,6 +92,13 @@ inline int tail_max_lg() {             // HEC_TAIL_MAXLG (tuning): 5..8
         v = e ? std::max(5, std::min(kTailMaxLg, std::atoi(e))) : kTailMaxLg;
     }
     return v;
+}
+// Target entries per lane of the tail kernels for a tail of this many entries
+// (plan_chunks and the fused small-tail map must agree; HEC_TAIL_EPL tunes).
+inline int tail_epl(size_t tail_nnz) {
+    int epl = tail_nnz >= ((size_t)1 << 22) ? kTailEplBig : 2;
+    if (const char* e = std::getenv("HEC_TAIL_EPL")) epl = std::max(1, std::min(64, std::atoi(e)));
+    return epl;
 }
 inline int tail_lg_for(int32_t L, int epl) {
     int lg = 0;
@@ -135,16 +149,19 @@ struct hec_matrix_s {
     int32_t tail_rows = 0;
     bool tail_coo = false;             // HYB comparison variant: the remainder in COO
     int32_t* d_coo_row = nullptr;      // HYB: output row of every remainder entry
-    std::vector<int32_t> h_tail_ptr;   // HYB: tail_ptr kept on the host for hec_export
+    std::vector<int32_t> h_tail_ptr;   // tail_ptr kept on the host for hec_export (both layouts)
     hec::HostHec host;                 // full copy only for host-only handles
     std::vector<int32_t> h_tail_rows;  // local tail row ids (always kept; small)
     // device arrays
     int32_t* d_ell_col = nullptr;
     double* d_ell_val = nullptr;
     int32_t* d_tail_out = nullptr;     // output row of each tail row (after row map)
-    std::vector<int32_t> h_tail_order; // device tail position p holds tail row h_tail_order[p]
+    std::vector<int32_t> h_tail_order; // device tail row position p holds tail row h_tail_order[p]
+    std::vector<int4> h_tail_blk;      // descriptors {first row position, count, lg, first warp}
+    std::vector<int4> h_tail_warp;     // 8 per descriptor: {first entry, iterations, first row, count << 8 | lg}
+    int4* d_tail_warp = nullptr;
+    int64_t tail_entries = 0;          // device tail positions (stored entries + padding)
     int4* d_tail_blk = nullptr;        // per CUDA block: {first position, count, lg, 0}
-    int32_t* d_tail_ptr = nullptr;
     int32_t* d_tail_col = nullptr;
     double* d_tail_val = nullptr;
     int32_t* d_rowmap = nullptr;       // output row of each row, or null (then row_off + i)
@@ -159,6 +176,13 @@ struct hec_matrix_s {
     std::vector<int32_t> chunk_row;    // [n_chunks+1], multiples of 512
     std::vector<int32_t> chunk_xend;   // [n_chunks]: x[0 : xend) needed by rows < chunk_row[c+1]
     std::vector<int64_t> chunk_blk;    // [n_chunks+1]: tail-kernel blocks of each chunk
+    // small tail fused into the ELL launch (plain hec_spmv only; the warp-chunk
+    // tail above stays for the chunked / epilogue paths)
+    int32_t* d_fuse = nullptr;         // one allocation: cta ptr | row | ptr | lg | col, then val
+    const int32_t *d_fuse_cta = nullptr, *d_fuse_row = nullptr, *d_fuse_ptr = nullptr, *d_fuse_lg = nullptr,
+                  *d_fuse_col = nullptr;
+    const double* d_fuse_val = nullptr;
+    int32_t fuse_tile = 0;             // rows per ELL CTA the map was built for (0: not fused)
     cudaStream_t s_h2d = nullptr, s_d2h = nullptr;
     std::vector<cudaEvent_t> ev_x, ev_y;
     cudaEvent_t ev_start = nullptr;
@@ -242,12 +266,22 @@ struct EllArgs {
     const double* b = nullptr;
     double omega = 0.0;
     bool pdl = false;  // launch as a programmatic dependent (peer-memory boundary rows)
+    // small CSR tail fused into this launch (plain y = A x of a whole matrix):
+    // CTA b adds the tail sums of its own rows, tail rows [fuse_cta[b], fuse_cta[b+1])
+    const int32_t* fuse_cta = nullptr;
+    const int32_t* fuse_row = nullptr;  // per fused tail row: output row
+    const int32_t* fuse_ptr = nullptr;  // per fused tail row: first entry (even), [q+1] = end
+    const int32_t* fuse_lg = nullptr;   // per fused tail row: lanes per row G = 2^lg (as the tail kernel)
+    const int32_t* fuse_col = nullptr;
+    const double* fuse_val = nullptr;
 };
+// Fused small tails: at most this many tail rows per CTA tile of the ELL kernel.
+constexpr int kFuseMaxRowsPerCta = 512;
 struct TailArgs {
-    const int4* blk;            // block descriptors {first, count, lg, 0}
+    const int4* blk;            // block descriptors {first row position, count, lg, first warp} (diag)
+    const int4* warp;           // 8 per descriptor: {first entry, iterations, first row, count << 8 | lg}
     int64_t blk_begin, blk_end;
     const int32_t* out_rows;
-    const int32_t* ptr;
     const int32_t* col;
     const double* val;
     const double* x;
@@ -271,11 +305,16 @@ struct CooArgs {               // HYB remainder: row-sorted (row, col, val) trip
 };
 cudaError_t launch_coo(const CooArgs& a, cudaStream_t s);
 cudaError_t launch_ell(const EllArgs& a, cudaStream_t s);
+// Threads per ELL CTA for a width (each thread owns a row pair), and the grid
+// cap beyond which the ELL kernel strides (fused tails need one tile per CTA).
+int ell_block_threads(int32_t width);
+int64_t ell_grid_cap();
 cudaError_t launch_tail(const TailArgs& a, cudaStream_t s);
 cudaError_t launch_ell_tma(const EllArgs& a, cudaStream_t s, int num_sms);
 cudaError_t launch_pack(const int32_t* idx, int32_t n, const double* x, double* out,
                         cudaStream_t s);
-// d[i] = A_ii of a square single-device handle: ELL scan, then the tail (CSR or COO)
+// d[i] = A_ii of a square single-device handle: ELL scan, then the tail (warp
+// chunks or COO)
 cudaError_t launch_diag(const hec_matrix_s* A, double* d, cudaStream_t s);
 cudaError_t launch_push(const PushArgs& a, cudaStream_t s);
 cudaError_t launch_peer_wait(const PeerWait& w, cudaStream_t s);

@@ -199,7 +199,7 @@ __device__ __forceinline__ double jacobi_row(double x, double b, double d, doubl
 }
 
 #ifndef HEC_TAIL_UNROLL
-#define HEC_TAIL_UNROLL 2  // entry pairs per lane unrolled (measured 2 > 4 = 8)
+#define HEC_TAIL_UNROLL 2  // entry-pair iterations per lane unrolled
 #endif
 constexpr int kTailUnroll = HEC_TAIL_UNROLL;
 #ifndef HEC_ELL_PHASE
@@ -230,9 +230,53 @@ __device__ __forceinline__ void ell_phase(const EllArgs& a, const int32_t* cp, c
     }
 }
 
-template <int W, bool HALO, bool ROWMAP, int EPI>
-__global__ void __launch_bounds__(256, EPI == EPI_JACOBI ? HEC_JAC_MINB : 0) ell_kernel(EllArgs a) {
+// One fused tail row (Alg. 1 lines 5-7 for a small tail): the warp computes
+// exactly what tail_kernel's G = 2^lg lanes compute for the row -- lane lr
+// sums entries 2 (i G + lr), +1 in order; G <= 32: the xor tree over G lanes;
+// G > 32: G / 32 virtual warps, each a full-warp tree, added in warp order --
+// so the fused and the two-kernel products are bitwise identical.
+__device__ __forceinline__ double fused_tail_row(const EllArgs& a, int32_t q, int l) {
+    const int lg = __ldg(a.fuse_lg + q), G = 1 << lg;
+    const int32_t kb = __ldg(a.fuse_ptr + q), ke = __ldg(a.fuse_ptr + q + 1);
+    const int nv = G > 32 ? G >> 5 : 1;
+    double total = 0.0;
+    for (int vw = 0; vw < nv; ++vw) {
+        const int lr = G > 32 ? 32 * vw + l : l;
+        double acc = 0.0;
+        if (lr < G) {
+            for (int32_t k = kb + 2 * lr; k < ke; k += 2 * G) {
+                const int2 c = __ldg(reinterpret_cast<const int2*>(a.fuse_col + k));
+                const double2 v = __ldg(reinterpret_cast<const double2*>(a.fuse_val + k));
+                const double x0 = c.x >= 0 ? __ldg(a.x + c.x) : 0.0;
+                const double x1 = c.y >= 0 ? __ldg(a.x + c.y) : 0.0;
+                if (c.x >= 0) acc = fma(v.x, x0, acc);
+                if (c.y >= 0) acc = fma(v.y, x1, acc);
+            }
+        }
+        if (G <= 32) {
+            for (int off = G >> 1; off > 0; off >>= 1) acc += __shfl_xor_sync(0xffffffffu, acc, off, G);
+            return acc;
+        }
+        for (int off = 16; off > 0; off >>= 1) acc += __shfl_xor_sync(0xffffffffu, acc, off);
+        total = vw == 0 ? acc : total + acc;
+    }
+    return total;
+}
+
+// (FUSE: the tail code would lift the kernel to 64 registers; cap it at the
+// plain kernel's occupancy, 5 x 256 threads per SM -- spills land in the
+// cold tail part only)
+template <int W, bool HALO, bool ROWMAP, int EPI, bool FUSE = false>
+__global__ void __launch_bounds__(256, EPI == EPI_JACOBI ? HEC_JAC_MINB : (FUSE ? 5 : 0)) ell_kernel(EllArgs a) {
     constexpr bool AXPBY = EPI == EPI_AXPBY;
+    // FUSE: the CTA's tail-row range is loaded now and used after the ELL rows
+    // (nothing in the ELL stream waits for it)
+    __shared__ double tsum[FUSE ? kFuseMaxRowsPerCta : 1];
+    int32_t q0 = 0, q1 = 0;
+    if constexpr (FUSE) {
+        q0 = __ldg(a.fuse_cta + blockIdx.x);
+        q1 = __ldg(a.fuse_cta + blockIdx.x + 1);
+    }
     // Programmatic dependent launch: the tail kernel may be scheduled once every
     // CTA of this grid has started (it griddepcontrol.waits for this grid's
     // completion before it touches y).  No memory clobber: nothing is ordered
@@ -318,6 +362,23 @@ __global__ void __launch_bounds__(256, EPI == EPI_JACOBI ? HEC_JAC_MINB : 0) ell
             }
         }
     }
+    if constexpr (FUSE) {
+        // the CTA's tail rows (a small tail): one warp per row, then
+        // y_i = ell_i + tail_i, one rounding (as tail_kernel's red.add); the
+        // barrier makes this CTA's y stores and sums visible to its threads
+        if (q1 > q0) {
+            const int l = threadIdx.x & 31;
+            for (int32_t q = q0 + (int32_t)(threadIdx.x >> 5); q < q1; q += (int32_t)(blockDim.x >> 5)) {
+                const double t = fused_tail_row(a, q, l);
+                if (l == 0) tsum[q - q0] = t;
+            }
+            __syncthreads();
+            for (int32_t q = q0 + (int32_t)threadIdx.x; q < q1; q += (int32_t)blockDim.x) {
+                double* yr = a.y + __ldg(a.fuse_row + q);
+                *yr = *yr + tsum[q - q0];
+            }
+        }
+    }
 }
 
 // ------------------------------------------------------------ tail kernel --
@@ -330,52 +391,84 @@ __global__ void __launch_bounds__(256, EPI == EPI_JACOBI ? HEC_JAC_MINB : 0) ell
 // ELL result (this kernel runs after ell_kernel on the same stream).
 // Blocks of one super-block run back to back, so its entries and the x window
 // they touch are reused in L2.  Fixed reduction order: deterministic.
-// One block descriptor's work for the 256 threads tid = 0..255 of a group.
+// One block descriptor's work for the 256 threads tid = 0..255 of the CTA.
+
+// Tail loop variants (measured on power-law 2^23, profiles/round2/tailvar/): 0 = one pair per
+// iteration, unroll 2 (323 us at 8 entries per lane); 3 = value loads predicated on a real index
+// (fewer bytes, slower: 344 us); 4 = each lane issues the index + value loads of HEC_TAIL_BATCH
+// iterations before any gather (batch 8 at 6 CTAs/SM and 32 entries per lane: 262 us)
+#ifndef HEC_TAIL_V
+#define HEC_TAIL_V 4
+#endif
+#ifndef HEC_TAIL_BATCH
+#define HEC_TAIL_BATCH 8  // HEC_TAIL_V 4: iterations whose loads are issued together
+#endif
+
 template <bool HALO, bool JACOBI>
-__device__ __forceinline__ void tail_desc(const TailArgs& a, int4 d, int tid, uint64_t pol) {
-    __shared__ double wsum[8];  // per-warp partials of rows wider than a warp
-    const int lg = d.z;
+__device__ __forceinline__ void tail_desc(const TailArgs& a, int64_t desc, int tid, uint64_t pol, double* wsum) {
+    // one load per warp: {first entry, iterations, first row, count << 8 | lg}
+    // (warp-chunk layout, hec_internal.h) -- no dependent metadata loads
+    // before the stream starts
+    const int4 wm = __ldg(a.warp + desc * 8 + (tid >> 5));
+    const int lg = wm.w & 255;
     const int G = 1 << lg;
     const int lane = tid & (G - 1);
     const int grp = tid >> lg;
     double acc = 0.0;
     double* yp = nullptr;
     int32_t orow = 0;
-    const bool active = grp < d.y;
-    if (active) {
-        const int32_t t = d.x + grp;  // device position: the block's rows are contiguous
-        const int32_t kb = __ldg(a.ptr + t), ke = __ldg(a.ptr + t + 1);
-        if (lane == 0) {
-            orow = __ldg(a.out_rows + t);
-            yp = a.y + orow;
-        }
-        // Entry pairs (kTailVec = 2; or quads): rows start at even positions
-        // and have even (padded) length, so lane l takes entries 2l, 2l+1,
-        // 2l+2G, ... as one 64-bit index and one 128-bit value load.  L1-allocating: the lanes of a
-        // row revisit each 32-byte sector on consecutive iterations.  The
-        // padding entry (-1, +0.0) reads no x and adds nothing.
-#pragma unroll kTailUnroll
-        for (int32_t k = kb + kTailVec * lane; k < ke; k += kTailVec * G) {
-            if constexpr (kTailVec == 2) {
-                const int2 c = ld_l1_i2(a.col + k, pol);
-                const double2 v = ld_l1_d2(a.val + k, pol);
-                const double x0 = gather_x<HALO>(a.x, a.x_halo, a.n_loc, c.x);
-                const double x1 = c.y >= 0 ? gather_x<HALO>(a.x, a.x_halo, a.n_loc, c.y) : 0.0;
-                acc = fma(v.x, x0, acc);
-                if (c.y >= 0) acc = fma(v.y, x1, acc);
-            } else {
-                const int4 c = ld_l1_i4(a.col + k, pol);
-                const double2 v0 = ld_l1_d2(a.val + k, pol), v1 = ld_l1_d2(a.val + k + 2, pol);
-                const double x0 = gather_x<HALO>(a.x, a.x_halo, a.n_loc, c.x);
-                const double x1 = c.y >= 0 ? gather_x<HALO>(a.x, a.x_halo, a.n_loc, c.y) : 0.0;
-                const double x2 = c.z >= 0 ? gather_x<HALO>(a.x, a.x_halo, a.n_loc, c.z) : 0.0;
-                const double x3 = c.w >= 0 ? gather_x<HALO>(a.x, a.x_halo, a.n_loc, c.w) : 0.0;
-                acc = fma(v0.x, x0, acc);
-                if (c.y >= 0) acc = fma(v0.y, x1, acc);
-                if (c.z >= 0) acc = fma(v1.x, x2, acc);
-                if (c.w >= 0) acc = fma(v1.y, x3, acc);
+    const bool active = grp < (wm.w >> 8);
+    if (active && lane == 0) {
+        orow = __ldg(a.out_rows + wm.z + grp);
+        yp = a.y + orow;
+    }
+    {
+        // every warp-wide load is one whole 256-byte (index) / 512-byte (value)
+        // segment, read once: streamed past L1 with the L2 evict-first policy,
+        // so L1 and L2 keep the x gathers.  Padding (-1, +0.0) reads no x and
+        // adds nothing (also for lanes of absent rows: all their pairs pad).
+        const int32_t k0 = wm.x + 2 * (tid & 31), k1 = k0 + kTailChunk * wm.y;
+#if HEC_TAIL_V == 4
+        // all of the lane's index and value loads first (<= HEC_TAIL_BATCH
+        // iterations per batch), then the gathers, then the FMAs in order
+        constexpr int B = HALO ? (HEC_TAIL_BATCH + 1) / 2 : HEC_TAIL_BATCH;  // the halo select costs registers
+        for (int32_t kb = k0; kb < k1; kb += B * kTailChunk) {
+            int2 c[B];
+            double2 v[B];
+#pragma unroll
+            for (int u = 0; u < B; ++u) {
+                const int32_t k = kb + u * kTailChunk;
+                c[u] = k < k1 ? ld_stream_i2(a.col + k, pol) : make_int2(-1, -1);
+                v[u] = k < k1 ? ld_stream_d2(a.val + k, pol) : make_double2(0.0, 0.0);
+            }
+            double xs[2 * B];
+#pragma unroll
+            for (int u = 0; u < B; ++u) {
+                xs[2 * u] = c[u].x >= 0 ? gather_x<HALO>(a.x, a.x_halo, a.n_loc, c[u].x) : 0.0;
+                xs[2 * u + 1] = c[u].y >= 0 ? gather_x<HALO>(a.x, a.x_halo, a.n_loc, c[u].y) : 0.0;
+            }
+#pragma unroll
+            for (int u = 0; u < B; ++u) {
+                if (c[u].x >= 0) acc = fma(v[u].x, xs[2 * u], acc);
+                if (c[u].y >= 0) acc = fma(v[u].y, xs[2 * u + 1], acc);
             }
         }
+#else
+#pragma unroll kTailUnroll
+        for (int32_t k = k0; k < k1; k += kTailChunk) {
+            const int2 c = ld_stream_i2(a.col + k, pol);
+#if HEC_TAIL_V == 3
+            // padding pairs (c.x < 0) read no value bytes
+            const double2 v = c.x >= 0 ? ld_stream_d2(a.val + k, pol) : make_double2(0.0, 0.0);
+#else
+            const double2 v = ld_stream_d2(a.val + k, pol);
+#endif
+            const double x0 = c.x >= 0 ? gather_x<HALO>(a.x, a.x_halo, a.n_loc, c.x) : 0.0;
+            const double x1 = c.y >= 0 ? gather_x<HALO>(a.x, a.x_halo, a.n_loc, c.y) : 0.0;
+            if (c.x >= 0) acc = fma(v.x, x0, acc);
+            if (c.y >= 0) acc = fma(v.y, x1, acc);
+        }
+#endif
     }
     if (lg <= 5) {
         for (int off = G >> 1; off > 0; off >>= 1) acc += __shfl_xor_sync(0xffffffffu, acc, off, G);
@@ -407,13 +500,14 @@ __device__ __forceinline__ void tail_desc(const TailArgs& a, int4 d, int tid, ui
 }
 
 #ifndef HEC_TAIL_MINB
-#define HEC_TAIL_MINB 8  // 8 CTAs (64 warps) per SM: the latency-bound tail wants every warp slot
+#define HEC_TAIL_MINB 6  // CTAs per SM: 6 leaves the batched loads 40 registers (8: 32 regs, 275 us; 4: 277 us)
 #endif
 
 template <bool HALO, bool JACOBI>
 __global__ void __launch_bounds__(256, HEC_TAIL_MINB) tail_kernel(TailArgs a) {
+    __shared__ double wsum[8];  // per-warp partials of rows wider than a warp
     const uint64_t pol = policy_evict_first();
-    tail_desc<HALO, JACOBI>(a, __ldg(a.blk + a.blk_begin + blockIdx.x), threadIdx.x, pol);
+    tail_desc<HALO, JACOBI>(a, a.blk_begin + blockIdx.x, threadIdx.x, pol, wsum);
 }
 
 // ------------------------------------------------------- HYB: COO kernel --
@@ -508,10 +602,12 @@ static int num_sms() {
 // pdl = programmatic dependent launch: the kernel may start while the previous
 // kernel on the stream drains (it must griddepcontrol.wait before consuming).
 template <typename... KArgs, typename... Args>
-static cudaError_t launch_k(void (*kernel)(KArgs...), dim3 g, dim3 b, cudaStream_t s, bool pdl, Args&&... args) {
+static cudaError_t launch_k(void (*kernel)(KArgs...), dim3 g, dim3 b, cudaStream_t s, bool pdl, size_t smem,
+                            Args&&... args) {
     cudaLaunchConfig_t cfg = {};
     cfg.gridDim = g;
     cfg.blockDim = b;
+    cfg.dynamicSmemBytes = smem;
     cfg.stream = s;
     cudaLaunchAttribute attr[1];
     attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
@@ -548,7 +644,10 @@ static int ell_block(int32_t width) {
     return (width > 0 && width <= HEC_ELL_PHASE) ? 128 : 256;
 }
 
-template <bool HALO, bool ROWMAP, int EPI>
+int ell_block_threads(int32_t width) { return ell_block(width); }
+int64_t ell_grid_cap() { return (int64_t)num_sms() * 8 * 64; }
+
+template <bool HALO, bool ROWMAP, int EPI, bool FUSE = false>
 static cudaError_t launch_ell_t(const EllArgs& a, cudaStream_t s) {
     const int64_t n_pairs = ((int64_t)a.n_rows + 1) >> 1;
     const int threads = ell_block(a.width);
@@ -556,17 +655,18 @@ static cudaError_t launch_ell_t(const EllArgs& a, cudaStream_t s) {
     // one row pair per thread, grid-stride only beyond 64 full waves (a
     // persistent grid of 5-40 blocks/SM was measured slower, r15; forcing
     // >= 6 CTAs/SM by a 40-register cap too, pdl run)
-    const int64_t cap = (int64_t)num_sms() * 8 * 64;
+    const int64_t cap = ell_grid_cap();
+    if (FUSE && (blocks > cap || 2 * threads * blocks < a.n_rows)) return cudaErrorInvalidValue;  // planned per tile
     if (blocks > cap) blocks = cap;
     if (blocks < 1) blocks = 1;
     const dim3 g((unsigned)blocks), b(threads);
     switch (a.width) {
 #define HEC_W(w) \
-    case w: return launch_k(ell_kernel<w, HALO, ROWMAP, EPI>, g, b, s, a.pdl, a);
+    case w: return launch_k(ell_kernel<w, HALO, ROWMAP, EPI, FUSE>, g, b, s, a.pdl, 0, a);
         HEC_W(1) HEC_W(2) HEC_W(3) HEC_W(4) HEC_W(5) HEC_W(6) HEC_W(7) HEC_W(8)
         HEC_W(9) HEC_W(10) HEC_W(11) HEC_W(12) HEC_W(13) HEC_W(14) HEC_W(15) HEC_W(16)
 #undef HEC_W
-        default: return launch_k(ell_kernel<0, HALO, ROWMAP, EPI>, g, b, s, a.pdl, a);
+        default: return launch_k(ell_kernel<0, HALO, ROWMAP, EPI, FUSE>, g, b, s, a.pdl, 0, a);
     }
 }
 
@@ -583,7 +683,7 @@ static int ell_variant() {
 
 cudaError_t launch_ell(const EllArgs& a, cudaStream_t s) {
     if (a.n_rows <= 0) return cudaSuccess;
-    if (ell_variant() == 1 && a.alpha == 1.0 && a.beta == 0.0 && !a.diag) {
+    if (ell_variant() == 1 && a.alpha == 1.0 && a.beta == 0.0 && !a.diag && !a.fuse_cta) {
         cudaError_t e = launch_ell_tma(a, s, num_sms());
         if (e != cudaErrorNotSupported) return e;
         cudaGetLastError();  // clear the sticky-free "not supported" status
@@ -598,6 +698,10 @@ cudaError_t launch_ell(const EllArgs& a, cudaStream_t s) {
         if (halo || rowmap) return cudaErrorInvalidValue;
         return launch_ell_t<false, false, EPI_AXPBY>(a, s);
     }
+    if (a.fuse_cta) {  // plain whole-matrix product with its small tail fused in
+        if (halo || rowmap) return cudaErrorInvalidValue;
+        return launch_ell_t<false, false, EPI_NONE, true>(a, s);
+    }
     if (halo) return rowmap ? launch_ell_t<true, true, EPI_NONE>(a, s) : launch_ell_t<true, false, EPI_NONE>(a, s);
     return rowmap ? launch_ell_t<false, true, EPI_NONE>(a, s) : launch_ell_t<false, false, EPI_NONE>(a, s);
 }
@@ -608,9 +712,9 @@ cudaError_t launch_tail(const TailArgs& a, cudaStream_t s) {
     if (blocks > 0x7fffffff) return cudaErrorInvalidValue;
     const bool pdl = tail_pdl();
     if (a.diag && a.x_halo) return cudaErrorInvalidValue;
-    if (a.diag) return launch_k(tail_kernel<false, true>, dim3((unsigned)blocks), dim3(256), s, pdl, a);
-    if (a.x_halo) return launch_k(tail_kernel<true, false>, dim3((unsigned)blocks), dim3(256), s, pdl, a);
-    return launch_k(tail_kernel<false, false>, dim3((unsigned)blocks), dim3(256), s, pdl, a);
+    if (a.diag) return launch_k(tail_kernel<false, true>, dim3((unsigned)blocks), dim3(256), s, pdl, 0, a);
+    if (a.x_halo) return launch_k(tail_kernel<true, false>, dim3((unsigned)blocks), dim3(256), s, pdl, 0, a);
+    return launch_k(tail_kernel<false, false>, dim3((unsigned)blocks), dim3(256), s, pdl, 0, a);
 }
 
 cudaError_t launch_pack(const int32_t* idx, int32_t n, const double* x, double* out,
@@ -636,15 +740,19 @@ __global__ void __launch_bounds__(256) diag_ell_kernel(const int32_t* __restrict
     }
 }
 
-__global__ void __launch_bounds__(256) diag_tail_kernel(const int32_t* __restrict__ out_rows,
-                                                        const int32_t* __restrict__ ptr,
-                                                        const int32_t* __restrict__ col,
-                                                        const double* __restrict__ val, int32_t t_rows,
-                                                        double* __restrict__ d) {
-    for (int32_t t = blockIdx.x * blockDim.x + threadIdx.x; t < t_rows; t += gridDim.x * blockDim.x) {
-        const int32_t r = out_rows[t];
-        for (int32_t k = ptr[t]; k < ptr[t + 1]; ++k)
-            if (col[k] == r) d[r] = val[k];
+// The tail's diagonal entries in the warp-chunk layout: one CTA per
+// descriptor, each lane scans its pairs; at most one entry per row matches,
+// so every d[row] has a single writer (after diag_ell_kernel, stream order).
+__global__ void __launch_bounds__(256) diag_tail_kernel(TailArgs a, double* __restrict__ d) {
+    const int tid = threadIdx.x;
+    const int4 wm = __ldg(a.warp + (int64_t)blockIdx.x * 8 + (tid >> 5));
+    const int grp = tid >> (wm.w & 255);
+    if (grp >= (wm.w >> 8)) return;
+    const int32_t r = __ldg(a.out_rows + wm.z + grp);
+    for (int32_t i = 0; i < wm.y; ++i) {
+        const int64_t k = wm.x + (int64_t)kTailChunk * i + 2 * (tid & 31);
+        if (a.col[k] == r) d[r] = a.val[k];
+        if (a.col[k + 1] == r) d[r] = a.val[k + 1];
     }
 }
 
@@ -713,9 +821,15 @@ cudaError_t launch_diag(const hec_matrix_s* A, double* d, cudaStream_t s) {
                                                     A->d_ell_col ? A->width : 0, A->n_rows, d);
     if (A->tail_rows > 0 && A->tail_coo)
         diag_coo_kernel<<<grid(A->tail_nnz), 256, 0, s>>>(A->d_coo_row, A->d_tail_col, A->d_tail_val, A->tail_nnz, d);
-    else if (A->tail_rows > 0)
-        diag_tail_kernel<<<grid(A->tail_rows), 256, 0, s>>>(A->d_tail_out, A->d_tail_ptr, A->d_tail_col,
-                                                            A->d_tail_val, A->tail_rows, d);
+    else if (A->tail_rows > 0 && !A->h_tail_blk.empty()) {
+        TailArgs t = {};
+        t.blk = A->d_tail_blk;
+        t.warp = A->d_tail_warp;
+        t.out_rows = A->d_tail_out;
+        t.col = A->d_tail_col;
+        t.val = A->d_tail_val;
+        diag_tail_kernel<<<(unsigned)A->h_tail_blk.size(), 256, 0, s>>>(t, d);
+    }
     return cudaGetLastError();
 }
 

@@ -292,6 +292,24 @@ __global__ void step_kernel(double* sc, int mode, double tol, int first) {
     step_body(sc, mode, tol, first);
 }
 
+// Local emulation of the all-reduce (hec_*_dist_local): every rank's reduced
+// dots summed in rank order and written back to every rank's scalars -- one
+// valid order of the sum ncclAllReduce computes across the ranks.
+__global__ void local_allreduce_kernel(double* const* scs, int R, int n_dots) {
+    if (threadIdx.x != 0 || blockIdx.x != 0) return;
+    for (int k = 0; k < n_dots; ++k) {
+        double v = 0.0;
+        for (int r = 0; r < R; ++r) v += scs[r][SC_D0 + k];
+        for (int r = 0; r < R; ++r) scs[r][SC_D0 + k] = v;
+    }
+}
+
+// The scalar step on every rank's scalars (identical inputs, identical results).
+__global__ void step_all_kernel(double* const* scs, int R, int mode, double tol, int first) {
+    const int r = threadIdx.x;
+    if (blockIdx.x == 0 && r < R) step_body(scs[r], mode, tol, first);
+}
+
 // ------------------------------------------------------------------ host --
 // The operator a solve runs on: one matrix, or this rank of a distributed one.
 struct Op {
@@ -299,9 +317,16 @@ struct Op {
     hec_dist_s* D = nullptr;
     int64_t n = 0;
     ncclComm_t comm = nullptr;  // non-null: dots are all-reduced across ranks
+    // local emulation (hec_*_dist_local): all R ranks on one device, this Op
+    // is rank 0's; the others are solved alongside (Solver::sub)
+    hec_dist_s** Dl = nullptr;
+    int32_t R = 1;
 };
 
 hec_status dist_spmv_launch(hec_dist_s* D, const double* x, double* y, cudaStream_t s);   // dist.cpp
+hec_status dist_local_spmv_launch(hec_dist_s** D, int32_t n, const double* const* xs, double* const* ys,
+                                  cudaStream_t s);
+bool dist_is_local(hec_dist_s* D);
 int64_t dist_n_local(hec_dist_s* D);
 ncclComm_t dist_comm(hec_dist_s* D);
 int32_t dist_parts(hec_dist_s* D);
@@ -397,6 +422,49 @@ struct Solver {
     SolverWs* ws = nullptr;
     std::unique_ptr<SolverWs> own;        // private workspace (cached one busy)
     std::unique_lock<std::mutex> lock;
+    // local emulation: one sub-solver (workspace) per rank r >= 1; tab[r] maps
+    // rank 0's vectors {b, x, workspace...} to rank r's, so the algorithm
+    // below is written once against rank 0's pointers
+    std::vector<std::unique_ptr<Solver>> sub;
+    std::vector<std::vector<const double*>> tab;
+    std::vector<int64_t> n_r;
+    double** d_scs = nullptr;
+    ~Solver() { if (d_scs) cudaFree(d_scs); }
+
+    // rank 0 pointer -> rank r pointer (null stays null)
+    const double* tr(const double* p, int r) const {
+        if (!p || r == 0) return p;
+        for (size_t i = 0; i < tab[0].size(); ++i)
+            if (tab[0][i] == p) return tab[r][i];
+        return nullptr;  // not a solver vector: a bug; the launch fails on null
+    }
+    hec_status init_group(const double* const* bs, double* const* xs) {
+        const int R = op.R;
+        tab.assign(R, {});
+        n_r.assign(R, 0);
+        std::vector<double*> scs(R);
+        for (int r = 0; r < R; ++r) {
+            Solver* S = this;
+            if (r > 0) {
+                sub.emplace_back(new Solver());
+                S = sub.back().get();
+                S->op.D = op.Dl[r];
+                S->op.n = dist_n_local(op.Dl[r]);
+                S->s = s;
+                S->tol = tol;
+                HEC_TRY(S->init());
+            }
+            n_r[r] = r == 0 ? op.n : S->op.n;
+            tab[r].push_back(bs[r]);
+            tab[r].push_back(xs[r]);
+            for (double* v : S->vecs) tab[r].push_back(v);
+            scs[r] = S->sc;
+        }
+        HEC_CUDA_TRY(cudaMalloc(&d_scs, R * sizeof(double*)));
+        HEC_CUDA_TRY(cudaMemcpyAsync(d_scs, scs.data(), R * sizeof(double*), cudaMemcpyHostToDevice, s));
+        return HEC_OK;
+    }
+    Solver* rank(int r) { return r == 0 ? this : sub[r - 1].get(); }
 
     hec_status init() {
         void** slot;
@@ -427,13 +495,53 @@ struct Solver {
     }
     hec_status spmv(const double* x, double* y) {
         if (op.A) return launch_spmv(op.A, x, nullptr, y, s);
+        if (op.R > 1) {
+            std::vector<const double*> xs(op.R);
+            std::vector<double*> ys(op.R);
+            for (int r = 0; r < op.R; ++r) {
+                xs[r] = tr(x, r);
+                ys[r] = const_cast<double*>(tr(y, r));
+            }
+            return dist_local_spmv_launch(op.Dl, op.R, xs.data(), ys.data(), s);
+        }
+        if (dist_is_local(op.D)) return dist_local_spmv_launch(&op.D, 1, &x, &y, s);
         return dist_spmv_launch(op.D, x, y, s);
+    }
+    // local emulation: the pass on every rank, per-rank reduce, the rank-order
+    // all-reduce stand-in, then the step on every rank's scalars
+    hec_status pass_group(int vop, const VecArgs& a0, int n_dots, int mode, int first) {
+        for (int r = 0; r < op.R; ++r) {
+            Solver* S = rank(r);
+            VecArgs a = a0;
+            a.x = const_cast<double*>(tr(a0.x, r)); a.r = const_cast<double*>(tr(a0.r, r));
+            a.r0 = const_cast<double*>(tr(a0.r0, r)); a.p = const_cast<double*>(tr(a0.p, r));
+            a.v = const_cast<double*>(tr(a0.v, r)); a.s = const_cast<double*>(tr(a0.s, r));
+            a.t = const_cast<double*>(tr(a0.t, r)); a.b = const_cast<double*>(tr(a0.b, r));
+            a.a1 = tr(a0.a1, r); a.b1 = tr(a0.b1, r); a.c1 = tr(a0.c1, r); a.d1 = tr(a0.d1, r);
+            a.n = n_r[r];
+            a.sc = S->sc;
+            a.part = n_dots > 0 ? S->part : nullptr;
+            a.ctr = nullptr;
+            a.vec2 = aligned16(a);
+            HEC_CUDA_TRY(launch_vec_op(vop, a, s));
+            if (n_dots > 0) {
+                reduce_kernel<<<1, kRedThreads, 0, s>>>(S->part, n_dots, S->sc);
+                HEC_CUDA_TRY(cudaGetLastError());
+            }
+        }
+        if (n_dots > 0) {
+            local_allreduce_kernel<<<1, 32, 0, s>>>(d_scs, op.R, n_dots);
+            HEC_CUDA_TRY(cudaGetLastError());
+        }
+        if (mode >= 0) HEC_TRY(step(mode, first));
+        return HEC_OK;
     }
     // One vector pass; n_dots > 0: its dots land in SC_D0.. (all-reduced across
     // ranks); then the scalar step `mode` (-1: none).  One GPU: a single launch
     // (the pass's last CTA reduces and steps).  Distributed: pass, reduce,
     // ncclAllReduce, step kernel.
     hec_status pass(int vop, VecArgs a, int n_dots, int mode = -1, int first = 0) {
+        if (op.R > 1) return pass_group(vop, a, n_dots, mode, first);
         a.n = op.n;
         a.sc = sc;
         a.part = n_dots > 0 ? part : nullptr;
@@ -458,6 +566,11 @@ struct Solver {
         return HEC_OK;
     }
     hec_status step(int mode, int first = 0) {
+        if (op.R > 1) {
+            step_all_kernel<<<1, 32 * ((op.R + 31) / 32), 0, s>>>(d_scs, op.R, mode, tol, first);
+            HEC_CUDA_TRY(cudaGetLastError());
+            return HEC_OK;
+        }
         step_kernel<<<1, 32, 0, s>>>(sc, mode, tol, first);
         HEC_CUDA_TRY(cudaGetLastError());
         return HEC_OK;
@@ -541,7 +654,7 @@ static hec_status cg(Solver& S, const double* b, double* x, int32_t max_it, hec_
 }
 
 static hec_status solve(Op op, int method, const double* b, double* x, double tol, int32_t max_it, void* stream,
-                        hec_solve_info* info) {
+                        hec_solve_info* info, const double* const* bs = nullptr, double* const* xs = nullptr) {
     if (!info || (op.n > 0 && (!b || !x))) return fail(HEC_ERR_ARG, "NULL argument");
     if (!(tol >= 0) || max_it < 0) return fail(HEC_ERR_ARG, "negative tol or max_it");
     std::memset(info, 0, sizeof(*info));
@@ -551,11 +664,13 @@ static hec_status solve(Op op, int method, const double* b, double* x, double to
     S.s = (cudaStream_t)stream;
     S.tol = tol;
     HEC_TRY(S.init());
+    if (op.R > 1) HEC_TRY(S.init_group(bs, xs));
     hec_status st = method == 0 ? bicgstab(S, b, x, max_it, info) : cg(S, b, x, max_it, info);
     if (st == HEC_OK) HEC_CUDA_TRY(cudaStreamSynchronize(S.s));
     // peer-memory transport: a halo wait that timed out leaves boundary rows
     // computed from stale data -- report it instead of a converged solve
     if (st == HEC_OK && op.D) st = dist_err(op.D);
+    for (int r = 1; r < op.R && st == HEC_OK; ++r) st = dist_err(op.Dl[r]);
     return st;
 }
 
@@ -653,6 +768,33 @@ hec_status hec_bicgstab_dist(hec_dist D, const double* b_local, double* x_local,
     if (dist_parts(D) > 1 && !op.comm)
         return fail(HEC_ERR_STATE, "distributed solvers need the NCCL communicator of hec_dist_create");
     return solve(op, 0, b_local, x_local, tol, max_it, stream, info);
+}
+
+static hec_status dist_local_solve(int method, hec_dist* D, int32_t n, const double* const* b_locals,
+                                   double* const* x_locals, double tol, int32_t max_it, void* stream,
+                                   hec_solve_info* info) {
+    if (!D || n < 1 || !b_locals || !x_locals) return fail(HEC_ERR_ARG, "NULL argument");
+    for (int32_t p = 0; p < n; ++p) {
+        if (!D[p] || !dist_is_local(D[p]) || dist_parts(D[p]) != n)
+            return fail(HEC_ERR_STATE, "handles must be the n ranks from hec_dist_create_local, in rank order");
+        if (dist_n_local(D[p]) > 0 && (!b_locals[p] || !x_locals[p])) return fail(HEC_ERR_ARG, "NULL segment");
+    }
+    Op op;
+    op.D = D[0];
+    op.n = dist_n_local(D[0]);
+    op.Dl = D;
+    op.R = n;
+    return solve(op, method, b_locals[0], x_locals[0], tol, max_it, stream, info, b_locals, x_locals);
+}
+
+hec_status hec_bicgstab_dist_local(hec_dist* D, int32_t n, const double* const* b_locals, double* const* x_locals,
+                                   double tol, int32_t max_it, void* stream, hec_solve_info* info) {
+    return dist_local_solve(0, D, n, b_locals, x_locals, tol, max_it, stream, info);
+}
+
+hec_status hec_cg_dist_local(hec_dist* D, int32_t n, const double* const* b_locals, double* const* x_locals,
+                             double tol, int32_t max_it, void* stream, hec_solve_info* info) {
+    return dist_local_solve(1, D, n, b_locals, x_locals, tol, max_it, stream, info);
 }
 
 hec_status hec_cg_dist(hec_dist D, const double* b_local, double* x_local, double tol, int32_t max_it,

@@ -83,6 +83,13 @@ static hec_status make_part_ptr(const CsrView& A, int32_t P, int32_t kind, const
             cur.swap(nxt);
         }
         *pp = cur;
+    } else if (kind == HEC_PART_EXPLICIT) {
+        if (!grid) return fail(HEC_ERR_ARG, "EXPLICIT partition needs part_ptr");
+        if (grid[0] != 0 || grid[P] != n) return fail(HEC_ERR_PARTS, "part_ptr must run from 0 to n_rows");
+        for (int32_t p = 0; p < P; ++p) {
+            if (grid[p + 1] <= grid[p]) return fail(HEC_ERR_PARTS, "part_ptr must be strictly increasing");
+            (*pp)[p] = grid[p];
+        }
     } else {
         return fail(HEC_ERR_ARG, "unknown partition kind");
     }

@@ -28,7 +28,8 @@ class HecError(RuntimeError):
 STATUS = {0: "HEC_OK", 1: "HEC_ERR_ARG", 2: "HEC_ERR_FORMAT", 3: "HEC_ERR_DIM", 4: "HEC_ERR_PARTS",
           5: "HEC_ERR_CUDA", 6: "HEC_ERR_NCCL", 7: "HEC_ERR_NOMEM", 8: "HEC_ERR_STATE", 9: "HEC_ERR_NODEV"}
 WIDTH_BG3, WIDTH_CAP, WIDTH_FIXED = 0, 1, 2
-PART_CONTIG_NNZ, PART_CONTIG_ROWS, PART_GRID, PART_CONTIG_COST = 0, 1, 2, 3
+PART_CONTIG_NNZ, PART_CONTIG_ROWS, PART_GRID, PART_CONTIG_COST, PART_EXPLICIT = 0, 1, 2, 3, 4
+ORDER_BISECT, ORDER_MULTILEVEL = 0, 1
 SUB_INTERIOR, SUB_BOUNDARY, SUB_ALL = 0, 1, 2
 NCCL_ID_BYTES = 128
 IPC_BYTES = 64
@@ -48,7 +49,7 @@ class OptsT(ctypes.Structure):
 class MatrixInfoT(ctypes.Structure):
     _fields_ = [("n_rows", i32), ("n_cols", i32), ("ell_width", i32), ("ell_stride", i32),
                 ("nnz", i64), ("ell_nnz", i64), ("tail_rows", i32), ("tail_group", i32),
-                ("tail_nnz", i64), ("device_bytes", i64), ("device", i32), ("reserved", i32)]
+                ("tail_nnz", i64), ("device_bytes", i64), ("device", i32), ("tail_fused", i32)]
 
 
 class HostArraysT(ctypes.Structure):
@@ -84,7 +85,8 @@ EXPORTED = [
     "hec_dist_enable_p2p", "hec_dist_p2p_connect_local", "hec_dist_check",
     "hec_spmv_axpby", "hec_diag", "hec_jacobi", "hec_axpby", "hec_axpbyz", "hec_dot", "hec_norm2", "hec_bicgstab", "hec_cg",
     "hec_bicgstab_dist", "hec_cg_dist", "hec_from_csr_hyb", "hec_reorder_rcm", "hec_permute",
-    "hec_spmv_dist_host", "hec_dist_comm_size",
+    "hec_spmv_dist_host", "hec_dist_comm_size", "hec_bicgstab_dist_local", "hec_cg_dist_local",
+    "hec_partition_order",
 ]
 
 
@@ -194,11 +196,16 @@ def load(build: bool = True):
     L.hec_norm2.argtypes = [i64, vp, ctypes.POINTER(dbl), vp]
     L.hec_reorder_rcm.restype = st
     L.hec_reorder_rcm.argtypes = [ctypes.POINTER(CsrT), vp]
+    L.hec_partition_order.restype = st
+    L.hec_partition_order.argtypes = [ctypes.POINTER(CsrT), i32, i32, vp, vp]
     L.hec_permute.restype = st
     L.hec_permute.argtypes = [ctypes.POINTER(CsrT), vp, vp, vp, vp]
     for f in (L.hec_bicgstab, L.hec_cg, L.hec_bicgstab_dist, L.hec_cg_dist):
         f.restype = st
         f.argtypes = [vp, vp, vp, dbl, i32, vp, ctypes.POINTER(SolveInfoT)]
+    for f in (L.hec_bicgstab_dist_local, L.hec_cg_dist_local):
+        f.restype = st
+        f.argtypes = [vp, i32, vp, vp, dbl, i32, vp, ctypes.POINTER(SolveInfoT)]
     _lib = L
     return L
 
@@ -427,7 +434,7 @@ class Plan:
         L = load()
         self._h = vp()
         args = _CsrArgs(A)
-        g = (ctypes.c_int32 * 3)(*grid) if grid is not None else None
+        g = (ctypes.c_int32 * len(grid))(*[int(v) for v in grid]) if grid is not None else None
         _check(L.hec_partition(args.ref(), n_parts, kind, ctypes.cast(g, vp) if g is not None else None,
                                ctypes.byref(self._h)))
         self.n_parts = n_parts
@@ -624,6 +631,22 @@ class LocalDistGroup:
         _check(_lib.hec_spmv_dist_local(self._arr, n, xs, ys, _stream_ptr(stream)))
         return y_locals
 
+    def _solve(self, fn, b_locals, x_locals, tol, max_it, stream):
+        n = len(self.ranks)
+        bs = (vp * n)(*[_dptr(b_locals[p], self.ranks[p].n_loc, "b_local") for p in range(n)])
+        xs = (vp * n)(*[_dptr(x_locals[p], self.ranks[p].n_loc, "x_local") for p in range(n)])
+        inf = SolveInfoT()
+        _check(fn(self._arr, n, bs, xs, float(tol), int(max_it), _stream_ptr(stream), ctypes.byref(inf)))
+        return inf
+
+    def bicgstab(self, b_locals, x_locals, tol: float = 1e-8, max_it: int = 1000, stream=None) -> SolveInfoT:
+        """Alg. 4 over all emulated ranks (hec_bicgstab_dist_local)."""
+        return self._solve(_lib.hec_bicgstab_dist_local, b_locals, x_locals, tol, max_it, stream)
+
+    def cg(self, b_locals, x_locals, tol: float = 1e-8, max_it: int = 1000, stream=None) -> SolveInfoT:
+        """CG over all emulated ranks (hec_cg_dist_local)."""
+        return self._solve(_lib.hec_cg_dist_local, b_locals, x_locals, tol, max_it, stream)
+
     def free(self):
         for r in self.ranks:
             r.free()
@@ -636,6 +659,19 @@ def reorder_rcm(A) -> np.ndarray:
     perm = np.empty(A.n_rows, np.int32)
     _check(_lib.hec_reorder_rcm(args.ref(), _p(perm)))
     return perm
+
+
+def partition_order(A, n_parts: int, method: int = ORDER_MULTILEVEL) -> tuple[np.ndarray, np.ndarray]:
+    """(perm, part_ptr): a partitioning order (perm[new] = old, parts contiguous
+    in the new order) by level-set recursive bisection or the multilevel
+    partitioner (hec_partition_order).  Use with permute() and
+    partition(B, n_parts, PART_EXPLICIT, part_ptr)."""
+    load()
+    args = _CsrArgs(A)
+    perm = np.empty(A.n_rows, np.int32)
+    pp = np.empty(n_parts + 1, np.int32)
+    _check(_lib.hec_partition_order(args.ref(), int(n_parts), int(method), _p(perm), _p(pp)))
+    return perm, pp
 
 
 def permute(A, perm: np.ndarray):

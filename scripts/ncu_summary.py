@@ -80,7 +80,12 @@ def main():
         kern[kname.split("<")[0]] = {"dram_bytes_per_launch": round(sum(vals) / len(vals)), "kernel": kname,
                                      "source": os.path.relpath(out, os.path.dirname(tj))}
         # a step launches each of these kernels once: its traffic is their sum
-        ent = {"dram_bytes_per_step": sum(k["dram_bytes_per_launch"] for k in kern.values()), "kernels": kern}
+        # keyed by the native sources the capture was taken with: bench.py
+        # reports it only while csrc/ + include/ still hash to this value
+        sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
+        from bench import csrc_hash
+        ent = {"dram_bytes_per_step": sum(k["dram_bytes_per_launch"] for k in kern.values()), "kernels": kern,
+               "csrc_sha": csrc_hash()}
         cur[config] = ent
         json.dump(cur, open(tj, "w"), indent=1)
     print("\n".join(lines))

@@ -190,3 +190,61 @@ def test_dist_solvers_single_rank_equal_single_gpu_bitwise():
         i2 = getattr(D, method)(dev(b), x2, 1e-9, 500)
         assert (i1.iterations, i1.converged) == (i2.iterations, i2.converged)
         assert x1.cpu().numpy().tobytes() == x2.cpu().numpy().tobytes()
+
+
+def _group_solve(A, b, P, kind, method, tol, max_it, grid=None, p2p=False):
+    plan = hec.partition(A, P, kind, grid)
+    grp = hec.LocalDistGroup(A, plan, 0, None, p2p=p2p)
+    pp = plan.part_ptr()
+    bs = [dev(b[pp[p]:pp[p + 1]]) for p in range(P)]
+    xs = [torch.zeros(int(pp[p + 1] - pp[p]), dtype=torch.float64, device="cuda") for p in range(P)]
+    info = getattr(grp, method)(bs, xs, tol, max_it)
+    x = np.concatenate([t.cpu().numpy() for t in xs])
+    grp.free()
+    return info, x
+
+
+@pytest.mark.parametrize("P", [2, 4, 8])
+@pytest.mark.parametrize("p2p", [False, True])
+def test_cg_dist_p_ranks_emulated_matches_oracle(P, p2p):
+    # hec_cg_dist's P > 1 logic (per-rank passes, the all-reduce of the dots,
+    # identical scalar steps on every rank, hec_spmv_dist's exchange) on one
+    # GPU: iteration count within +-1 of the oracle, its solution, a true
+    # residual at the tolerance (SURVEY §8(f) NEXT-1 pins)
+    A = hecgen.poisson3d(24, 20, 16)
+    b = hecgen.vector(A.n_rows, "uniform", seed=21)
+    ref = K.cg(A, b, np.zeros(A.n_rows), 1e-10, 1000)
+    info, x = _group_solve(A, b, P, hec.PART_GRID, "cg", 1e-10, 1000, grid=(24, 20, 16), p2p=p2p)
+    assert info.converged and ref.converged and info.breakdown == 0
+    assert abs(info.iterations - ref.iterations) <= 1, (info.iterations, ref.iterations)
+    assert np.linalg.norm(x - ref.x) <= 1e-8 * np.linalg.norm(ref.x)
+    true_rel = np.linalg.norm(b - oracle.csr_spmv(A, x)) / np.linalg.norm(b)
+    assert true_rel <= 2e-10 and abs(true_rel - info.rel_residual) <= 1e-11
+
+
+@pytest.mark.parametrize("P", [4, 8])
+def test_bicgstab_dist_p_ranks_emulated_matches_oracle(P):
+    A = hecgen.powerlaw(20000, seed=3)
+    b = hecgen.vector(A.n_rows, "uniform", seed=12)
+    traj = K.bicgstab(A, b, np.zeros(A.n_rows), 1e-30, 10).history
+    for k, rel in ((1, 1e-12), (5, 1e-12), (10, 1e-10)):
+        info, _ = _group_solve(A, b, P, hec.PART_CONTIG_NNZ, "bicgstab", 1e-30, k)
+        assert info.iterations == k
+        assert abs(info.rel_residual - traj[k]) <= rel * traj[k], (k, info.rel_residual, traj[k])
+    ref = K.bicgstab(A, b, np.zeros(A.n_rows), 1e-10, 2000)
+    info, x = _group_solve(A, b, P, hec.PART_CONTIG_NNZ, "bicgstab", 1e-10, 2000, p2p=True)
+    assert info.converged == ref.converged == 1 and info.breakdown == 0
+    assert np.linalg.norm(b - oracle.csr_spmv(A, x)) / np.linalg.norm(b) <= 5e-10
+    assert np.linalg.norm(x - ref.x) <= 1e-7 * np.linalg.norm(ref.x)
+
+
+def test_dist_local_single_rank_equals_single_gpu_bitwise():
+    A = hecgen.poisson3d(16, 16, 12)
+    b = hecgen.vector(A.n_rows, "uniform", seed=13)
+    M = hec.from_csr(A)
+    for method in ("cg", "bicgstab"):
+        x1 = torch.zeros(A.n_rows, dtype=torch.float64, device="cuda")
+        i1 = getattr(M, method)(dev(b), x1, 1e-9, 500)
+        i2, x2 = _group_solve(A, b, 1, hec.PART_CONTIG_NNZ, method, 1e-9, 500)
+        assert (i1.iterations, i1.converged) == (i2.iterations, i2.converged)
+        assert x1.cpu().numpy().tobytes() == x2.tobytes()

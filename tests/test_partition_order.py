@@ -1,0 +1,143 @@
+"""NEXT-4 partitioning orders (hec_partition_order; SPEC's partition_rows
+contract; "quasi-optimal partition" with
+METIS, reading A21) and the EXPLICIT row partition they feed.
+
+These are heuristics, so they are pinned by the properties that define them:
+SPEC's worked examples (tridiagonal 4 parts of 25 with 6 off-block entries;
+Poisson 20^3 into 8 parts within 1 of 1000 rows; identity for one part),
+row balance of the level-set bisection, nonzero balance of the multilevel
+partitioner, valid permutations, determinism, and the halo against the
+natural order and a scrambled order of the same matrix."""
+import numpy as np
+import pytest
+
+import hecgen
+import oracle
+import paper_1606_00545_b200 as hec
+from oracle import plan_ref as PR
+
+
+def halo(A, P, kind=hec.PART_CONTIG_NNZ, pp=None):
+    plan = hec.partition(A, P, kind, pp)
+    return sum(plan.part_info(p).n_halo for p in range(P))
+
+
+def off_block_nnz(B, pp):
+    owner = np.searchsorted(pp, np.arange(B.n_rows), side="right") - 1
+    rows = np.repeat(np.arange(B.n_rows), np.diff(B.row_ptr))
+    return int(np.count_nonzero(owner[rows] != owner[B.col]))
+
+
+def scrambled(A, seed):
+    perm = np.random.default_rng(seed).permutation(A.n_rows).astype(np.int32)
+    return hec.permute(A, perm)
+
+
+def tridiagonal(n):
+    return hecgen.from_rows(n, [[(j, 2.0 if j == i else -1.0) for j in (i - 1, i, i + 1) if 0 <= j < n]
+                                for i in range(n)])
+
+
+def check_order(A, P, method):
+    perm, pp = hec.partition_order(A, P, method)
+    assert sorted(perm.tolist()) == list(range(A.n_rows))            # a permutation
+    assert pp[0] == 0 and pp[-1] == A.n_rows and np.all(np.diff(pp) >= 1)
+    return perm, pp
+
+
+@pytest.mark.parametrize("method", [hec.ORDER_BISECT, hec.ORDER_MULTILEVEL])
+def test_one_part_is_the_identity(method):
+    A = hecgen.powerlaw(500, seed=1)
+    perm, pp = check_order(A, 1, method)
+    assert perm.tolist() == list(range(500)) and pp.tolist() == [0, 500]
+
+
+def test_spec_tridiagonal_four_parts():
+    A = scrambled(tridiagonal(100), 3)
+    perm, pp = check_order(A, 4, hec.ORDER_BISECT)
+    assert np.diff(pp).tolist() == [25, 25, 25, 25]
+    B = hec.permute(A, perm)
+    assert off_block_nnz(B, pp) == 6                                  # 3 cut chain edges, both directions
+    assert halo(B, 4, hec.PART_EXPLICIT, pp) == 6
+
+
+def test_spec_poisson_20_cubed_eight_parts():
+    A = scrambled(hecgen.poisson3d(20, 20, 20), 4)
+    perm, pp = check_order(A, 8, hec.ORDER_BISECT)
+    assert np.all(np.abs(np.diff(pp) - 1000) <= 1)
+
+
+@pytest.mark.parametrize("n,P", [(60, 3), (96, 8), (1000, 5)])
+def test_bisect_rows_balanced_on_connected_graphs(n, P):
+    A = scrambled(hecgen.poisson2d(n // 4, 4), n)
+    _, pp = check_order(A, P, hec.ORDER_BISECT)
+    sizes = np.diff(pp)
+    assert sizes.max() - sizes.min() <= 1
+
+
+def test_bisect_restores_scrambled_grid_halo():
+    A = hecgen.poisson3d(16, 16, 16)
+    S = scrambled(A, 7)
+    perm, pp = check_order(S, 8, hec.ORDER_BISECT)
+    slabs = halo(A, 8, hec.PART_GRID, (16, 16, 16))
+    assert halo(hec.permute(S, perm), 8, hec.PART_EXPLICIT, pp) <= 2 * slabs
+    assert halo(S, 8) > 3 * slabs                                     # what the scramble did
+
+
+def test_multilevel_balances_nonzeros_and_beats_slabs_on_a_grid():
+    A = hecgen.poisson3d(16, 16, 16)
+    perm, pp = check_order(scrambled(A, 8), 8, hec.ORDER_MULTILEVEL)
+    B = hec.permute(scrambled(A, 8), perm)
+    nnz = np.diff(B.row_ptr[pp])
+    assert nnz.max() <= 1.03 * nnz.mean() + 7
+    assert halo(B, 8, hec.PART_EXPLICIT, pp) <= halo(A, 8, hec.PART_GRID, (16, 16, 16))
+
+
+def test_multilevel_recovers_the_scrambled_power_law():
+    # the scrambled power-law: the 90% local couplings are hidden by the random
+    # symmetric permutation; a contiguous cut of the scrambled order pays ~3x
+    # the natural order's halo.  The multilevel order must land near the
+    # natural order's halo (the 10% uniform far couplings keep it from doing
+    # much better: each is cut with probability 7/8 whatever the partition).
+    A = hecgen.powerlaw(1 << 16, seed=1)
+    nat = halo(A, 8)
+    S = scrambled(A, 5)
+    perm, pp = check_order(S, 8, hec.ORDER_MULTILEVEL)
+    B = hec.permute(S, perm)
+    got = halo(B, 8, hec.PART_EXPLICIT, pp)
+    assert halo(S, 8) > 2.5 * nat
+    assert got <= 1.1 * nat, (got, nat)
+    nnz = np.diff(B.row_ptr[pp])
+    assert nnz.max() <= 1.03 * nnz.mean() + 2000
+
+
+@pytest.mark.parametrize("method", [hec.ORDER_BISECT, hec.ORDER_MULTILEVEL])
+def test_deterministic_and_explicit_plan_matches_oracle(method):
+    A = scrambled(hecgen.spe10(10, 12, 6, seed=2), 9)
+    p1, q1 = check_order(A, 5, method)
+    p2, q2 = check_order(A, 5, method)
+    assert p1.tobytes() == p2.tobytes() and q1.tobytes() == q2.tobytes()
+    B = hec.permute(A, p1)
+    plan = hec.partition(B, 5, hec.PART_EXPLICIT, q1)
+    ref = PR.plan_ref(B, q1)
+    for p in range(5):
+        a = plan.export(p)
+        assert a.recv_cols.tolist() == ref[p].recv.tolist()
+        assert a.boundary.tolist() == ref[p].boundary.tolist()
+    x = hecgen.vector(A.n_cols, "uniform", seed=1)                  # (P A P^T)(P x) = P (A x)
+    assert np.all(np.abs(oracle.csr_spmv(B, x[p1]) - oracle.csr_spmv(A, x)[p1]) <= 2 * oracle.tolerance(A, x)[p1])
+
+
+def test_errors_and_explicit_validation():
+    A = hecgen.powerlaw(200, seed=2)
+    with pytest.raises(hec.HecError) as e:
+        hec.partition_order(A, 201, hec.ORDER_BISECT)
+    assert e.value.status == 4
+    with pytest.raises(hec.HecError) as e:
+        hec.partition_order(hecgen.random_csr(5, 7, 0.5, seed=1), 2, hec.ORDER_BISECT)
+    assert e.value.status == 3
+    for bad in ([0, 100, 100, 200], [1, 100, 200], [0, 150, 100, 200], [0, 100, 199]):
+        with pytest.raises(hec.HecError):
+            hec.partition(A, len(bad) - 1, hec.PART_EXPLICIT, bad)
+    ok = hec.partition(A, 4, hec.PART_EXPLICIT, [0, 50, 100, 150, 200])
+    assert ok.part_ptr().tolist() == hec.partition(A, 4, hec.PART_CONTIG_ROWS).part_ptr().tolist()
