@@ -103,7 +103,9 @@ typedef struct {
     int64_t tail_nnz;
     int64_t device_bytes;  /* bytes of device arrays owned by the handle */
     int32_t device;        /* CUDA device ordinal, or -1 for a host-only handle */
-    int32_t tail_fused;    /* 1: hec_spmv runs the (small) CSR tail inside the ELL launch */
+    int32_t tail_fused;    /* 1: hec_spmv runs a small CSR tail FIRST (its row sums stored into y)
+                              and the ELL kernel, launched as its programmatic dependent, adds
+                              them -- the tail's latency hides under the ELL stream */
 } hec_matrix_info;
 
 /* Caller-allocated export buffers, sized from hec_matrix_info:

@@ -244,62 +244,32 @@ hec_status make_matrix(HostHec&& h, int32_t device, cudaStream_t s, const int32_
         if ((st = dmalloc_copy(&m->d_tail_val, dval.data(), dval.size(), s, &bytes))) return st;
         HEC_CUDA_TRY(cudaStreamSynchronize(s));  // host vectors die after return
     }
-    // Small tails fused into the ELL launch (one launch per hec_spmv instead of
-    // two): whole matrices only, every ELL CTA one tile of rows (no grid
-    // stride), <= kFuseMaxRowsPerCta tail rows per tile.  HEC_FUSE_TAIL=0
-    // disables; HEC_FUSE_TAIL_MAX = most tail entries fused (default 65536).
+    // Small tails, tail first: the tail kernel (one wave) stores its row sums
+    // into y and the ELL kernel, its programmatic dependent, adds them in the
+    // CTAs that own tail rows -- the tail's latency hides under the ELL stream
+    // instead of trailing it.  Whole matrices whose ELL CTAs each take one tile
+    // of rows (no grid stride).  HEC_FUSE_TAIL=0 disables; HEC_FUSE_TAIL_MAX =
+    // most tail-kernel CTAs (default: one wave, 148 x 6).
     if (!h.tail_rows.empty() && n_loc < 0 && !rowmap && row_off == 0) {
-        int64_t fmax = 65536;
+        int64_t fmax = (int64_t)148 * 6;
         if (const char* e = std::getenv("HEC_FUSE_TAIL_MAX")) fmax = std::atol(e);
-        bool fuse = (int64_t)h.tail_col.size() <= fmax;
+        bool fuse = (int64_t)blk.size() <= fmax;
         if (const char* e = std::getenv("HEC_FUSE_TAIL")) fuse = fuse && std::atoi(e) != 0;
         const int32_t T = 2 * ell_block_threads(h.width);
         const int64_t n_cta = ((int64_t)h.n_rows + T - 1) / T;
         if (fuse && n_cta <= ell_grid_cap()) {
             const size_t tr = h.tail_rows.size();
-            std::vector<int32_t> cta((size_t)n_cta + 1, 0), frow(tr), fptr(tr + 1), flg(tr), fcol;
-            std::vector<double> fval;
-            const int epl = tail_epl(h.tail_col.size());  // as plan_chunks: same lanes per row
+            std::vector<int32_t> buf((size_t)n_cta + 1 + tr, 0);
             for (size_t t = 0; t < tr; ++t) {
-                cta[(size_t)(h.tail_rows[t] / T) + 1]++;
-                const int32_t b = h.tail_ptr[t], e = h.tail_ptr[t + 1];
-                frow[t] = h.tail_rows[t];
-                flg[t] = tail_lg_for(e - b, epl);
-                fptr[t] = (int32_t)fcol.size();
-                fcol.insert(fcol.end(), h.tail_col.begin() + b, h.tail_col.begin() + e);
-                fval.insert(fval.end(), h.tail_val.begin() + b, h.tail_val.begin() + e);
-                if ((e - b) & 1) { fcol.push_back(-1); fval.push_back(0.0); }  // rows start even: pair loads
+                buf[(size_t)(h.tail_rows[t] / T) + 1]++;
+                buf[(size_t)n_cta + 1 + t] = h.tail_rows[t];  // ascending
             }
-            fptr[tr] = (int32_t)fcol.size();
-            int32_t most = 0;
-            for (int64_t c = 0; c < n_cta; ++c) {
-                most = std::max(most, cta[(size_t)c + 1]);
-                cta[(size_t)c + 1] += cta[(size_t)c];
-            }
-            if (most <= kFuseMaxRowsPerCta && !fcol.empty()) {
-                // one allocation: the int32 arrays, the column indices from an
-                // 8-byte boundary (int2 pair loads), the values from a 16-byte
-                // boundary (double2 pair loads)
-                const size_t nmeta = cta.size() + 3 * tr + 1, ocol = (nmeta + 1) & ~(size_t)1;
-                const size_t ni2 = (ocol + fcol.size() + 3) & ~(size_t)3;
-                std::vector<int32_t> buf(ni2 + 2 * fval.size(), 0);
-                size_t o = 0;
-                for (auto* v : {&cta, &frow, &fptr, &flg}) {
-                    std::copy(v->begin(), v->end(), buf.begin() + o);
-                    o += v->size();
-                }
-                std::copy(fcol.begin(), fcol.end(), buf.begin() + ocol);
-                std::memcpy(buf.data() + ni2, fval.data(), fval.size() * sizeof(double));
-                if ((st = dmalloc_copy(&m->d_fuse, buf.data(), buf.size(), s, &bytes))) return st;
-                HEC_CUDA_TRY(cudaStreamSynchronize(s));  // buf dies after this scope
-                m->d_fuse_cta = m->d_fuse;
-                m->d_fuse_row = m->d_fuse_cta + cta.size();
-                m->d_fuse_ptr = m->d_fuse_row + tr;
-                m->d_fuse_lg = m->d_fuse_ptr + tr + 1;
-                m->d_fuse_col = m->d_fuse + ocol;
-                m->d_fuse_val = reinterpret_cast<const double*>(m->d_fuse + ni2);
-                m->fuse_tile = T;
-            }
+            for (int64_t c = 0; c < n_cta; ++c) buf[(size_t)c + 1] += buf[(size_t)c];
+            if ((st = dmalloc_copy(&m->d_fuse, buf.data(), buf.size(), s, &bytes))) return st;
+            HEC_CUDA_TRY(cudaStreamSynchronize(s));  // buf dies after this scope
+            m->d_fuse_cta = m->d_fuse;
+            m->d_fuse_row = m->d_fuse + n_cta + 1;
+            m->fuse_tile = T;
         }
     }
     if (rowmap)
@@ -342,19 +312,42 @@ static hec_status launch_chunks(const hec_matrix_s* A, int c, const double* x, c
     if (fused) {
         e.fuse_cta = A->d_fuse_cta;
         e.fuse_row = A->d_fuse_row;
-        e.fuse_ptr = A->d_fuse_ptr;
-        e.fuse_lg = A->d_fuse_lg;
-        e.fuse_col = A->d_fuse_col;
-        e.fuse_val = A->d_fuse_val;
+        e.pdl = true;  // dependent of the tail kernel launched just before it
     }
     if (pw) {  // peer-memory transport: wait for the peers' flags, boundary ELL as its dependent
         cudaError_t we = launch_peer_wait(*pw, s);
         if (we != cudaSuccess) return cuda_fail(we, "peer_wait_kernel launch");
         e.pdl = pw->n > 0;
     }
-    cudaError_t err = launch_ell(e, s);  // Alg. 1 lines 1-3: ELL first
+    const int64_t b0 = c < 0 ? 0 : A->chunk_blk[c];
+    const int64_t b1 = c < 0 ? A->chunk_blk[A->n_chunks] : A->chunk_blk[c + 1];
+    TailArgs t;
+    t.blk = A->d_tail_blk;
+    t.warp = A->d_tail_warp;
+    t.blk_begin = b0;
+    t.blk_end = b1;
+    t.out_rows = A->d_tail_out;
+    t.col = A->d_tail_col;
+    t.val = A->d_tail_val;
+    t.x = x;
+    t.x_halo = x_halo;
+    t.n_loc = e.n_loc;
+    t.y = y;
+    t.alpha = alpha;
+    t.diag = jd;
+    t.omega = omega;
+    cudaError_t err;
+    if (fused) {
+        // small tail, tail first: its row sums go into y, then the ELL kernel
+        // (programmatic dependent) adds them -- the same y_i = ell_i + tail_i
+        t.store_only = true;
+        err = launch_tail(t, s);
+        if (err != cudaSuccess) return cuda_fail(err, "tail_kernel launch");
+        err = launch_ell(e, s);
+        return err == cudaSuccess ? HEC_OK : cuda_fail(err, "ell_kernel launch");
+    }
+    err = launch_ell(e, s);  // Alg. 1 lines 1-3: ELL first
     if (err != cudaSuccess) return cuda_fail(err, "ell_kernel launch");
-    if (fused) return HEC_OK;            // lines 5-7 ran in the same launch
     if (A->tail_coo) {                   // HYB comparison variant: COO remainder
         CooArgs k;
         k.nnz = A->tail_nnz;
@@ -369,24 +362,7 @@ static hec_status launch_chunks(const hec_matrix_s* A, int c, const double* x, c
         err = launch_coo(k, s);
         return err == cudaSuccess ? HEC_OK : cuda_fail(err, "coo_kernel launch");
     }
-    const int64_t b0 = c < 0 ? 0 : A->chunk_blk[c];
-    const int64_t b1 = c < 0 ? A->chunk_blk[A->n_chunks] : A->chunk_blk[c + 1];
     if (A->tail_rows > 0 && b1 > b0) {  // Alg. 1 lines 5-7: then the CSR part
-        TailArgs t;
-        t.blk = A->d_tail_blk;
-        t.warp = A->d_tail_warp;
-        t.blk_begin = b0;
-        t.blk_end = b1;
-        t.out_rows = A->d_tail_out;
-        t.col = A->d_tail_col;
-        t.val = A->d_tail_val;
-        t.x = x;
-        t.x_halo = x_halo;
-        t.n_loc = e.n_loc;
-        t.y = y;
-        t.alpha = alpha;
-        t.diag = jd;
-        t.omega = omega;
         err = launch_tail(t, s);
         if (err != cudaSuccess) return cuda_fail(err, "tail_kernel launch");
     }
@@ -468,7 +444,7 @@ hec_status hec_info(hec_matrix A, hec_matrix_info* o) {
     o->tail_nnz = A->tail_nnz;
     o->device_bytes = A->device_bytes;
     o->device = A->device;
-    o->tail_fused = A->fuse_tile > 0 ? 1 : 0;
+    o->tail_fused = A->fuse_tile > 0 && A->fuse_tile == 2 * ell_block_threads(A->width) ? 1 : 0;
     return HEC_OK;
 }
 
@@ -662,8 +638,7 @@ hec_status hec_spmv_host(hec_matrix A, const double* x_host, double* y_host, voi
 
 int32_t hec_spmv_launches(hec_matrix A) {
     if (!A || A->n_rows == 0) return 0;
-    if (A->fuse_tile > 0 && A->fuse_tile == 2 * ell_block_threads(A->width)) return 1;
-    return 1 + (A->tail_rows > 0 ? 1 : 0);
+    return 1 + (A->tail_rows > 0 ? 1 : 0);  // (tail first for small tails: still two launches)
 }
 
 void hec_free(hec_matrix A) { release(A); }

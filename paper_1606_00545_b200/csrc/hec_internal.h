@@ -176,12 +176,10 @@ struct hec_matrix_s {
     std::vector<int32_t> chunk_row;    // [n_chunks+1], multiples of 512
     std::vector<int32_t> chunk_xend;   // [n_chunks]: x[0 : xend) needed by rows < chunk_row[c+1]
     std::vector<int64_t> chunk_blk;    // [n_chunks+1]: tail-kernel blocks of each chunk
-    // small tail fused into the ELL launch (plain hec_spmv only; the warp-chunk
-    // tail above stays for the chunked / epilogue paths)
-    int32_t* d_fuse = nullptr;         // one allocation: cta ptr | row | ptr | lg | col, then val
-    const int32_t *d_fuse_cta = nullptr, *d_fuse_row = nullptr, *d_fuse_ptr = nullptr, *d_fuse_lg = nullptr,
-                  *d_fuse_col = nullptr;
-    const double* d_fuse_val = nullptr;
+    // small tails, tail first (plain hec_spmv only): per ELL CTA tile, its tail
+    // rows (the tail kernel stores their sums, the ELL kernel adds them)
+    int32_t* d_fuse = nullptr;         // one allocation: cta ptr [n_cta + 1] | tail rows ascending
+    const int32_t *d_fuse_cta = nullptr, *d_fuse_row = nullptr;
     int32_t fuse_tile = 0;             // rows per ELL CTA the map was built for (0: not fused)
     cudaStream_t s_h2d = nullptr, s_d2h = nullptr;
     std::vector<cudaEvent_t> ev_x, ev_y;
@@ -266,17 +264,12 @@ struct EllArgs {
     const double* b = nullptr;
     double omega = 0.0;
     bool pdl = false;  // launch as a programmatic dependent (peer-memory boundary rows)
-    // small CSR tail fused into this launch (plain y = A x of a whole matrix):
-    // CTA b adds the tail sums of its own rows, tail rows [fuse_cta[b], fuse_cta[b+1])
+    // small tails, tail first (plain y = A x of a whole matrix): the tail kernel
+    // stored the tail rows' sums into y just before; CTA b adds them to its
+    // rows fuse_row[fuse_cta[b] .. fuse_cta[b+1]) (ascending)
     const int32_t* fuse_cta = nullptr;
-    const int32_t* fuse_row = nullptr;  // per fused tail row: output row
-    const int32_t* fuse_ptr = nullptr;  // per fused tail row: first entry (even), [q+1] = end
-    const int32_t* fuse_lg = nullptr;   // per fused tail row: lanes per row G = 2^lg (as the tail kernel)
-    const int32_t* fuse_col = nullptr;
-    const double* fuse_val = nullptr;
+    const int32_t* fuse_row = nullptr;
 };
-// Fused small tails: at most this many tail rows per CTA tile of the ELL kernel.
-constexpr int kFuseMaxRowsPerCta = 512;
 struct TailArgs {
     const int4* blk;            // block descriptors {first row position, count, lg, first warp} (diag)
     const int4* warp;           // 8 per descriptor: {first entry, iterations, first row, count << 8 | lg}
@@ -289,6 +282,7 @@ struct TailArgs {
     int32_t n_loc;
     double* y;
     double alpha = 1.0;  // the tail adds alpha * (its part of A x)
+    bool store_only = false;  // small tails, tail first: store the row sums into y (the ELL kernel adds them)
     const double* diag = nullptr;  // Jacobi (A22): the tail adds -omega * (its part / diag[row])
     double omega = 0.0;
 };

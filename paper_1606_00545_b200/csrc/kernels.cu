@@ -22,6 +22,7 @@
 // the roofline is HBM bandwidth.
 #include <cuda_runtime.h>
 
+#include <algorithm>
 #include <cstdint>
 #include <cstdlib>
 #include <cstring>
@@ -230,50 +231,27 @@ __device__ __forceinline__ void ell_phase(const EllArgs& a, const int32_t* cp, c
     }
 }
 
-// One fused tail row (Alg. 1 lines 5-7 for a small tail): the warp computes
-// exactly what tail_kernel's G = 2^lg lanes compute for the row -- lane lr
-// sums entries 2 (i G + lr), +1 in order; G <= 32: the xor tree over G lanes;
-// G > 32: G / 32 virtual warps, each a full-warp tree, added in warp order --
-// so the fused and the two-kernel products are bitwise identical.
-__device__ __forceinline__ double fused_tail_row(const EllArgs& a, int32_t q, int l) {
-    const int lg = __ldg(a.fuse_lg + q), G = 1 << lg;
-    const int32_t kb = __ldg(a.fuse_ptr + q), ke = __ldg(a.fuse_ptr + q + 1);
-    const int nv = G > 32 ? G >> 5 : 1;
-    double total = 0.0;
-    for (int vw = 0; vw < nv; ++vw) {
-        const int lr = G > 32 ? 32 * vw + l : l;
-        double acc = 0.0;
-        if (lr < G) {
-            for (int32_t k = kb + 2 * lr; k < ke; k += 2 * G) {
-                const int2 c = __ldg(reinterpret_cast<const int2*>(a.fuse_col + k));
-                const double2 v = __ldg(reinterpret_cast<const double2*>(a.fuse_val + k));
-                const double x0 = c.x >= 0 ? __ldg(a.x + c.x) : 0.0;
-                const double x1 = c.y >= 0 ? __ldg(a.x + c.y) : 0.0;
-                if (c.x >= 0) acc = fma(v.x, x0, acc);
-                if (c.y >= 0) acc = fma(v.y, x1, acc);
-            }
-        }
-        if (G <= 32) {
-            for (int off = G >> 1; off > 0; off >>= 1) acc += __shfl_xor_sync(0xffffffffu, acc, off, G);
-            return acc;
-        }
-        for (int off = 16; off > 0; off >>= 1) acc += __shfl_xor_sync(0xffffffffu, acc, off);
-        total = vw == 0 ? acc : total + acc;
+// FUSE (small tails, "tail first"): the tail kernel ran just before this
+// launch and stored each tail row's sum into y; this kernel is its
+// programmatic dependent, so its CTAs stream their ELL rows while the tail
+// finishes, and only a CTA that owns tail rows waits for it (at its very end)
+// before adding the stored sum: y_i = ell_i + tail_i, the one rounding of the
+// red.add path.  The CTA's tail rows: fuse_row[fuse_cta[b] .. fuse_cta[b+1]).
+__device__ __forceinline__ bool fuse_has(const EllArgs& a, int32_t q0, int32_t q1, int64_t row) {
+    while (q0 < q1) {  // binary search of the CTA's (ascending) tail rows
+        const int32_t m = (q0 + q1) >> 1;
+        const int32_t r = __ldg(a.fuse_row + m);
+        if (r == row) return true;
+        if (r < row) q0 = m + 1; else q1 = m;
     }
-    return total;
+    return false;
 }
 
-// (FUSE: the tail code would lift the kernel to 64 registers; cap it at the
-// plain kernel's occupancy, 5 x 256 threads per SM -- spills land in the
-// cold tail part only)
 template <int W, bool HALO, bool ROWMAP, int EPI, bool FUSE = false>
-__global__ void __launch_bounds__(256, EPI == EPI_JACOBI ? HEC_JAC_MINB : (FUSE ? 5 : 0)) ell_kernel(EllArgs a) {
+__global__ void __launch_bounds__(256, EPI == EPI_JACOBI ? HEC_JAC_MINB : 0) ell_kernel(EllArgs a) {
     constexpr bool AXPBY = EPI == EPI_AXPBY;
-    // FUSE: the CTA's tail-row range is loaded now and used after the ELL rows
-    // (nothing in the ELL stream waits for it)
-    __shared__ double tsum[FUSE ? kFuseMaxRowsPerCta : 1];
     int32_t q0 = 0, q1 = 0;
-    if constexpr (FUSE) {
+    if constexpr (FUSE) {  // loaded now, used after the ELL rows (nothing waits for it)
         q0 = __ldg(a.fuse_cta + blockIdx.x);
         q1 = __ldg(a.fuse_cta + blockIdx.x + 1);
     }
@@ -354,28 +332,21 @@ __global__ void __launch_bounds__(256, EPI == EPI_JACOBI ? HEC_JAC_MINB : (FUSE 
                 acc0 *= a.alpha;
                 acc1 *= a.alpha;
             }
+            if constexpr (FUSE) {
+                if (q1 > q0) {
+                    const bool t0 = fuse_has(a, q0, q1, i0), t1 = two && fuse_has(a, q0, q1, i0 + 1);
+                    if (t0 || t1) {
+                        asm volatile("griddepcontrol.wait;" ::: "memory");  // the tail kernel's stores
+                        if (t0) acc0 = acc0 + __ldcg(yp);
+                        if (t1) acc1 = acc1 + __ldcg(yp + 1);
+                    }
+                }
+            }
             if (two && ((reinterpret_cast<uintptr_t>(yp) & 15) == 0)) {
                 st_stream_d2(yp, acc0, acc1);
             } else {
                 st_stream_d1(yp, acc0);
                 if (two) st_stream_d1(yp + 1, acc1);
-            }
-        }
-    }
-    if constexpr (FUSE) {
-        // the CTA's tail rows (a small tail): one warp per row, then
-        // y_i = ell_i + tail_i, one rounding (as tail_kernel's red.add); the
-        // barrier makes this CTA's y stores and sums visible to its threads
-        if (q1 > q0) {
-            const int l = threadIdx.x & 31;
-            for (int32_t q = q0 + (int32_t)(threadIdx.x >> 5); q < q1; q += (int32_t)(blockDim.x >> 5)) {
-                const double t = fused_tail_row(a, q, l);
-                if (l == 0) tsum[q - q0] = t;
-            }
-            __syncthreads();
-            for (int32_t q = q0 + (int32_t)threadIdx.x; q < q1; q += (int32_t)blockDim.x) {
-                double* yr = a.y + __ldg(a.fuse_row + q);
-                *yr = *yr + tsum[q - q0];
             }
         }
     }
@@ -495,6 +466,10 @@ __device__ __forceinline__ void tail_desc(const TailArgs& a, int64_t desc, int t
     // y holds the ELL result: with programmatic dependent launch this kernel may
     // have started before ell_kernel finished, so wait for it here (a no-op
     // when launched normally or once it has returned)
+    if (a.store_only) {  // small tails, tail first: the ELL kernel adds it (FUSE)
+        if (lane == 0 && active) *yp = q;
+        return;
+    }
     asm volatile("griddepcontrol.wait;" ::: "memory");
     if (lane == 0 && active) asm volatile("red.global.add.f64 [%0], %1;" ::"l"(yp), "d"(q) : "memory");
 }
@@ -506,6 +481,9 @@ __device__ __forceinline__ void tail_desc(const TailArgs& a, int64_t desc, int t
 template <bool HALO, bool JACOBI>
 __global__ void __launch_bounds__(256, HEC_TAIL_MINB) tail_kernel(TailArgs a) {
     __shared__ double wsum[8];  // per-warp partials of rows wider than a warp
+    // store_only: the ELL kernel is this grid's programmatic dependent -- let
+    // it start streaming right away (it waits for these stores where it needs them)
+    if (a.store_only) asm volatile("griddepcontrol.launch_dependents;");
     const uint64_t pol = policy_evict_first();
     tail_desc<HALO, JACOBI>(a, a.blk_begin + blockIdx.x, threadIdx.x, pol, wsum);
 }
@@ -655,8 +633,14 @@ static cudaError_t launch_ell_t(const EllArgs& a, cudaStream_t s) {
     // one row pair per thread, grid-stride only beyond 64 full waves (a
     // persistent grid of 5-40 blocks/SM was measured slower, r15; forcing
     // >= 6 CTAs/SM by a 40-register cap too, pdl run)
-    const int64_t cap = ell_grid_cap();
+    int64_t cap = ell_grid_cap();
     if (FUSE && (blocks > cap || 2 * threads * blocks < a.n_rows)) return cudaErrorInvalidValue;  // planned per tile
+    static int per_sm = -1;  // HEC_ELL_CAP (tuning): at most this many CTAs per SM, grid-stride beyond
+    if (per_sm < 0) {
+        const char* e = std::getenv("HEC_ELL_CAP");
+        per_sm = e ? std::max(0, std::atoi(e)) : 0;
+    }
+    if (per_sm > 0 && !FUSE) cap = std::min<int64_t>(cap, (int64_t)num_sms() * per_sm);
     if (blocks > cap) blocks = cap;
     if (blocks < 1) blocks = 1;
     const dim3 g((unsigned)blocks), b(threads);
@@ -710,8 +694,9 @@ cudaError_t launch_tail(const TailArgs& a, cudaStream_t s) {
     const int64_t blocks = a.blk_end - a.blk_begin;
     if (blocks <= 0) return cudaSuccess;
     if (blocks > 0x7fffffff) return cudaErrorInvalidValue;
-    const bool pdl = tail_pdl();
+    const bool pdl = tail_pdl() && !a.store_only;  // store_only runs first: an ordinary launch
     if (a.diag && a.x_halo) return cudaErrorInvalidValue;
+    if (a.store_only && (a.diag || a.x_halo || a.alpha != 1.0)) return cudaErrorInvalidValue;
     if (a.diag) return launch_k(tail_kernel<false, true>, dim3((unsigned)blocks), dim3(256), s, pdl, 0, a);
     if (a.x_halo) return launch_k(tail_kernel<true, false>, dim3((unsigned)blocks), dim3(256), s, pdl, 0, a);
     return launch_k(tail_kernel<false, false>, dim3((unsigned)blocks), dim3(256), s, pdl, 0, a);

@@ -1,10 +1,11 @@
-"""GPU parity of the fused small-tail path: for a whole matrix whose CSR tail is
-small (<= 65,536 entries, <= 512 tail rows per ELL tile), hec_spmv runs Alg. 1
-lines 1-3 AND 5-7 in ONE launch -- each ELL CTA adds the tail
-sums of its own rows after its ELL stores.  The fused warp reproduces the tail
-kernel's lanes and reduction tree, so fused and two-kernel products must be
-BITWISE equal; both within the north_star tolerance of the oracle (bitwise on
-integer data).  HEC_FUSE_TAIL=0 forces the two-kernel path."""
+"""GPU parity of the small-tail "tail first" path: for a whole matrix whose CSR
+tail kernel fits one wave, hec_spmv runs Alg. 1 lines 5-7 FIRST,
+storing each tail row's sum into y, and the ELL kernel (lines 1-3), launched
+as its programmatic dependent, adds the stored sums in the CTAs that own tail
+rows.  Same lanes, order and single rounding y_i = ell_i + tail_i as the
+ELL-then-tail path, so the two products must be BITWISE equal; both within the
+north_star tolerance of the oracle (bitwise on integer data).
+HEC_FUSE_TAIL=0 forces the ELL-then-tail order."""
 import os
 
 import numpy as np
@@ -63,27 +64,27 @@ def test_fused_equals_two_kernel_bitwise_and_oracle(name, maker, o):
     A = maker()
     x = hecgen.vector(A.n_cols, "uniform", seed=1606)
     Mf, M2 = build(A, True, o), build(A, False, o)
-    assert M2.info.tail_rows > 0 and M2.launches == 2
-    assert Mf.launches == 1, name                  # Alg. 1 in one launch
+    assert M2.info.tail_rows > 0 and M2.launches == 2 and M2.info.tail_fused == 0
+    assert Mf.info.tail_fused == 1, name           # tail first, ELL as its dependent
     yf, y2 = run(Mf, x), run(M2, x)
     assert yf.tobytes() == y2.tobytes()
     assert np.all(np.abs(yf - oracle.csr_spmv(A, x)) <= oracle.tolerance(A, x))
 
 
 def test_fused_integer_bitwise():
-    A = hecgen.powerlaw(4096, integer_values=True, seed=5)
+    A = hecgen.powerlaw(8192, integer_values=True, seed=5)
     xi = hecgen.vector(A.n_cols, "int", seed=1)
     M = build(A, True)
-    assert M.launches == 1
+    assert M.info.tail_fused == 1
     assert run(M, xi).tobytes() == oracle.csr_spmv(A, xi).tobytes()
 
 
 def test_fused_all_rows_in_the_tail():
-    # CAP 0: width 0, every row is a tail row (512 per 256-thread tile, the
-    # per-tile maximum): the fused launch is the whole product
+    # CAP 0: width 0, every row is a tail row: the ELL kernel only adds the
+    # stored sums (every CTA waits for the tail grid)
     A = hecgen.powerlaw(3000, seed=6)
     Mf, M2 = build(A, True, hec.opts(hec.WIDTH_CAP, 0)), build(A, False, hec.opts(hec.WIDTH_CAP, 0))
-    assert Mf.info.ell_width == 0 and Mf.launches == 1
+    assert Mf.info.ell_width == 0 and Mf.info.tail_fused == 1
     x = hecgen.vector(A.n_cols, "uniform", seed=2)
     yf = run(Mf, x)
     assert yf.tobytes() == run(M2, x).tobytes()
@@ -96,7 +97,7 @@ def test_fused_epilogues_and_host_path_use_two_kernels_consistently():
     A = hecgen.spe10(20, 30, 10, seed=9)
     x = hecgen.vector(A.n_cols, "uniform", seed=3)
     M = build(A, True)
-    assert M.launches == 1
+    assert M.info.tail_fused == 1
     y = run(M, x)
     yd = torch.zeros(A.n_rows, dtype=torch.float64, device="cuda")
     M.spmv_axpby(2.0, torch.from_numpy(x).cuda(), 0.0, yd)

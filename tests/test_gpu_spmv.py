@@ -52,7 +52,7 @@ def test_parity_uniform_x(name, maker):
     y, M = gpu_spmv(A, x)
     assert_parity(A, x, y)
     if name == "spe10":
-        assert M.info.tail_rows > 0 and M.launches == 1        # the CSR tail is exercised, fused into the ELL launch
+        assert M.info.tail_rows > 0 and M.launches == 2        # the CSR tail is exercised (tail first: M.info.tail_fused)
 
 
 @pytest.mark.parametrize("name,maker", CONFIGS[:5])
