@@ -142,9 +142,13 @@ hec_status hec_info(hec_matrix A, hec_matrix_info* out);
 hec_status hec_export(hec_matrix A, hec_host_arrays* out);
 
 /* y = A x (Alg. 1): the ELL kernel writes every row of y, then the
- * CSR-tail kernel adds the spilled entries of the tail rows.  x: device,
- * n_cols doubles; y: device, n_rows doubles, fully overwritten; x and y must
- * not overlap (HEC_ERR_ARG).  Asynchronous on `stream`. */
+ * CSR-tail kernel adds the spilled entries of the tail rows (a small tail --
+ * one wave of tail CTAs -- runs first instead, storing its row sums, and the
+ * ELL kernel adds them: the same y bit for bit).  x: device, n_cols doubles;
+ * y: device, n_rows doubles, fully overwritten; x and y must not overlap
+ * (HEC_ERR_ARG).  Asynchronous on `stream`.  Calls on ONE handle must be
+ * ordered (one stream, or synchronised): a big tail's SM-local schedule keeps
+ * its claim counters in the handle. */
 hec_status hec_spmv(hec_matrix A, const double* x, double* y, void* stream);
 
 /* Same product with HOST x and y (n_cols / n_rows doubles; pinned memory is

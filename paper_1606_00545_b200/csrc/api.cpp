@@ -30,7 +30,8 @@ static void release(hec_matrix_s* m) {
         cudaGetDevice(&cur);
         cudaSetDevice(m->device);
         if (m->ws && m->ws_free) m->ws_free(m->ws);
-        void* ptrs[] = {m->d_ell_col, m->d_ell_val, m->d_tail_out, m->d_tail_blk, m->d_fuse,
+        void* ptrs[] = {m->d_ell_col, m->d_ell_val, m->d_tail_out, m->d_tail_blk, m->d_fuse, m->d_tail_region,
+                        m->d_tail_ctr, m->d_tsum,
                         m->d_tail_warp, m->d_tail_col, m->d_tail_val, m->d_rowmap, m->d_coo_row, m->d_stage_x,
                         m->d_stage_y};
         for (void* p : ptrs)
@@ -38,6 +39,9 @@ static void release(hec_matrix_s* m) {
         for (cudaEvent_t e : m->ev_x) cudaEventDestroy(e);
         for (cudaEvent_t e : m->ev_y) cudaEventDestroy(e);
         if (m->ev_start) cudaEventDestroy(m->ev_start);
+        if (m->ev_fork) cudaEventDestroy(m->ev_fork);
+        if (m->ev_join) cudaEventDestroy(m->ev_join);
+        if (m->s_tail) cudaStreamDestroy(m->s_tail);
         if (m->s_h2d) cudaStreamDestroy(m->s_h2d);
         if (m->s_d2h) cudaStreamDestroy(m->s_d2h);
         cudaSetDevice(cur);
@@ -242,6 +246,47 @@ hec_status make_matrix(HostHec&& h, int32_t device, cudaStream_t s, const int32_
         if ((st = dmalloc_copy(&m->d_tail_warp, warp.data(), warp.size(), s, &bytes))) return st;
         if ((st = dmalloc_copy(&m->d_tail_col, dcol.data(), dcol.size(), s, &bytes))) return st;
         if ((st = dmalloc_copy(&m->d_tail_val, dval.data(), dval.size(), s, &bytes))) return st;
+        // SM-local persistent schedule for big tails (more descriptors than one
+        // wave): one region of descriptors per SM, equal stored entries each.
+        // Opt-in (HEC_TAIL_SM=1): it lifts the gathers' L1 hit rate 20% -> 57%
+        // but measured slower (power-law tail 320 vs 264 us: the per-descriptor
+        // barriers idle the early warps), DESIGN §5
+        int n_sm = 0;
+        cudaDeviceGetAttribute(&n_sm, cudaDevAttrMultiProcessorCount, device);
+        bool sm_sched = false;
+        if (const char* e = std::getenv("HEC_TAIL_SM"))
+            sm_sched = n_sm > 0 && (int64_t)blk.size() > (int64_t)n_sm * 6 && std::atoi(e) != 0;
+        if (sm_sched) {
+            std::vector<int64_t> wsum(blk.size() + 1, 0);  // entries (padded) per descriptor, prefix
+            for (size_t d = 0; d < blk.size(); ++d) {
+                int64_t e = 0;
+                for (int w = 0; w < 8; ++w) e += (int64_t)warp[(size_t)blk[d].w + w].y * kTailChunk;
+                wsum[d + 1] = wsum[d] + e;
+            }
+            std::vector<int64_t> reg((size_t)n_sm + 1, 0);
+            for (int r = 1; r < n_sm; ++r) {
+                const int64_t target = wsum.back() * r / n_sm;
+                reg[r] = std::lower_bound(wsum.begin(), wsum.end(), target) - wsum.begin();
+                reg[r] = std::max(reg[r], reg[r - 1]);
+            }
+            reg[n_sm] = (int64_t)blk.size();
+            if ((st = dmalloc_copy(&m->d_tail_region, reg.data(), reg.size(), s, &bytes))) return st;
+            std::vector<unsigned int> zero((size_t)n_sm + 1, 0u);
+            if ((st = dmalloc_copy(&m->d_tail_ctr, zero.data(), zero.size(), s, &bytes))) return st;
+            m->tail_regions = n_sm;
+        }
+        // concurrent tail for big tails (opt-in HEC_TAIL_CONC=1): measured slower
+        // (power-law 0.484 vs 0.436 ms: the two kernels share the memory system
+        // and the scattered combine pass costs 48 us), DESIGN §5
+        if (const char* e = std::getenv("HEC_TAIL_CONC"))
+            if (std::atoi(e) != 0 && (int64_t)blk.size() > (int64_t)n_sm * 6 && n_loc < 0 && !rowmap) {
+                HEC_CUDA_TRY(cudaMalloc(&m->d_tsum, sizeof(double) * h.tail_rows.size()));
+                bytes += (int64_t)(sizeof(double) * h.tail_rows.size());
+                HEC_CUDA_TRY(cudaStreamCreateWithFlags(&m->s_tail, cudaStreamNonBlocking));
+                HEC_CUDA_TRY(cudaEventCreateWithFlags(&m->ev_fork, cudaEventDisableTiming));
+                HEC_CUDA_TRY(cudaEventCreateWithFlags(&m->ev_join, cudaEventDisableTiming));
+                m->tail_conc = true;
+            }
         HEC_CUDA_TRY(cudaStreamSynchronize(s));  // host vectors die after return
     }
     // Small tails, tail first: the tail kernel (one wave) stores its row sums
@@ -336,7 +381,30 @@ static hec_status launch_chunks(const hec_matrix_s* A, int c, const double* x, c
     t.alpha = alpha;
     t.diag = jd;
     t.omega = omega;
+    if (c < 0 && A->tail_regions > 0) {  // whole launch: the SM-local persistent schedule
+        t.region = A->d_tail_region;
+        t.n_regions = A->tail_regions;
+        t.region_ctr = A->d_tail_ctr;
+        t.region_done = A->d_tail_ctr + A->tail_regions;
+    }
     cudaError_t err;
+    if (A->tail_conc && c < 0 && !pw && !jd && alpha == 1.0 && beta == 0.0 && !x_halo) {
+        // concurrent tail: the tail kernel (sums into tsum) on its own stream
+        // beside the ELL kernel, then y[row] += tsum once both are done
+        HEC_CUDA_TRY(cudaEventRecord(A->ev_fork, s));
+        HEC_CUDA_TRY(cudaStreamWaitEvent(A->s_tail, A->ev_fork, 0));
+        t.store_only = true;
+        t.tsum = A->d_tsum;
+        t.region = nullptr;
+        err = launch_tail(t, A->s_tail);
+        if (err != cudaSuccess) return cuda_fail(err, "tail_kernel launch");
+        HEC_CUDA_TRY(cudaEventRecord(A->ev_join, A->s_tail));
+        err = launch_ell(e, s);
+        if (err != cudaSuccess) return cuda_fail(err, "ell_kernel launch");
+        HEC_CUDA_TRY(cudaStreamWaitEvent(s, A->ev_join, 0));
+        err = launch_tail_combine(A->d_tail_out, A->d_tsum, A->tail_rows, y, s);
+        return err == cudaSuccess ? HEC_OK : cuda_fail(err, "tail_combine launch");
+    }
     if (fused) {
         // small tail, tail first: its row sums go into y, then the ELL kernel
         // (programmatic dependent) adds them -- the same y_i = ell_i + tail_i

@@ -74,7 +74,7 @@ hec_status convert(const CsrView& A, int32_t width, int32_t stride_unit, HostHec
 // (reading A4).  A lane's pairs are its row's entries 2(iG + lr), +1 in
 // order, lr = its lane within the row.
 constexpr int kTailChunk = 64;         // entries per warp per iteration (32 lanes x a pair)
-constexpr int kTailSuperRows = 4096;   // tail rows regrouped by length within blocks of this many
+constexpr int kTailSuperRows = 2048;   // tail rows regrouped by length within blocks of this many (sweep: 256 340 us, 512 282, 1024 251, 2048 249, 4096 262, 16384 300 on the power-law tail)
 
 // Lanes per tail row: the smallest power of two >= ceil(L / epl), capped at
 // 2^kTailMaxLg, where epl = target entries per lane.  Up to 32 lanes a row
@@ -160,6 +160,15 @@ struct hec_matrix_s {
     std::vector<int4> h_tail_blk;      // descriptors {first row position, count, lg, first warp}
     std::vector<int4> h_tail_warp;     // 8 per descriptor: {first entry, iterations, first row, count << 8 | lg}
     int4* d_tail_warp = nullptr;
+    int64_t* d_tail_region = nullptr;  // SM-local tail schedule: [n_regions + 1] descriptor boundaries
+    unsigned int* d_tail_ctr = nullptr;  // [n_regions] claim counters + 1 done counter
+    int32_t tail_regions = 0;
+    // concurrent tail (big tails, whole plain launches): the tail kernel on its
+    // own stream beside the ELL kernel, sums into tsum, then one combine pass
+    bool tail_conc = false;
+    double* d_tsum = nullptr;
+    cudaStream_t s_tail = nullptr;
+    cudaEvent_t ev_fork = nullptr, ev_join = nullptr;
     int64_t tail_entries = 0;          // device tail positions (stored entries + padding)
     int4* d_tail_blk = nullptr;        // per CUDA block: {first position, count, lg, 0}
     int32_t* d_tail_col = nullptr;
@@ -282,7 +291,15 @@ struct TailArgs {
     int32_t n_loc;
     double* y;
     double alpha = 1.0;  // the tail adds alpha * (its part of A x)
-    bool store_only = false;  // small tails, tail first: store the row sums into y (the ELL kernel adds them)
+    bool store_only = false;  // store the row sums instead of adding them: into y (small tails first,
+                              // the ELL kernel adds them) or into tsum (concurrent tail, combined after)
+    double* tsum = nullptr;   // [tail rows], indexed by device row position
+    // SM-local persistent schedule (tail_sm_kernel; whole launches only): descriptors
+    // [region[r], region[r+1]) are SM r's, claimed through region_ctr[r]
+    const int64_t* region = nullptr;
+    int32_t n_regions = 0;
+    unsigned int* region_ctr = nullptr;  // [n_regions], zero between launches
+    unsigned int* region_done = nullptr; // CTA completion counter (self-resetting)
     const double* diag = nullptr;  // Jacobi (A22): the tail adds -omega * (its part / diag[row])
     double omega = 0.0;
 };
@@ -307,6 +324,7 @@ cudaError_t launch_tail(const TailArgs& a, cudaStream_t s);
 cudaError_t launch_ell_tma(const EllArgs& a, cudaStream_t s, int num_sms);
 cudaError_t launch_pack(const int32_t* idx, int32_t n, const double* x, double* out,
                         cudaStream_t s);
+cudaError_t launch_tail_combine(const int32_t* out_rows, const double* tsum, int32_t n, double* y, cudaStream_t s);
 // d[i] = A_ii of a square single-device handle: ELL scan, then the tail (warp
 // chunks or COO)
 cudaError_t launch_diag(const hec_matrix_s* A, double* d, cudaStream_t s);

@@ -466,8 +466,11 @@ __device__ __forceinline__ void tail_desc(const TailArgs& a, int64_t desc, int t
     // y holds the ELL result: with programmatic dependent launch this kernel may
     // have started before ell_kernel finished, so wait for it here (a no-op
     // when launched normally or once it has returned)
-    if (a.store_only) {  // small tails, tail first: the ELL kernel adds it (FUSE)
-        if (lane == 0 && active) *yp = q;
+    if (a.store_only) {  // small tails first (the ELL kernel adds it) / concurrent tail (combined later)
+        if (lane == 0 && active) {
+            if (a.tsum) a.tsum[wm.z + grp] = q;
+            else *yp = q;
+        }
         return;
     }
     asm volatile("griddepcontrol.wait;" ::: "memory");
@@ -486,6 +489,55 @@ __global__ void __launch_bounds__(256, HEC_TAIL_MINB) tail_kernel(TailArgs a) {
     if (a.store_only) asm volatile("griddepcontrol.launch_dependents;");
     const uint64_t pol = policy_evict_first();
     tail_desc<HALO, JACOBI>(a, a.blk_begin + blockIdx.x, threadIdx.x, pol, wsum);
+}
+
+// SM-local persistent schedule (whole-matrix launches of big tails): the
+// descriptors are cut into one contiguous region per SM (equal entries), and
+// the CTAs resident on an SM claim its region's descriptors in order through
+// a counter -- so the 6 CTAs sharing an SM's L1 work on neighbouring rows and
+// share the x window their gathers touch (the stream bypasses L1, leaving L1
+// to x).  A CTA that runs out of its SM's work steals from the next regions:
+// every descriptor is claimed exactly once whatever the CTA placement.  The
+// last CTA to finish resets the counters (the next launch is stream-ordered).
+// Same descriptors, lanes and red.add per row as tail_kernel: bitwise equal.
+__device__ __forceinline__ uint32_t sm_id() {
+    uint32_t r;
+    asm volatile("mov.u32 %0, %%smid;" : "=r"(r));
+    return r;
+}
+
+template <bool HALO, bool JACOBI>
+__global__ void __launch_bounds__(256, HEC_TAIL_MINB) tail_sm_kernel(TailArgs a) {
+    __shared__ double wsum[8];
+    __shared__ int64_t claim;
+    const uint64_t pol = policy_evict_first();
+    const int R = a.n_regions;
+    const int home = (int)(sm_id() % (uint32_t)R);
+    for (int k = 0; k < R; ++k) {
+        const int r = home + k < R ? home + k : home + k - R;
+        const int64_t r0 = __ldg(a.region + r), r1 = __ldg(a.region + r + 1);
+        if (threadIdx.x == 0) claim = r0 + (int64_t)atomicAdd(a.region_ctr + r, 1u);
+        __syncthreads();
+        int64_t d = claim;
+        while (d < r1) {
+            // claim the next descriptor now; its atomic's latency overlaps this one's work
+            unsigned int nxt = 0;
+            if (threadIdx.x == 0) nxt = atomicAdd(a.region_ctr + r, 1u);
+            tail_desc<HALO, JACOBI>(a, d, threadIdx.x, pol, wsum);
+            __syncthreads();  // everybody is done with this descriptor (wsum, claim)
+            if (threadIdx.x == 0) claim = r0 + (int64_t)nxt;
+            __syncthreads();
+            d = claim;
+        }
+    }
+    if (threadIdx.x == 0) {
+        __threadfence();
+        if (atomicAdd(a.region_done, 1u) == gridDim.x - 1) {
+            for (int r = 0; r < R; ++r) a.region_ctr[r] = 0;
+            __threadfence();
+            *a.region_done = 0;
+        }
+    }
 }
 
 // ------------------------------------------------------- HYB: COO kernel --
@@ -697,9 +749,35 @@ cudaError_t launch_tail(const TailArgs& a, cudaStream_t s) {
     const bool pdl = tail_pdl() && !a.store_only;  // store_only runs first: an ordinary launch
     if (a.diag && a.x_halo) return cudaErrorInvalidValue;
     if (a.store_only && (a.diag || a.x_halo || a.alpha != 1.0)) return cudaErrorInvalidValue;
+    if (a.region && !a.store_only) {  // SM-local persistent schedule: <= 6 CTAs per SM
+        const int64_t g = std::min<int64_t>(blocks, (int64_t)num_sms() * HEC_TAIL_MINB);
+        if (a.diag) return launch_k(tail_sm_kernel<false, true>, dim3((unsigned)g), dim3(256), s, pdl, 0, a);
+        if (a.x_halo) return launch_k(tail_sm_kernel<true, false>, dim3((unsigned)g), dim3(256), s, pdl, 0, a);
+        return launch_k(tail_sm_kernel<false, false>, dim3((unsigned)g), dim3(256), s, pdl, 0, a);
+    }
     if (a.diag) return launch_k(tail_kernel<false, true>, dim3((unsigned)blocks), dim3(256), s, pdl, 0, a);
     if (a.x_halo) return launch_k(tail_kernel<true, false>, dim3((unsigned)blocks), dim3(256), s, pdl, 0, a);
     return launch_k(tail_kernel<false, false>, dim3((unsigned)blocks), dim3(256), s, pdl, 0, a);
+}
+
+// Concurrent tail: y[out_rows[p]] += tsum[p] once the ELL kernel and the
+// store-only tail kernel (on a second stream) have both finished -- the single
+// rounded addition y_i = ell_i + tail_i of the red.add path, bitwise.
+__global__ void __launch_bounds__(256) tail_combine_kernel(const int32_t* __restrict__ out_rows,
+                                                           const double* __restrict__ tsum, int32_t n,
+                                                           double* __restrict__ y) {
+    for (int32_t p = blockIdx.x * blockDim.x + threadIdx.x; p < n; p += gridDim.x * blockDim.x) {
+        double* yr = y + __ldg(out_rows + p);
+        *yr = *yr + __ldg(tsum + p);
+    }
+}
+
+cudaError_t launch_tail_combine(const int32_t* out_rows, const double* tsum, int32_t n, double* y, cudaStream_t s) {
+    if (n <= 0) return cudaSuccess;
+    int blocks = (n + 255) / 256;
+    if (blocks > num_sms() * 8) blocks = num_sms() * 8;
+    tail_combine_kernel<<<blocks, 256, 0, s>>>(out_rows, tsum, n, y);
+    return cudaGetLastError();
 }
 
 cudaError_t launch_pack(const int32_t* idx, int32_t n, const double* x, double* out,

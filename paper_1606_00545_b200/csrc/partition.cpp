@@ -436,10 +436,9 @@ hec_status hec_partition_order(const hec_csr* A, int32_t n_parts, int32_t method
         const Graph& gc = G.back();
         std::vector<int32_t> part(gc.n, 0), in(gc.n, 0), seen(gc.n, 0), coarse_order;
         int32_t in_stamp = 0, seen_stamp = 0;
-        if (method == HEC_ORDER_MULTILEVEL && gc.n <= kSpectralMax) {
-            // coarsest graph: spectral order, cut into n_parts consecutive
-            // pieces of (nearly) equal weight
-            coarse_order = spectral_order(gc);
+        if (method == HEC_ORDER_MULTILEVEL && gc.n <= kSpectralMax) coarse_order = spectral_order(gc);
+        if (method == HEC_ORDER_MULTILEVEL && !coarse_order.empty()) {
+            // the coarsest order cut into n_parts consecutive pieces of (nearly) equal weight
             int64_t acc = 0;
             int32_t p = 0;
             for (size_t i = 0; i < coarse_order.size(); ++i) {

@@ -112,3 +112,38 @@ def test_tail_jacobi_diag_regimes():
         ref = np.array([A.val[k] for i in range(A.n_rows) for k in range(A.row_ptr[i], A.row_ptr[i + 1])
                         if A.col[k] == i])
         assert d.cpu().numpy().tobytes() == ref.tobytes()
+
+
+@pytest.mark.parametrize("integer", [False, True])
+def test_tail_sm_local_schedule_bitwise(integer):
+    # the SM-local persistent schedule (whole launches of tails with more
+    # descriptors than one wave) claims the same descriptors: bitwise equal to
+    # the one-CTA-per-descriptor grid, over repeated launches (the claim
+    # counters reset themselves)
+    A = hecgen.powerlaw(1 << 18, integer_values=integer, seed=11)
+    x = hecgen.vector(A.n_cols, "int" if integer else "uniform", seed=4)
+    with env(HEC_TAIL_SM=1, HEC_FUSE_TAIL=0):
+        Ms = hec.from_csr(A)
+    with env(HEC_TAIL_SM=0, HEC_FUSE_TAIL=0):
+        Mp = hec.from_csr(A)
+    ys = [run(Ms, x) for _ in range(3)]
+    yp = run(Mp, x)
+    assert all(y.tobytes() == yp.tobytes() for y in ys)
+    if integer:
+        assert yp.tobytes() == oracle.csr_spmv(A, x).tobytes()
+    else:
+        assert np.all(np.abs(yp - oracle.csr_spmv(A, x)) <= oracle.tolerance(A, x))
+
+
+def test_tail_concurrent_stream_bitwise():
+    # HEC_TAIL_CONC=1: the tail kernel on its own stream beside the ELL kernel,
+    # sums into a scratch, one combine pass -- bitwise the ELL-then-tail y
+    A = hecgen.powerlaw(1 << 18, seed=12)
+    x = hecgen.vector(A.n_cols, "uniform", seed=5)
+    with env(HEC_TAIL_CONC=1, HEC_FUSE_TAIL=0):
+        Mc = hec.from_csr(A)
+    with env(HEC_TAIL_CONC=0, HEC_FUSE_TAIL=0):
+        Mp = hec.from_csr(A)
+    yp = run(Mp, x)
+    for _ in range(3):
+        assert run(Mc, x).tobytes() == yp.tobytes()
