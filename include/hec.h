@@ -319,9 +319,10 @@ hec_status hec_reorder_rcm(const hec_csr* A, int32_t* perm);
  *   HEC_ORDER_BISECT: recursive bisection by BFS level sets from a
  *     pseudo-peripheral vertex (George-Liu), lowest index first; parts
  *     balanced by rows (sizes within 1 when n_parts | n on connected graphs).
- *   HEC_ORDER_MULTILEVEL: multilevel k-way (heavy-edge matching, weighted
- *     level-set bisection of the coarsest graph, greedy boundary refinement
- *     at every level); parts balanced by nonzeros within 3%.
+ *   HEC_ORDER_MULTILEVEL: multilevel k-way (heavy-edge matching, spectral
+ *     order of the coarsest graph cut into equal-nonzero pieces, greedy
+ *     boundary refinement at every level; the best edge cut of 3 matching
+ *     orders); parts balanced by nonzeros within 3%.
  * Outputs (caller-allocated): perm[n] with perm[new] = old, the parts
  * contiguous in the new order, and part_ptr[n_parts + 1].  Partition B =
  * P A P^T (hec_permute) with HEC_PART_EXPLICIT and part_ptr.  Deterministic.

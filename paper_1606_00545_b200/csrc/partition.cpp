@@ -260,7 +260,8 @@ static Graph coarsen(const Graph& g, uint64_t seed, std::vector<int32_t>* cmap) 
     for (int32_t v = 0; v < n; ++v) key[v] = mix64(seed ^ (uint64_t)v);
     std::sort(visit.begin(), visit.end(), [&](int32_t a, int32_t b) { return key[a] < key[b]; });
     std::vector<int32_t> match(n, -1);
-    const int64_t cap = std::max<int64_t>(1, g.total / 64);  // no coarse vertex heavier than ~1/64 of the graph
+    const int64_t capdiv = std::getenv("HEC_PART_CAPDIV") ? std::atoll(std::getenv("HEC_PART_CAPDIV")) : 64;
+    const int64_t cap = std::max<int64_t>(1, g.total / capdiv);  // no coarse vertex heavier than ~1/64 of the graph
     for (int32_t v : visit) {
         if (match[v] >= 0) continue;
         int32_t best = -1, bw = -1;
@@ -419,44 +420,59 @@ hec_status hec_partition_order(const hec_csr* A, int32_t n_parts, int32_t method
         return HEC_OK;
     }
     try {
-        std::vector<Graph> G;
-        G.push_back(build_graph(v, method == HEC_ORDER_BISECT));
-        std::vector<std::vector<int32_t>> cmaps;
-        if (method == HEC_ORDER_MULTILEVEL) {
-            const int32_t stop = std::max<int32_t>(32 * n_parts, 256);
+        const Graph g0 = build_graph(v, method == HEC_ORDER_BISECT);
+        if (method == HEC_ORDER_BISECT) {
+            std::vector<int32_t> part(g0.n, 0), in(g0.n, 0), seen(g0.n, 0), order, all(g0.n);
+            int32_t in_stamp = 0, seen_stamp = 0;
+            std::iota(all.begin(), all.end(), 0);
+            recursive_bisect(g0, all, n_parts, 0, part, in, in_stamp, seen, seen_stamp, &order);
+            return order_from_parts({g0}, {}, order, part, n_parts, perm, part_ptr);
+        }
+        // multilevel: a few independent trials (matching orders), the smallest
+        // edge cut wins -- the result of one trial depends on where the
+        // coarsening happens to fold the graph
+        int trials = 3;
+        if (const char* e = std::getenv("HEC_PART_TRIALS")) trials = std::max(1, std::atoi(e));
+        int64_t best_cut = -1;
+        std::vector<int32_t> bperm(v.n_rows), bpp(n_parts + 1);
+        for (int trial = 0; trial < trials; ++trial) {
+            std::vector<Graph> G;
+            G.push_back(g0);
+            std::vector<std::vector<int32_t>> cmaps;
+            int32_t stop = std::max<int32_t>(32 * n_parts, 256);
+            if (const char* e = std::getenv("HEC_PART_STOP")) stop = std::max(2 * n_parts, std::atoi(e));  // tuning
+            const char* sd = std::getenv("HEC_PART_SEED");  // matching order seed (tuning)
+            const uint64_t seed = (sd ? std::atoll(sd) : 1606) + 7919ULL * trial;
             while (G.back().n > stop) {
                 std::vector<int32_t> cmap;
-                const char* sd = std::getenv("HEC_PART_SEED");  // matching order seed (tuning)
-                Graph c = coarsen(G.back(), (sd ? std::atoll(sd) : 1606) + G.size(), &cmap);
+                Graph c = coarsen(G.back(), seed + G.size(), &cmap);
                 if (c.n > (int32_t)(0.95 * G.back().n)) break;  // matching stalled
                 cmaps.push_back(std::move(cmap));
                 G.push_back(std::move(c));
             }
-        }
-        const Graph& gc = G.back();
-        std::vector<int32_t> part(gc.n, 0), in(gc.n, 0), seen(gc.n, 0), coarse_order;
-        int32_t in_stamp = 0, seen_stamp = 0;
-        if (method == HEC_ORDER_MULTILEVEL && gc.n <= kSpectralMax) coarse_order = spectral_order(gc);
-        if (method == HEC_ORDER_MULTILEVEL && !coarse_order.empty()) {
-            // the coarsest order cut into n_parts consecutive pieces of (nearly) equal weight
-            int64_t acc = 0;
-            int32_t p = 0;
-            for (size_t i = 0; i < coarse_order.size(); ++i) {
-                const int32_t v = coarse_order[i];
-                // advance while this vertex's midpoint lies past part p's share
-                // (and enough vertices remain for the parts after it)
-                while (p < n_parts - 1 && (acc + gc.vw[v] / 2) * n_parts >= (int64_t)(p + 1) * gc.total &&
-                       (int64_t)(coarse_order.size() - i) >= n_parts - p)
-                    ++p;
-                part[v] = p;
-                acc += gc.vw[v];
+            const Graph& gc = G.back();
+            std::vector<int32_t> part(gc.n, 0), in(gc.n, 0), seen(gc.n, 0), coarse_order;
+            int32_t in_stamp = 0, seen_stamp = 0;
+            if (gc.n <= kSpectralMax) coarse_order = spectral_order(gc);
+            if (!coarse_order.empty()) {
+                // the coarsest order cut into n_parts consecutive pieces of (nearly) equal weight
+                int64_t acc = 0;
+                int32_t p = 0;
+                for (size_t i = 0; i < coarse_order.size(); ++i) {
+                    const int32_t u = coarse_order[i];
+                    // advance while this vertex's midpoint lies past part p's share
+                    // (and enough vertices remain for the parts after it)
+                    while (p < n_parts - 1 && (acc + gc.vw[u] / 2) * n_parts >= (int64_t)(p + 1) * gc.total &&
+                           (int64_t)(coarse_order.size() - i) >= n_parts - p)
+                        ++p;
+                    part[u] = p;
+                    acc += gc.vw[u];
+                }
+            } else {
+                std::vector<int32_t> all(gc.n);
+                std::iota(all.begin(), all.end(), 0);
+                recursive_bisect(gc, all, n_parts, 0, part, in, in_stamp, seen, seen_stamp, &coarse_order);
             }
-        } else {
-            std::vector<int32_t> all(gc.n);
-            std::iota(all.begin(), all.end(), 0);
-            recursive_bisect(gc, all, n_parts, 0, part, in, in_stamp, seen, seen_stamp, &coarse_order);
-        }
-        if (method == HEC_ORDER_MULTILEVEL) {
             refine(gc, n_parts, part, 8);
             for (int l = (int)G.size() - 2; l >= 0; --l) {
                 std::vector<int32_t> fine(G[l].n);
@@ -464,8 +480,20 @@ hec_status hec_partition_order(const hec_csr* A, int32_t n_parts, int32_t method
                 part.swap(fine);
                 refine(G[l], n_parts, part, 4);
             }
+            int64_t cut = 0;
+            for (int32_t u = 0; u < g0.n; ++u)
+                for (int64_t k = g0.xadj[u]; k < g0.xadj[u + 1]; ++k)
+                    if (part[g0.adj[(size_t)k]] != part[u]) cut += g0.ew[(size_t)k];
+            if (best_cut < 0 || cut < best_cut) {
+                st = order_from_parts(G, cmaps, coarse_order, part, n_parts, bperm.data(), bpp.data());
+                if (st != HEC_OK) continue;
+                best_cut = cut;
+            }
         }
-        return order_from_parts(G, cmaps, coarse_order, part, n_parts, perm, part_ptr);
+        if (best_cut < 0) return fail(HEC_ERR_PARTS, "a part came out empty");
+        std::memcpy(perm, bperm.data(), sizeof(int32_t) * (size_t)v.n_rows);
+        std::memcpy(part_ptr, bpp.data(), sizeof(int32_t) * (size_t)(n_parts + 1));
+        return HEC_OK;
     } catch (const std::bad_alloc&) {
         return fail(HEC_ERR_NOMEM, "host allocation failed in hec_partition_order");
     }
