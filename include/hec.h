@@ -367,7 +367,8 @@ hec_status hec_spmv_dist(hec_dist D, const double* x_local, double* y_local, voi
  * hec_spmv_host): copies x_host_local (n_loc doubles, pageable or pinned) to a
  * device staging buffer on `stream`, runs hec_spmv_dist, copies y back into
  * y_host_local (n_loc doubles) and synchronises `stream`.  Staging buffers are
- * allocated by the first call and kept in the handle. */
+ * allocated by the first call and kept in the handle (calls on one handle must
+ * therefore not overlap). */
 hec_status hec_spmv_dist_host(hec_dist D, const double* x_host_local, double* y_host_local, void* stream);
 
 /* The handle's NCCL communicator: *nranks = ncclCommCount (0 when the handle

@@ -31,7 +31,7 @@ static void release(hec_matrix_s* m) {
         cudaSetDevice(m->device);
         if (m->ws && m->ws_free) m->ws_free(m->ws);
         void* ptrs[] = {m->d_ell_col, m->d_ell_val, m->d_tail_out, m->d_tail_blk, m->d_fuse, m->d_tail_region,
-                        m->d_tail_ctr, m->d_tsum,
+                        m->d_tail_ctr, m->d_tsum, m->d_tail_units, m->d_tail_uwidx,
                         m->d_tail_warp, m->d_tail_col, m->d_tail_val, m->d_rowmap, m->d_coo_row, m->d_stage_x,
                         m->d_stage_y};
         for (void* p : ptrs)
@@ -246,34 +246,53 @@ hec_status make_matrix(HostHec&& h, int32_t device, cudaStream_t s, const int32_
         if ((st = dmalloc_copy(&m->d_tail_warp, warp.data(), warp.size(), s, &bytes))) return st;
         if ((st = dmalloc_copy(&m->d_tail_col, dcol.data(), dcol.size(), s, &bytes))) return st;
         if ((st = dmalloc_copy(&m->d_tail_val, dval.data(), dval.size(), s, &bytes))) return st;
-        // SM-local persistent schedule for big tails (more descriptors than one
-        // wave): one region of descriptors per SM, equal stored entries each.
-        // Opt-in (HEC_TAIL_SM=1): it lifts the gathers' L1 hit rate 20% -> 57%
-        // but measured slower (power-law tail 320 vs 264 us: the per-descriptor
-        // barriers idle the early warps), DESIGN §5
+        // SM-local persistent schedule, warp by warp (opt-in HEC_TAIL_WARP=1,
+        // big tails: more descriptors than one wave): warp units cut into one
+        // region per SM with equal entries.  DESIGN §5 has the measurements.
         int n_sm = 0;
         cudaDeviceGetAttribute(&n_sm, cudaDevAttrMultiProcessorCount, device);
-        bool sm_sched = false;
-        if (const char* e = std::getenv("HEC_TAIL_SM"))
-            sm_sched = n_sm > 0 && (int64_t)blk.size() > (int64_t)n_sm * 6 && std::atoi(e) != 0;
-        if (sm_sched) {
-            std::vector<int64_t> wsum(blk.size() + 1, 0);  // entries (padded) per descriptor, prefix
+        bool warp_sched = false;
+        if (const char* e = std::getenv("HEC_TAIL_WARP"))
+            warp_sched = n_sm > 0 && (int64_t)blk.size() > (int64_t)n_sm * 6 && std::atoi(e) != 0;
+        if (warp_sched) {
+            std::vector<int4> units;
+            std::vector<int32_t> uwidx;
+            std::vector<int64_t> uent(1, 0);  // prefix of the units' (padded) entries
             for (size_t d = 0; d < blk.size(); ++d) {
-                int64_t e = 0;
-                for (int w = 0; w < 8; ++w) e += (int64_t)warp[(size_t)blk[d].w + w].y * kTailChunk;
-                wsum[d + 1] = wsum[d] + e;
+                const int g = blk[d].z, G = 1 << g, cnt = blk[d].y;
+                const int32_t w0 = blk[d].w;
+                if (G <= 32) {
+                    for (int w = 0; w < 8; ++w) {
+                        if (((32 * w) >> g) >= cnt) break;  // no rows in this warp (nor later ones)
+                        units.push_back(warp[(size_t)w0 + w]);
+                        uwidx.push_back(w0 + w);
+                        uent.push_back(uent.back() + (int64_t)warp[(size_t)w0 + w].y * kTailChunk);
+                    }
+                } else {
+                    const int nw = G >> 5;
+                    for (int r = 0; r < cnt; ++r) {
+                        int64_t e = 0;
+                        for (int j = 0; j < nw; ++j) e += (int64_t)warp[(size_t)w0 + r * nw + j].y * kTailChunk;
+                        units.push_back(warp[(size_t)w0 + r * nw]);
+                        uwidx.push_back(w0 + r * nw);
+                        uent.push_back(uent.back() + e);
+                    }
+                }
             }
             std::vector<int64_t> reg((size_t)n_sm + 1, 0);
             for (int r = 1; r < n_sm; ++r) {
-                const int64_t target = wsum.back() * r / n_sm;
-                reg[r] = std::lower_bound(wsum.begin(), wsum.end(), target) - wsum.begin();
+                const int64_t target = uent.back() * r / n_sm;
+                reg[r] = std::lower_bound(uent.begin(), uent.end(), target) - uent.begin();
                 reg[r] = std::max(reg[r], reg[r - 1]);
             }
-            reg[n_sm] = (int64_t)blk.size();
+            reg[n_sm] = (int64_t)units.size();
+            if ((st = dmalloc_copy(&m->d_tail_units, units.data(), units.size(), s, &bytes))) return st;
+            if ((st = dmalloc_copy(&m->d_tail_uwidx, uwidx.data(), uwidx.size(), s, &bytes))) return st;
             if ((st = dmalloc_copy(&m->d_tail_region, reg.data(), reg.size(), s, &bytes))) return st;
             std::vector<unsigned int> zero((size_t)n_sm + 1, 0u);
             if ((st = dmalloc_copy(&m->d_tail_ctr, zero.data(), zero.size(), s, &bytes))) return st;
             m->tail_regions = n_sm;
+            HEC_CUDA_TRY(cudaStreamSynchronize(s));  // units / reg die after this scope
         }
         // concurrent tail for big tails (opt-in HEC_TAIL_CONC=1): measured slower
         // (power-law 0.484 vs 0.436 ms: the two kernels share the memory system
@@ -383,6 +402,8 @@ static hec_status launch_chunks(const hec_matrix_s* A, int c, const double* x, c
     t.omega = omega;
     if (c < 0 && A->tail_regions > 0) {  // whole launch: the SM-local persistent schedule
         t.region = A->d_tail_region;
+        t.units = A->d_tail_units;
+        t.unit_widx = A->d_tail_uwidx;
         t.n_regions = A->tail_regions;
         t.region_ctr = A->d_tail_ctr;
         t.region_done = A->d_tail_ctr + A->tail_regions;

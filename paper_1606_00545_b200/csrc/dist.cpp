@@ -577,6 +577,8 @@ int64_t dist_n_local(hec_dist_s* D) { return (int64_t)D->r1 - D->r0; }
 
 bool dist_is_local(hec_dist_s* D) { return D->local; }
 
+int32_t dist_rank(hec_dist_s* D) { return D->rank; }
+
 ncclComm_t dist_comm(hec_dist_s* D) { return D->comm; }
 
 int32_t dist_parts(hec_dist_s* D) { return D->n_parts; }

@@ -160,7 +160,9 @@ struct hec_matrix_s {
     std::vector<int4> h_tail_blk;      // descriptors {first row position, count, lg, first warp}
     std::vector<int4> h_tail_warp;     // 8 per descriptor: {first entry, iterations, first row, count << 8 | lg}
     int4* d_tail_warp = nullptr;
-    int64_t* d_tail_region = nullptr;  // SM-local tail schedule: [n_regions + 1] descriptor boundaries
+    int64_t* d_tail_region = nullptr;  // SM-local tail schedule: [n_regions + 1] unit boundaries
+    int4* d_tail_units = nullptr;      // SM-local tail schedule: each warp unit's first warp meta
+    int32_t* d_tail_uwidx = nullptr;   // ... and its index in the warp-meta array
     unsigned int* d_tail_ctr = nullptr;  // [n_regions] claim counters + 1 done counter
     int32_t tail_regions = 0;
     // concurrent tail (big tails, whole plain launches): the tail kernel on its
@@ -294,9 +296,12 @@ struct TailArgs {
     bool store_only = false;  // store the row sums instead of adding them: into y (small tails first,
                               // the ELL kernel adds them) or into tsum (concurrent tail, combined after)
     double* tsum = nullptr;   // [tail rows], indexed by device row position
-    // SM-local persistent schedule (tail_sm_kernel; whole launches only): descriptors
-    // [region[r], region[r+1]) are SM r's, claimed through region_ctr[r]
+    // SM-local persistent schedule (tail_warp_kernel; whole launches only): warp
+    // units [region[r], region[r+1]) are SM r's, claimed through region_ctr[r];
+    // units[u] = {first warp-meta index, warp metas of the unit}
     const int64_t* region = nullptr;
+    const int4* units = nullptr;        // per unit: its first warp meta (carried inline)
+    const int32_t* unit_widx = nullptr; // per unit: that meta's index in `warp`
     int32_t n_regions = 0;
     unsigned int* region_ctr = nullptr;  // [n_regions], zero between launches
     unsigned int* region_done = nullptr; // CTA completion counter (self-resetting)

@@ -375,24 +375,13 @@ __global__ void __launch_bounds__(256, EPI == EPI_JACOBI ? HEC_JAC_MINB : 0) ell
 #define HEC_TAIL_BATCH 8  // HEC_TAIL_V 4: iterations whose loads are issued together
 #endif
 
-template <bool HALO, bool JACOBI>
-__device__ __forceinline__ void tail_desc(const TailArgs& a, int64_t desc, int tid, uint64_t pol, double* wsum) {
-    // one load per warp: {first entry, iterations, first row, count << 8 | lg}
-    // (warp-chunk layout, hec_internal.h) -- no dependent metadata loads
-    // before the stream starts
-    const int4 wm = __ldg(a.warp + desc * 8 + (tid >> 5));
-    const int lg = wm.w & 255;
-    const int G = 1 << lg;
-    const int lane = tid & (G - 1);
-    const int grp = tid >> lg;
+// One warp's pairs in the warp-chunk layout (hec_internal.h): wm = {first
+// entry, iterations, ...}; lane l reads the pair at base + 64 i + 2 l.  Returns
+// the lane's partial sum (its row's entries 2 (i G + lr), +1 in order).
+template <bool HALO>
+__device__ __forceinline__ double warp_chunk_sum(const TailArgs& a, int4 wm, int l, uint64_t pol) {
     double acc = 0.0;
-    double* yp = nullptr;
-    int32_t orow = 0;
-    const bool active = grp < (wm.w >> 8);
-    if (active && lane == 0) {
-        orow = __ldg(a.out_rows + wm.z + grp);
-        yp = a.y + orow;
-    }
+    const int tid = l;  // only tid & 31 is used below
     {
         // every warp-wide load is one whole 256-byte (index) / 512-byte (value)
         // segment, read once: streamed past L1 with the L2 evict-first policy,
@@ -441,6 +430,27 @@ __device__ __forceinline__ void tail_desc(const TailArgs& a, int64_t desc, int t
         }
 #endif
     }
+    return acc;
+}
+
+template <bool HALO, bool JACOBI>
+__device__ __forceinline__ void tail_desc(const TailArgs& a, int64_t desc, int tid, uint64_t pol, double* wsum) {
+    // one load per warp: {first entry, iterations, first row, count << 8 | lg}
+    // (warp-chunk layout, hec_internal.h) -- no dependent metadata loads
+    // before the stream starts
+    const int4 wm = __ldg(a.warp + desc * 8 + (tid >> 5));
+    const int lg = wm.w & 255;
+    const int G = 1 << lg;
+    const int lane = tid & (G - 1);
+    const int grp = tid >> lg;
+    double* yp = nullptr;
+    int32_t orow = 0;
+    const bool active = grp < (wm.w >> 8);
+    if (active && lane == 0) {
+        orow = __ldg(a.out_rows + wm.z + grp);
+        yp = a.y + orow;
+    }
+    double acc = warp_chunk_sum<HALO>(a, wm, tid & 31, pol);
     if (lg <= 5) {
         for (int off = G >> 1; off > 0; off >>= 1) acc += __shfl_xor_sync(0xffffffffu, acc, off, G);
     } else {
@@ -491,48 +501,109 @@ __global__ void __launch_bounds__(256, HEC_TAIL_MINB) tail_kernel(TailArgs a) {
     tail_desc<HALO, JACOBI>(a, a.blk_begin + blockIdx.x, threadIdx.x, pol, wsum);
 }
 
-// SM-local persistent schedule (whole-matrix launches of big tails): the
-// descriptors are cut into one contiguous region per SM (equal entries), and
-// the CTAs resident on an SM claim its region's descriptors in order through
-// a counter -- so the 6 CTAs sharing an SM's L1 work on neighbouring rows and
-// share the x window their gathers touch (the stream bypasses L1, leaving L1
-// to x).  A CTA that runs out of its SM's work steals from the next regions:
-// every descriptor is claimed exactly once whatever the CTA placement.  The
-// last CTA to finish resets the counters (the next launch is stream-ordered).
-// Same descriptors, lanes and red.add per row as tail_kernel: bitwise equal.
+// SM-local persistent schedule, warp by warp (whole-matrix launches of big
+// tails; opt-in HEC_TAIL_WARP=1): the tail's WARP UNITS (one warp-chunk warp
+// of rows with G <= 32 lanes; or all G/32 warps of one row with G > 32, which
+// the warp then walks one after the other) are cut into one contiguous region
+// per SM, and each resident warp claims the next unit of its SM's region
+// through a counter (the next claim issued before the current unit's work) --
+// so the warps sharing an SM's L1 gather from neighbouring rows' x window, with
+// no barrier between units.  A warp that runs out of its SM's work steals from
+// the next regions: every unit is claimed exactly once whatever the placement;
+// the last warp to finish resets the counters.  Same lanes, partial sums,
+// reduction order and one red.add per row as tail_kernel: bitwise equal.
 __device__ __forceinline__ uint32_t sm_id() {
     uint32_t r;
     asm volatile("mov.u32 %0, %%smid;" : "=r"(r));
     return r;
 }
 
+// One warp unit: wm0 = the unit's first warp meta (carried in the unit list,
+// so no dependent metadata load); its index in the warp-meta array is read
+// for the row-in-descriptor and, for rows over several warps, the next metas.
 template <bool HALO, bool JACOBI>
-__global__ void __launch_bounds__(256, HEC_TAIL_MINB) tail_sm_kernel(TailArgs a) {
-    __shared__ double wsum[8];
-    __shared__ int64_t claim;
-    const uint64_t pol = policy_evict_first();
-    const int R = a.n_regions;
-    const int home = (int)(sm_id() % (uint32_t)R);
-    for (int k = 0; k < R; ++k) {
-        const int r = home + k < R ? home + k : home + k - R;
-        const int64_t r0 = __ldg(a.region + r), r1 = __ldg(a.region + r + 1);
-        if (threadIdx.x == 0) claim = r0 + (int64_t)atomicAdd(a.region_ctr + r, 1u);
-        __syncthreads();
-        int64_t d = claim;
-        while (d < r1) {
-            // claim the next descriptor now; its atomic's latency overlaps this one's work
-            unsigned int nxt = 0;
-            if (threadIdx.x == 0) nxt = atomicAdd(a.region_ctr + r, 1u);
-            tail_desc<HALO, JACOBI>(a, d, threadIdx.x, pol, wsum);
-            __syncthreads();  // everybody is done with this descriptor (wsum, claim)
-            if (threadIdx.x == 0) claim = r0 + (int64_t)nxt;
-            __syncthreads();
-            d = claim;
+__device__ __forceinline__ void tail_unit(const TailArgs& a, int4 wm0, int64_t u, int l, uint64_t pol) {
+    const int lg = wm0.w & 255, G = 1 << lg;
+    const int32_t widx = __ldg(a.unit_widx + u);
+    const int grp = (((widx & 7) << 5) + l) >> lg;  // the lane's row within its descriptor
+    double acc;
+    if (G <= 32) {
+        acc = warp_chunk_sum<HALO>(a, wm0, l, pol);
+        for (int off = G >> 1; off > 0; off >>= 1) acc += __shfl_xor_sync(0xffffffffu, acc, off, G);
+    } else {  // one row over G / 32 warps: each a full-warp tree, added in warp order
+        acc = 0.0;
+        for (int j = 0; j < (G >> 5); ++j) {
+            double p = warp_chunk_sum<HALO>(a, j == 0 ? wm0 : __ldg(a.warp + widx + j), l, pol);
+            for (int off = 16; off > 0; off >>= 1) p += __shfl_xor_sync(0xffffffffu, p, off);
+            acc = j == 0 ? p : acc + p;
         }
     }
-    if (threadIdx.x == 0) {
+    const bool lead = (l & (G - 1)) == 0 && grp < (wm0.w >> 8);
+    if (lead) {
+        const int32_t orow = __ldg(a.out_rows + wm0.z + grp);
+        const double q = JACOBI ? -__dmul_rn(a.omega, __ddiv_rn(acc, __ldg(a.diag + orow))) : __dmul_rn(a.alpha, acc);
+        asm volatile("griddepcontrol.wait;" ::: "memory");
+        asm volatile("red.global.add.f64 [%0], %1;" ::"l"(a.y + orow), "d"(q) : "memory");
+    }
+}
+
+// A region's units, claimed two ahead: while unit i runs, the claim for i + 2
+// is in flight and unit i + 1's meta (claimed an iteration ago) is loading.
+template <bool HALO, bool JACOBI>
+__device__ __forceinline__ void tail_region(const TailArgs& a, int r, int l, uint64_t pol) {
+    const int64_t r0 = __ldg(a.region + r), r1 = __ldg(a.region + r + 1);
+    unsigned int c0 = 0, c1 = 0;
+    if (l == 0) {
+        c0 = atomicAdd(a.region_ctr + r, 1u);
+        c1 = atomicAdd(a.region_ctr + r, 1u);
+    }
+    int64_t u = r0 + __shfl_sync(0xffffffffu, c0, 0);
+    if (u >= r1) return;
+    int4 wm = __ldg(a.units + u);
+    int64_t un = r0 + __shfl_sync(0xffffffffu, c1, 0);
+    while (true) {
+        unsigned int c2 = 0;
+        if (l == 0 && un < r1) c2 = atomicAdd(a.region_ctr + r, 1u);
+        const int4 wn = un < r1 ? __ldg(a.units + un) : make_int4(0, 0, 0, 0);
+        tail_unit<HALO, JACOBI>(a, wm, u, l, pol);
+        if (un >= r1) break;
+        u = un;
+        wm = wn;
+        un = r0 + __shfl_sync(0xffffffffu, c2, 0);
+    }
+}
+
+template <bool HALO, bool JACOBI>
+__global__ void __launch_bounds__(256, HEC_TAIL_MINB) tail_warp_kernel(TailArgs a) {
+    const uint64_t pol = policy_evict_first();
+    const int l = threadIdx.x & 31;
+    const int R = a.n_regions;
+    const int home = (int)(sm_id() % (uint32_t)R);
+    tail_region<HALO, JACOBI>(a, home, l, pol);
+    // then steal: the lanes read every region's counter at once (one round
+    // trip per 32 regions, starting after home) and the warp joins the first
+    // region with work left; done when none has any
+    while (true) {
+        int found = -1;
+        for (int base = 1; base < R && found < 0; base += 32) {
+            const int k = base + l;
+            const int r = home + k < R ? home + k : home + k - R;
+            bool has = false;
+            if (k < R)
+                has = __ldg(a.region + r) + (int64_t)*(volatile const unsigned int*)(a.region_ctr + r) <
+                      __ldg(a.region + r + 1);
+            const unsigned int m = __ballot_sync(0xffffffffu, has);
+            if (m) {
+                const int kk = base + __ffs(m) - 1;
+                found = home + kk < R ? home + kk : home + kk - R;
+            }
+        }
+        if (found < 0) break;
+        tail_region<HALO, JACOBI>(a, found, l, pol);
+    }
+    if (l == 0) {
         __threadfence();
-        if (atomicAdd(a.region_done, 1u) == gridDim.x - 1) {
+        if (atomicAdd(a.region_done, 1u) == gridDim.x * (blockDim.x >> 5) - 1) {
             for (int r = 0; r < R; ++r) a.region_ctr[r] = 0;
             __threadfence();
             *a.region_done = 0;
@@ -749,11 +820,11 @@ cudaError_t launch_tail(const TailArgs& a, cudaStream_t s) {
     const bool pdl = tail_pdl() && !a.store_only;  // store_only runs first: an ordinary launch
     if (a.diag && a.x_halo) return cudaErrorInvalidValue;
     if (a.store_only && (a.diag || a.x_halo || a.alpha != 1.0)) return cudaErrorInvalidValue;
-    if (a.region && !a.store_only) {  // SM-local persistent schedule: <= 6 CTAs per SM
+    if (a.region && !a.store_only) {  // SM-local persistent schedule, warp by warp: 6 CTAs per SM
         const int64_t g = std::min<int64_t>(blocks, (int64_t)num_sms() * HEC_TAIL_MINB);
-        if (a.diag) return launch_k(tail_sm_kernel<false, true>, dim3((unsigned)g), dim3(256), s, pdl, 0, a);
-        if (a.x_halo) return launch_k(tail_sm_kernel<true, false>, dim3((unsigned)g), dim3(256), s, pdl, 0, a);
-        return launch_k(tail_sm_kernel<false, false>, dim3((unsigned)g), dim3(256), s, pdl, 0, a);
+        if (a.diag) return launch_k(tail_warp_kernel<false, true>, dim3((unsigned)g), dim3(256), s, pdl, 0, a);
+        if (a.x_halo) return launch_k(tail_warp_kernel<true, false>, dim3((unsigned)g), dim3(256), s, pdl, 0, a);
+        return launch_k(tail_warp_kernel<false, false>, dim3((unsigned)g), dim3(256), s, pdl, 0, a);
     }
     if (a.diag) return launch_k(tail_kernel<false, true>, dim3((unsigned)blocks), dim3(256), s, pdl, 0, a);
     if (a.x_halo) return launch_k(tail_kernel<true, false>, dim3((unsigned)blocks), dim3(256), s, pdl, 0, a);

@@ -327,6 +327,7 @@ hec_status dist_spmv_launch(hec_dist_s* D, const double* x, double* y, cudaStrea
 hec_status dist_local_spmv_launch(hec_dist_s** D, int32_t n, const double* const* xs, double* const* ys,
                                   cudaStream_t s);
 bool dist_is_local(hec_dist_s* D);
+int32_t dist_rank(hec_dist_s* D);
 int64_t dist_n_local(hec_dist_s* D);
 ncclComm_t dist_comm(hec_dist_s* D);
 int32_t dist_parts(hec_dist_s* D);
@@ -775,7 +776,7 @@ static hec_status dist_local_solve(int method, hec_dist* D, int32_t n, const dou
                                    hec_solve_info* info) {
     if (!D || n < 1 || !b_locals || !x_locals) return fail(HEC_ERR_ARG, "NULL argument");
     for (int32_t p = 0; p < n; ++p) {
-        if (!D[p] || !dist_is_local(D[p]) || dist_parts(D[p]) != n)
+        if (!D[p] || !dist_is_local(D[p]) || dist_parts(D[p]) != n || dist_rank(D[p]) != p)
             return fail(HEC_ERR_STATE, "handles must be the n ranks from hec_dist_create_local, in rank order");
         if (dist_n_local(D[p]) > 0 && (!b_locals[p] || !x_locals[p])) return fail(HEC_ERR_ARG, "NULL segment");
     }

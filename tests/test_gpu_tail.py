@@ -115,16 +115,18 @@ def test_tail_jacobi_diag_regimes():
 
 
 @pytest.mark.parametrize("integer", [False, True])
-def test_tail_sm_local_schedule_bitwise(integer):
-    # the SM-local persistent schedule (whole launches of tails with more
-    # descriptors than one wave) claims the same descriptors: bitwise equal to
-    # the one-CTA-per-descriptor grid, over repeated launches (the claim
-    # counters reset themselves)
+def test_tail_sm_local_warp_schedule_bitwise(integer):
+    # the SM-local persistent schedule, warp by warp (whole launches of tails
+    # with more descriptors than one wave): the same warp chunks, partial sums
+    # and reduction order -- bitwise equal to the one-CTA-per-descriptor grid,
+    # over repeated launches (the claim counters reset themselves)
     A = hecgen.powerlaw(1 << 18, integer_values=integer, seed=11)
+    if not integer:  # long rows (G > 32: one warp walks the row's G/32 warp chunks)
+        A = hecgen.degree_sorted(A)
     x = hecgen.vector(A.n_cols, "int" if integer else "uniform", seed=4)
-    with env(HEC_TAIL_SM=1, HEC_FUSE_TAIL=0):
+    with env(HEC_TAIL_WARP=1, HEC_FUSE_TAIL=0):
         Ms = hec.from_csr(A)
-    with env(HEC_TAIL_SM=0, HEC_FUSE_TAIL=0):
+    with env(HEC_TAIL_WARP=0, HEC_FUSE_TAIL=0):
         Mp = hec.from_csr(A)
     ys = [run(Ms, x) for _ in range(3)]
     yp = run(Mp, x)
