@@ -150,8 +150,8 @@ def ncu_traffic_live(config: str, launches_per_step: int, timeout_s: float = 300
         return None, None, None, "ncu not found"
     log = tempfile.NamedTemporaryFile(prefix="hec_ncu_", suffix=".csv", delete=False).name
     cmd = [ncu, "--metrics", "dram__bytes_read.sum,dram__bytes_write.sum,gpu__time_duration.sum",
-           "--clock-control", "none", "--csv", "--log-file", log, "-k", "regex:ell_kernel|tail_kernel",
-           sys.executable, os.path.abspath(__file__), "--profile", "--config", config,
+           "--clock-control", "none", "--csv", "--log-file", log, "--kernel-name-base", "demangled",
+           "-k", "regex:hec::", sys.executable, os.path.abspath(__file__), "--profile", "--config", config,
            "--steps", "3", "--warmup", "2"]
     try:
         r = subprocess.run(cmd, stdout=subprocess.DEVNULL, stderr=subprocess.PIPE, timeout=timeout_s, text=True)
@@ -171,16 +171,21 @@ def ncu_traffic_live(config: str, launches_per_step: int, timeout_s: float = 300
     for row in rows[1:]:
         k = per.setdefault(int(row[iid]), {"kernel": row[ik]})
         k[row[im]] = float(row[iv].replace(",", ""))
-    ids = sorted(per)[-launches_per_step:]
+    # every libhec kernel of the child's 5 SpMV steps (2 warm-up + 3): the
+    # launches per step are counted, not assumed; the last step's are summed
+    counted = len(per) / 5.0
+    lps = int(round(counted)) if counted >= 1 else launches_per_step
+    ids = sorted(per)[-lps:]
     split, times = {}, {}
     for i in ids:
         k = per[i]
-        name = k["kernel"].split("<")[0].replace("void ", "").strip()
-        split[name] = int(k.get("dram__bytes_read.sum", 0) + k.get("dram__bytes_write.sum", 0))
-        times[name] = round(k.get("gpu__time_duration.sum", 0.0) * 1e-6, 5)  # ns -> ms
+        name = k["kernel"].replace("void ", "").split("<")[0].split("(")[0].replace("hec::", "").strip()
+        split[name] = split.get(name, 0) + int(k.get("dram__bytes_read.sum", 0) + k.get("dram__bytes_write.sum", 0))
+        times[name] = round(times.get(name, 0.0) + k.get("gpu__time_duration.sum", 0.0) * 1e-6, 5)  # ns -> ms
+    times["launches_per_step_counted"] = counted
     return (sum(split.values()), split, times,
-            f"measured in this run: ncu --metrics dram__bytes_read.sum,dram__bytes_write.sum (last of 5 steps, "
-            f"{launches_per_step} launch(es)/step)")
+            f"measured in this run: ncu --metrics dram__bytes_read.sum,dram__bytes_write.sum over every libhec "
+            f"kernel (hec::*) of 5 steps: {counted:g} launch(es)/step counted; the last step's summed")
 
 
 class L2Flusher:
@@ -555,6 +560,10 @@ def run_single(args):
                 tr, split, src = ncu_traffic_committed(args.config)
                 src = f"{src} (live pass unavailable: {reason})"
                 ncu_ms = None
+        if ncu_ms and "launches_per_step_counted" in ncu_ms:
+            counted = ncu_ms.pop("launches_per_step_counted")
+            roof["gpu_launches_evidence"] = {"ncu_launches_per_step": counted, "claimed_per_step": launches_per_step,
+                                             "agrees": abs(counted - launches_per_step) < 1e-9}
         roof.update({"traffic": tr, "traffic_by_kernel": split, "traffic_source": src,
                      "ncu_ms_by_kernel": ncu_ms, "csrc_sha": csrc_hash()})
         if tr:

@@ -351,7 +351,7 @@ static void refine(const Graph& g, int32_t P, std::vector<int32_t>& part, int pa
                         best = q;
                     }
                 }
-                if (best != own) {
+                if (best != own && pw[own] > g.vw[v]) {  // never empty a part
                     part[v] = best;
                     pw[own] -= g.vw[v];
                     pw[best] += g.vw[v];
