@@ -623,6 +623,35 @@ def time_dist_steps(D, x, y, stream, K, flusher, dist, torch):
     return per.cpu().numpy(), wall
 
 
+def dist_overlap(D, x, y, stream, flusher, dist, torch, reps=10):
+    """The a10 overlap evidence: hec_dist_set_timing's events on each rank
+    (interior rows end / exchange + boundary rows end, both from the call's
+    start), median of `reps` aligned calls; per rank, then the max over ranks
+    of the exposed exchange time max(0, comm - interior)."""
+    D.set_timing(True)
+    align = torch.zeros(1, dtype=torch.float32, device="cuda")
+    it, co = [], []
+    for _ in range(reps):
+        with torch.cuda.stream(stream):
+            if flusher:
+                flusher()
+            dist.all_reduce(align)
+            D.spmv(x, y, stream)
+        a, b = D.phase_times()
+        it.append(a)
+        co.append(b)
+    D.set_timing(False)
+    mine = torch.tensor([statistics.median(it), statistics.median(co)], dtype=torch.float64, device="cuda")
+    allr = [torch.zeros_like(mine) for _ in range(dist.get_world_size())]
+    dist.all_gather(allr, mine)
+    per = [(round(float(t[0]), 5), round(float(t[1]), 5)) for t in allr]
+    exposed = [max(0.0, c - i) for i, c in per if c >= 0]
+    return {"what": "per rank: ms from the call's start to the end of the interior rows / of exchange + boundary "
+                    "rows (CUDA events on the two streams, hec_dist_phase_times), median of 10 aligned calls",
+            "interior_ms": [p[0] for p in per], "exchange_boundary_ms": [p[1] for p in per],
+            "exposed_ms_max": round(max(exposed), 5) if exposed else None}
+
+
 def dist_parity(A, x_h, y, r0, r1, dist, torch):
     """Every row of every rank against the serial C oracle O1 (tolerance
     1e-12 (|A||x|)_i): each rank checks its own rows [r0, r1); the bad-row
@@ -700,12 +729,13 @@ def run_multi(args):
             sampler.__exit__()
         D.check()  # raises if a peer-memory halo wait timed out (the results would be garbage)
         par = dist_parity(A, x_h, y, r0, r1, dist, torch)
+        overlap = dist_overlap(D, x, y, stream, flusher, dist, torch) if world > 1 else None
         ms_mean = float(np.mean(per))
         results[t] = {"ms_per_step": round(ms_mean, 5), "median_ms": round(float(np.median(per)), 5),
                       "p10_ms": round(float(np.percentile(per, 10)), 5),
                       "p90_ms": round(float(np.percentile(per, 90)), 5),
                       "gflops": round(2 * A.nnz / (ms_mean * 1e-3) / 1e9, 2),
-                      "wall_s_between_barriers": round(wall, 4), "parity": par,
+                      "wall_s_between_barriers": round(wall, 4), "parity": par, "overlap": overlap,
                       "launches_per_step": D.info.launches, "clocks": sampler.summary() if sampler else None}
     head = "p2p" if "p2p" in results and "ms_per_step" in results["p2p"] else \
         ("nccl" if "nccl" in results else order[-1])

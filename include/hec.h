@@ -371,6 +371,18 @@ hec_status hec_spmv_dist(hec_dist D, const double* x_local, double* y_local, voi
  * therefore not overlap). */
 hec_status hec_spmv_dist_host(hec_dist D, const double* x_host_local, double* y_host_local, void* stream);
 
+/* Phase timing of hec_spmv_dist (the overlap evidence of SURVEY §8(a) a10):
+ * with timing on, every call records CUDA events at its start (caller's
+ * stream), at the end of the interior rows (caller's stream) and at the end
+ * of the exchange + boundary rows (communication stream).
+ * hec_dist_phase_times (synchronises them) gives, for the LAST call, both ends
+ * in ms from the call's start: interior_ms, and comm_ms (-1 when the call had
+ * no exchange).  comm_ms <= interior_ms means the exchange and the boundary
+ * rows were entirely hidden behind the interior rows.  HEC_ERR_STATE without
+ * a timed call. */
+hec_status hec_dist_set_timing(hec_dist D, int32_t enable);
+hec_status hec_dist_phase_times(hec_dist D, float* interior_ms, float* comm_ms);
+
 /* The handle's NCCL communicator: *nranks = ncclCommCount (0 when the handle
  * has none: P = 1 or a peer-memory-only handle), *version = ncclGetVersion. */
 hec_status hec_dist_comm_size(hec_dist D, int32_t* nranks, int32_t* version);

@@ -51,6 +51,12 @@ struct hec_dist_s {
     void (*ws_free)(void*) = nullptr;
     double* d_stage_x = nullptr;        // hec_spmv_dist_host staging (first call)
     double* d_stage_y = nullptr;
+    // phase timing (hec_dist_set_timing): events at the call's start and at the
+    // end of the interior rows (caller's stream) and of exchange + boundary rows
+    // (communication stream)
+    bool timing = false;
+    cudaEvent_t tm_start = nullptr, tm_interior = nullptr, tm_comm = nullptr;
+    bool tm_valid = false, tm_comm_valid = false;
 };
 
 namespace hec {
@@ -80,6 +86,8 @@ static void dist_release(hec_dist_s* d) {
     if (d->d_done) cudaFree(d->d_done);
     if (d->d_err) cudaFree(d->d_err);
     if (d->ev_start) cudaEventDestroy(d->ev_start);
+    for (cudaEvent_t e : {d->tm_start, d->tm_interior, d->tm_comm})
+        if (e) cudaEventDestroy(e);
     if (d->ev_halo) cudaEventDestroy(d->ev_halo);
     if (d->comm_stream) cudaStreamDestroy(d->comm_stream);
     if (d->d_send_idx) cudaFree(d->d_send_idx);
@@ -463,6 +471,7 @@ hec_status dist_spmv_launch(hec_dist_s* D, const double* x_local, double* y_loca
         // the comm stream, then wait for the neighbours' flags and run the
         // boundary rows behind it; the interior overlaps on the caller's stream
         const uint64_t ep = ++D->epoch;
+        if (D->timing) HEC_CUDA_TRY(cudaEventRecord(D->tm_start, s));
         HEC_CUDA_TRY(cudaEventRecord(D->ev_start, s));
         HEC_CUDA_TRY(cudaStreamWaitEvent(D->comm_stream, D->ev_start, 0));
         {
@@ -480,15 +489,20 @@ hec_status dist_spmv_launch(hec_dist_s* D, const double* x_local, double* y_loca
             }
         }
         HEC_CUDA_TRY(cudaEventRecord(D->ev_halo, D->comm_stream));
+        if (D->timing) HEC_CUDA_TRY(cudaEventRecord(D->tm_comm, D->comm_stream));
         NvtxRange r("hec.interior");
         hec_status st = launch_spmv(D->interior, x_local, nullptr, y_local, s);
         if (st != HEC_OK) return st;
+        if (D->timing) HEC_CUDA_TRY(cudaEventRecord(D->tm_interior, s));
+        D->tm_valid = D->timing;
+        D->tm_comm_valid = D->timing;
         HEC_CUDA_TRY(cudaStreamWaitEvent(s, D->ev_halo, 0));
         return HEC_OK;
     }
     if (has_exchange(D) && !D->comm && !D->local)
         return fail(HEC_ERR_STATE, "no halo transport: connect the peer-memory windows (hec_dist_p2p_connect)");
     const bool ex = has_exchange(D) && D->comm;
+    if (D->timing) HEC_CUDA_TRY(cudaEventRecord(D->tm_start, s));
     if (ex) {
         // comm stream: pack + grouped send/recv, overlapped with the interior SpMV
         HEC_CUDA_TRY(cudaEventRecord(D->ev_start, s));
@@ -514,10 +528,14 @@ hec_status dist_spmv_launch(hec_dist_s* D, const double* x_local, double* y_loca
             if (st != HEC_OK) return st;
         }
         HEC_CUDA_TRY(cudaEventRecord(D->ev_halo, D->comm_stream));
+        if (D->timing) HEC_CUDA_TRY(cudaEventRecord(D->tm_comm, D->comm_stream));
     }
     NvtxRange ri("hec.interior");
     hec_status st = launch_spmv(D->interior, x_local, nullptr, y_local, s);  // interior rows
     if (st != HEC_OK) return st;
+    if (D->timing) HEC_CUDA_TRY(cudaEventRecord(D->tm_interior, s));
+    D->tm_valid = D->timing;
+    D->tm_comm_valid = D->timing && ex;
     if (ex) HEC_CUDA_TRY(cudaStreamWaitEvent(s, D->ev_halo, 0));
     else if (D->n_boundary > 0) st = launch_spmv(D->boundary, x_local, D->d_x_halo, y_local, s);
     return st;
@@ -630,6 +648,33 @@ hec_status hec_spmv_dist_host(hec_dist D, const double* x_host_local, double* y_
     if (n_loc > 0)
         HEC_CUDA_TRY(cudaMemcpyAsync(y_host_local, D->d_stage_y, sizeof(double) * n_loc, cudaMemcpyDeviceToHost, s));
     HEC_CUDA_TRY(cudaStreamSynchronize(s));
+    return HEC_OK;
+}
+
+hec_status hec_dist_set_timing(hec_dist D, int32_t enable) {
+    if (!D) return fail(HEC_ERR_ARG, "NULL handle");
+    DeviceGuard g(D->device);
+    if (enable && !D->tm_start) {
+        HEC_CUDA_TRY(cudaEventCreate(&D->tm_start));
+        HEC_CUDA_TRY(cudaEventCreate(&D->tm_interior));
+        HEC_CUDA_TRY(cudaEventCreate(&D->tm_comm));
+    }
+    D->timing = enable != 0;
+    D->tm_valid = D->tm_comm_valid = false;
+    return HEC_OK;
+}
+
+hec_status hec_dist_phase_times(hec_dist D, float* interior_ms, float* comm_ms) {
+    if (!D || !interior_ms || !comm_ms) return fail(HEC_ERR_ARG, "NULL argument");
+    if (!D->tm_valid) return fail(HEC_ERR_STATE, "no timed hec_spmv_dist call (hec_dist_set_timing first)");
+    DeviceGuard g(D->device);
+    HEC_CUDA_TRY(cudaEventSynchronize(D->tm_interior));
+    HEC_CUDA_TRY(cudaEventElapsedTime(interior_ms, D->tm_start, D->tm_interior));
+    *comm_ms = -1.0f;
+    if (D->tm_comm_valid) {
+        HEC_CUDA_TRY(cudaEventSynchronize(D->tm_comm));
+        HEC_CUDA_TRY(cudaEventElapsedTime(comm_ms, D->tm_start, D->tm_comm));
+    }
     return HEC_OK;
 }
 

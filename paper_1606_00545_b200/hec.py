@@ -86,7 +86,7 @@ EXPORTED = [
     "hec_spmv_axpby", "hec_diag", "hec_jacobi", "hec_axpby", "hec_axpbyz", "hec_dot", "hec_norm2", "hec_bicgstab", "hec_cg",
     "hec_bicgstab_dist", "hec_cg_dist", "hec_from_csr_hyb", "hec_reorder_rcm", "hec_permute",
     "hec_spmv_dist_host", "hec_dist_comm_size", "hec_bicgstab_dist_local", "hec_cg_dist_local",
-    "hec_partition_order",
+    "hec_partition_order", "hec_dist_set_timing", "hec_dist_phase_times",
 ]
 
 
@@ -161,6 +161,10 @@ def load(build: bool = True):
     L.hec_spmv_dist.argtypes = [vp, vp, vp, vp]
     L.hec_spmv_dist_host.restype = st
     L.hec_spmv_dist_host.argtypes = [vp, vp, vp, vp]
+    L.hec_dist_set_timing.restype = st
+    L.hec_dist_set_timing.argtypes = [vp, i32]
+    L.hec_dist_phase_times.restype = st
+    L.hec_dist_phase_times.argtypes = [vp, ctypes.POINTER(ctypes.c_float), ctypes.POINTER(ctypes.c_float)]
     L.hec_dist_comm_size.restype = st
     L.hec_dist_comm_size.argtypes = [vp, ctypes.POINTER(i32), ctypes.POINTER(i32)]
     L.hec_spmv_dist_local.restype = st
@@ -574,6 +578,17 @@ class Dist:
         _check(_lib.hec_spmv_dist_host(self._h, _hptr(x_local, self.n_loc, "x_local"),
                                        _hptr(y_local, self.n_loc, "y_local"), _stream_ptr(stream)))
         return y_local
+
+    def set_timing(self, enable: bool = True):
+        """Record phase events in every hec_spmv_dist call (hec_dist_set_timing)."""
+        _check(_lib.hec_dist_set_timing(self._h, int(bool(enable))))
+
+    def phase_times(self) -> tuple[float, float]:
+        """(interior_ms, comm_ms) of the last timed call, both from its start;
+        comm_ms = -1 without an exchange (hec_dist_phase_times)."""
+        a, b = ctypes.c_float(), ctypes.c_float()
+        _check(_lib.hec_dist_phase_times(self._h, ctypes.byref(a), ctypes.byref(b)))
+        return a.value, b.value
 
     def comm_size(self) -> tuple[int, int]:
         """(ncclCommCount of the handle's communicator or 0, ncclGetVersion)."""

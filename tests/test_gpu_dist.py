@@ -91,6 +91,14 @@ def test_dist_single_rank_equals_hec_spmv_bitwise():
     M.spmv(x, y2)
     torch.cuda.synchronize()
     assert y1.cpu().numpy().tobytes() == y2.cpu().numpy().tobytes()
+    with pytest.raises(hec.HecError):
+        D.phase_times()                      # no timed call yet
+    D.set_timing(True)
+    D.spmv(x, y1)
+    t_int, t_comm = D.phase_times()
+    assert t_int > 0 and t_comm == -1.0      # one rank: no exchange
+    torch.cuda.synchronize()
+    assert y1.cpu().numpy().tobytes() == y2.cpu().numpy().tobytes()
 
 
 def test_local_group_p1_equals_hec_spmv_bitwise():

@@ -136,7 +136,15 @@ WORKER = textwrap.dedent(r"""
         ok = np.abs(y - oracle.csr_spmv(A, x, r0, r1)) <= oracle.tolerance(A, x, r0, r1)
         bad += int((~ok).sum())
     D.check()
-    print(f"rank {rank} launches {D.info.launches} bad {bad}", flush=True)
+    # phase timing (the overlap evidence): both ends of the last call
+    D.set_timing(True)
+    xl = torch.from_numpy(np.ascontiguousarray(hecgen.vector(A.n_cols, "uniform", seed=99)[r0:r1])).cuda()
+    D.spmv(xl, yl)
+    t_int, t_comm = D.phase_times()
+    D.set_timing(False)
+    if not (t_int > 0 and t_comm > 0):
+        bad += 1
+    print(f"rank {rank} launches {D.info.launches} bad {bad} interior {t_int:.4f} ms comm {t_comm:.4f} ms", flush=True)
     dist.barrier()
     D.free()
     dist.destroy_process_group()
