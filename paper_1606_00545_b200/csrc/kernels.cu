@@ -374,6 +374,9 @@ __global__ void __launch_bounds__(256, EPI == EPI_JACOBI ? HEC_JAC_MINB : 0) ell
 #ifndef HEC_TAIL_BATCH
 #define HEC_TAIL_BATCH 8  // HEC_TAIL_V 4: iterations whose loads are issued together
 #endif
+#ifndef HEC_TAIL_NOVAL
+#define HEC_TAIL_NOVAL 0
+#endif
 
 // One warp's pairs in the warp-chunk layout (hec_internal.h): wm = {first
 // entry, iterations, ...}; lane l reads the pair at base + 64 i + 2 l.  Returns
@@ -399,7 +402,11 @@ __device__ __forceinline__ double warp_chunk_sum(const TailArgs& a, int4 wm, int
             for (int u = 0; u < B; ++u) {
                 const int32_t k = kb + u * kTailChunk;
                 c[u] = k < k1 ? ld_stream_i2(a.col + k, pol) : make_int2(-1, -1);
+#if HEC_TAIL_NOVAL  // EXPERIMENT ONLY (wrong results): no value stream, to size the L1 sector cost
+                v[u] = make_double2(1.0, 1.0);
+#else
                 v[u] = k < k1 ? ld_stream_d2(a.val + k, pol) : make_double2(0.0, 0.0);
+#endif
             }
             double xs[2 * B];
 #pragma unroll
