@@ -378,6 +378,36 @@ __global__ void __launch_bounds__(256, EPI == EPI_JACOBI ? HEC_JAC_MINB : 0) ell
 #define HEC_TAIL_NOVAL 0
 #endif
 
+// ---- value stream through the bulk-copy engine (HEC_TAIL_V 5) ----
+// The tail is bound by the L1 sector throughput of its loads (ncu: ~82% of
+// peak; dropping the value stream cuts the sectors 112 M -> 90 M and the time
+// 249 -> 202 us, profiles/round2/l1probe): so each warp copies its batch of
+// values (B iterations x 64 entries, contiguous in the warp-chunk layout) into
+// its own shared-memory buffer with one cp.async.bulk completing on the
+// warp's mbarrier, while the lanes load the indices and gather x through the
+// LSU as before; the values are read from shared memory after the wait.
+__device__ __forceinline__ uint32_t smem_addr(const void* p) {
+    return static_cast<uint32_t>(__cvta_generic_to_shared(p));
+}
+__device__ __forceinline__ void mbar_init1(uint64_t* bar) {
+    asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;" ::"r"(smem_addr(bar)) : "memory");
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+}
+__device__ __forceinline__ void bulk_val(double* dst, const double* src, uint32_t bytes, uint64_t* bar, uint64_t pol) {
+    asm volatile("fence.proxy.async.shared::cta;" ::: "memory");  // the lanes' reads of the last batch came first
+    asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_addr(bar)), "r"(bytes) : "memory");
+    asm volatile(
+        "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes.L2::cache_hint [%0], [%1], %2, [%3], %4;"
+        ::"r"(smem_addr(dst)), "l"(src), "r"(bytes), "r"(smem_addr(bar)), "l"(pol)
+        : "memory");
+}
+__device__ __forceinline__ void mbar_wait_parity(uint64_t* bar, uint32_t parity) {
+    asm volatile(
+        "{\n.reg .pred P1;\nW_%=:\n"
+        "mbarrier.try_wait.parity.shared::cta.b64 P1, [%0], %1;\n"
+        "@!P1 bra.uni W_%=;\n}\n" ::"r"(smem_addr(bar)), "r"(parity) : "memory");
+}
+
 // One warp's pairs in the warp-chunk layout (hec_internal.h): wm = {first
 // entry, iterations, ...}; lane l reads the pair at base + 64 i + 2 l.  Returns
 // the lane's partial sum (its row's entries 2 (i G + lr), +1 in order).
@@ -440,8 +470,51 @@ __device__ __forceinline__ double warp_chunk_sum(const TailArgs& a, int4 wm, int
     return acc;
 }
 
+// HEC_TAIL_V 5: warp_chunk_sum with the values staged by the bulk-copy engine
+// into sv (B x 64 doubles, this warp's) on mbarrier bar; phase counts the
+// warp's batches so far (the mbarrier's parity).
+template <bool HALO>
+__device__ __forceinline__ double warp_chunk_sum_tma(const TailArgs& a, int4 wm, int l, uint64_t pol, double* sv,
+                                                     uint64_t* bar, uint32_t& phase) {
+    constexpr int B = HALO ? (HEC_TAIL_BATCH + 1) / 2 : HEC_TAIL_BATCH;
+    double acc = 0.0;
+    const int32_t w0 = wm.x, w1 = wm.x + kTailChunk * wm.y;  // the warp's entries
+    for (int32_t kw = w0; kw < w1; kw += B * kTailChunk) {
+        const int32_t nb = min(B * kTailChunk, w1 - kw);      // entries in this batch (a multiple of 64)
+        __syncwarp();                                          // every lane is done with sv
+        if (l == 0) bulk_val(sv, a.val + kw, (uint32_t)nb * 8u, bar, pol);
+        int2 c[B];
+#pragma unroll
+        for (int u = 0; u < B; ++u) {
+            const int32_t k = kw + u * kTailChunk + 2 * l;
+            c[u] = u * kTailChunk < nb ? ld_stream_i2(a.col + k, pol) : make_int2(-1, -1);
+        }
+        double xs[2 * B];
+#pragma unroll
+        for (int u = 0; u < B; ++u) {
+            xs[2 * u] = c[u].x >= 0 ? gather_x<HALO>(a.x, a.x_halo, a.n_loc, c[u].x) : 0.0;
+            xs[2 * u + 1] = c[u].y >= 0 ? gather_x<HALO>(a.x, a.x_halo, a.n_loc, c[u].y) : 0.0;
+        }
+        mbar_wait_parity(bar, phase & 1u);
+        ++phase;
+        // a padding entry has x = 0 (no gather) and value +0.0: its FMA adds
+        // +0.0 to a sum that is never -0.0 (it starts at +0.0), i.e. nothing --
+        // so no predicate (and no live indices) is needed here
+#pragma unroll
+        for (int u = 0; u < B; ++u) {
+            if (u * kTailChunk < nb) {
+                const double2 v = *reinterpret_cast<const double2*>(sv + u * kTailChunk + 2 * l);
+                acc = fma(v.x, xs[2 * u], acc);
+                acc = fma(v.y, xs[2 * u + 1], acc);
+            }
+        }
+    }
+    return acc;
+}
+
 template <bool HALO, bool JACOBI>
-__device__ __forceinline__ void tail_desc(const TailArgs& a, int64_t desc, int tid, uint64_t pol, double* wsum) {
+__device__ __forceinline__ void tail_desc(const TailArgs& a, int64_t desc, int tid, uint64_t pol, double* wsum,
+                                          double* sv = nullptr, uint64_t* bar = nullptr) {
     // one load per warp: {first entry, iterations, first row, count << 8 | lg}
     // (warp-chunk layout, hec_internal.h) -- no dependent metadata loads
     // before the stream starts
@@ -457,7 +530,13 @@ __device__ __forceinline__ void tail_desc(const TailArgs& a, int64_t desc, int t
         orow = __ldg(a.out_rows + wm.z + grp);
         yp = a.y + orow;
     }
-    double acc = warp_chunk_sum<HALO>(a, wm, tid & 31, pol);
+    double acc;
+    if (sv) {
+        uint32_t phase = 0;
+        acc = warp_chunk_sum_tma<HALO>(a, wm, tid & 31, pol, sv, bar, phase);
+    } else {
+        acc = warp_chunk_sum<HALO>(a, wm, tid & 31, pol);
+    }
     if (lg <= 5) {
         for (int off = G >> 1; off > 0; off >>= 1) acc += __shfl_xor_sync(0xffffffffu, acc, off, G);
     } else {
@@ -505,7 +584,17 @@ __global__ void __launch_bounds__(256, HEC_TAIL_MINB) tail_kernel(TailArgs a) {
     // it start streaming right away (it waits for these stores where it needs them)
     if (a.store_only) asm volatile("griddepcontrol.launch_dependents;");
     const uint64_t pol = policy_evict_first();
+#if HEC_TAIL_V == 5
+    constexpr int B = HALO ? (HEC_TAIL_BATCH + 1) / 2 : HEC_TAIL_BATCH;
+    __shared__ __align__(128) double sval[8][B * kTailChunk];  // per warp: one batch of values
+    __shared__ __align__(8) uint64_t sbar[8];
+    const int w = threadIdx.x >> 5;
+    if ((threadIdx.x & 31) == 0) mbar_init1(&sbar[w]);
+    __syncwarp();
+    tail_desc<HALO, JACOBI>(a, a.blk_begin + blockIdx.x, threadIdx.x, pol, wsum, sval[w], &sbar[w]);
+#else
     tail_desc<HALO, JACOBI>(a, a.blk_begin + blockIdx.x, threadIdx.x, pol, wsum);
+#endif
 }
 
 // SM-local persistent schedule, warp by warp (whole-matrix launches of big
