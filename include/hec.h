@@ -106,6 +106,15 @@ typedef struct {
     int32_t tail_fused;    /* 1: hec_spmv runs a small CSR tail FIRST (its row sums stored into y)
                               and the ELL kernel, launched as its programmatic dependent, adds
                               them -- the tail's latency hides under the ELL stream */
+    int32_t tail_ring;     /* 1: hec_spmv runs a big CSR tail with the x-ring schedule (one CTA
+                              per SM; each stage's x window staged in shared memory) */
+    int32_t ell_idx16;     /* 1: the device ELL part also holds 16-bit column deltas and the ELL
+                              kernel streams those (10 instead of 12 bytes per slot; opt-in with
+                              HEC_IDX16=1 at hec_from_csr, measured no faster: DESIGN §5) */
+    double tail_ring_cover; /* fraction of the stored tail entries whose column lies in their
+                               stage's x window (computed for ring candidates, else 0) */
+    double ell_idx16_escaped; /* fraction of ELL slots whose delta does not fit 16 bits and are
+                                 read as int32 (-1: not evaluated) */
 } hec_matrix_info;
 
 /* Caller-allocated export buffers, sized from hec_matrix_info:

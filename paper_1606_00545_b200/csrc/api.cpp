@@ -33,7 +33,7 @@ static void release(hec_matrix_s* m) {
         void* ptrs[] = {m->d_ell_col, m->d_ell_val, m->d_tail_out, m->d_tail_blk, m->d_fuse, m->d_tail_region,
                         m->d_tail_ctr, m->d_tsum, m->d_tail_units, m->d_tail_uwidx,
                         m->d_tail_warp, m->d_tail_col, m->d_tail_val, m->d_rowmap, m->d_coo_row, m->d_stage_x,
-                        m->d_stage_y};
+                        m->d_stage_y, m->d_ring, m->d_ell_d16};
         for (void* p : ptrs)
             if (p) cudaFree(p);
         for (cudaEvent_t e : m->ev_x) cudaEventDestroy(e);
@@ -52,7 +52,8 @@ static void release(hec_matrix_s* m) {
 // Row chunks (for hec_spmv_host; one chunk for sub-matrices and small
 // matrices), the x prefix each chunk reads, and the tail-kernel work list.
 static void plan_chunks(hec_matrix_s* m, const HostHec& h, bool pipelined, std::vector<int32_t>* order,
-                        std::vector<int4>* blk, std::vector<int4>* warp, int64_t* entries) {
+                        std::vector<int4>* blk, std::vector<int4>* warp, int64_t* entries, int32_t super,
+                        std::vector<int64_t>* sb_blk) {
     const int32_t n = h.n_rows;
     // ~1M-row chunks, at most 16 (32 chunks measured slower: 3.62 vs 3.41 ms on
     // 256^3; smaller first/last chunks too: 3.36 vs 3.31 ms; the floor is the
@@ -106,14 +107,15 @@ static void plan_chunks(hec_matrix_s* m, const HostHec& h, bool pipelined, std::
     // row and fewer rows in flight -- better for big tails (measured r11:
     // power-law 2^23 tail 8 > 4 > 2 > 1), worse for tiny ones (SPE10)
     const int epl = tail_epl(h.tail_col.size());
-    int32_t super = kTailSuperRows;  // HEC_TAIL_SUPER (tuning)
-    if (const char* e = std::getenv("HEC_TAIL_SUPER")) super = std::max(256, std::atoi(e));
+    if (const char* e = std::getenv("HEC_TAIL_SUPER")) super = std::max(256, std::atoi(e));  // tuning
+    sb_blk->clear();
     int32_t t0 = 0;
     for (int c = 0; c < C; ++c) {
         int32_t t1 = t0;
         while (t1 < tr && h.tail_rows[t1] < m->chunk_row[c + 1]) ++t1;
         for (int32_t sb = t0; sb < t1; sb += super) {
             const int32_t se = std::min(t1, sb + super);
+            sb_blk->push_back((int64_t)blk->size());  // this super-block's first descriptor
             for (int32_t t = sb; t < se; ++t) (*order)[t] = t;
             auto key = [&](int32_t t) {
                 const int32_t L = tp[t + 1] - tp[t];
@@ -143,6 +145,7 @@ static void plan_chunks(hec_matrix_s* m, const HostHec& h, bool pipelined, std::
         m->chunk_blk[c + 1] = (int64_t)blk->size();
         t0 = t1;
     }
+    sb_blk->push_back((int64_t)blk->size());
 }
 
 // Every stored tail entry's device position in the warp-chunk layout:
@@ -170,6 +173,177 @@ static void for_each_tail_entry(const std::vector<int4>& blk, const std::vector<
             }
         }
     }
+}
+
+// x-ring schedule of the tail (tail_ring_kernel).  Warp units --
+// one warp meta of rows with G <= 32 lanes, or the G / 32 metas of one longer
+// row, which a single warp then walks in turn -- are split over one CTA per
+// SM in contiguous runs of equal stored positions; a CTA's run is cut into
+// stages at super-block boundaries.  Each stage gets the window [lo, hi) of
+// x columns its gathers read from the CTA's shared-memory ring: centred on
+// the median column of the stage's entries (made non-decreasing along the
+// run), with one half-width h per CTA so that hi_s - lo_(s-D+1) <= the ring's
+// kRingCols columns, D = kRingDepth stages in flight (stage s's new columns
+// only overwrite ring slots of columns below lo_(s-D+1), i.e. of stages
+// <= s - D) and lo, hi even (16-byte bulk copies).  Columns outside the window are gathered from global memory,
+// so any matrix is correct; `cover` says how many stored entries hit.
+struct RingPlan {
+    std::vector<int4> stage;   // {lo, hi, u0, u1}
+    std::vector<int4> unit;    // {warp meta, metas, warp index in the descriptor, 0}
+    std::vector<int32_t> cta;  // [n_cta + 1] stage prefix
+    double cover = 0.0;
+};
+static void plan_ring(const std::vector<int4>& blk, const std::vector<int4>& warp, const std::vector<int64_t>& sb_blk,
+                      const std::vector<int32_t>& dcol, int32_t n_x, int n_cta, RingPlan* rp) {
+    std::vector<int4> unit;
+    std::vector<int32_t> usb;          // super-block of each unit
+    std::vector<int64_t> upre(1, 0);   // prefix of the units' stored positions
+    for (size_t q = 0; q + 1 < sb_blk.size(); ++q)
+        for (int64_t d = sb_blk[q]; d < sb_blk[q + 1]; ++d) {
+            const int g = blk[(size_t)d].z, G = 1 << g, cnt = blk[(size_t)d].y;
+            const int32_t w0 = blk[(size_t)d].w;
+            if (G <= 32) {
+                for (int w = 0; w < 8 && ((32 * w) >> g) < cnt; ++w) {
+                    unit.push_back(make_int4(w0 + w, 1, w, 0));
+                    usb.push_back((int32_t)q);
+                    upre.push_back(upre.back() + (int64_t)warp[(size_t)w0 + w].y * kTailChunk);
+                }
+            } else {
+                const int nw = G >> 5;
+                for (int r = 0; r < cnt; ++r) {
+                    int64_t e = 0;
+                    for (int j = 0; j < nw; ++j) e += (int64_t)warp[(size_t)w0 + r * nw + j].y * kTailChunk;
+                    unit.push_back(make_int4(w0 + r * nw, nw, r * nw, 0));
+                    usb.push_back((int32_t)q);
+                    upre.push_back(upre.back() + e);
+                }
+            }
+        }
+    const int64_t U = (int64_t)unit.size();
+    if (U == 0 || n_cta <= 0) return;
+    std::vector<int64_t> ub((size_t)n_cta + 1, U);
+    ub[0] = 0;
+    for (int c = 1; c < n_cta; ++c) {
+        ub[c] = std::lower_bound(upre.begin(), upre.end(), upre.back() * c / n_cta) - upre.begin();
+        ub[c] = std::max(std::min(ub[c], U), ub[c - 1]);
+    }
+    // stored columns (local x) of a unit's positions
+    auto unit_cols = [&](int64_t u, std::vector<int32_t>* out) {
+        const int4 un = unit[(size_t)u];
+        for (int j = 0; j < un.y; ++j) {
+            const int4 wm = warp[(size_t)un.x + j];
+            for (int64_t p = wm.x; p < (int64_t)wm.x + (int64_t)wm.y * kTailChunk; ++p) {
+                const int32_t c = dcol[(size_t)p];
+                if (c >= 0 && c < n_x) out->push_back(c);
+            }
+        }
+    };
+    const int64_t W = kRingCols;
+    const int32_t nx_even = n_x & ~1;
+    int64_t stored = 0, hit = 0;
+    rp->cta.assign(1, 0);
+    std::vector<int32_t> cols;
+    for (int c = 0; c < n_cta; ++c) {
+        std::vector<int64_t> cen;
+        std::vector<std::pair<int64_t, int64_t>> su;  // stage unit ranges
+        for (int64_t u = ub[c]; u < ub[c + 1];) {
+            int64_t v = u;
+            while (v < ub[c + 1] && usb[(size_t)v] == usb[(size_t)u]) ++v;
+            cols.clear();
+            for (int64_t k = u; k < v; ++k) unit_cols(k, &cols);
+            int64_t m = cen.empty() ? 0 : cen.back();
+            if (!cols.empty()) {
+                std::nth_element(cols.begin(), cols.begin() + cols.size() / 2, cols.end());
+                m = std::max<int64_t>(cols[cols.size() / 2], cen.empty() ? 0 : cen.back());
+            }
+            cen.push_back(m);
+            su.emplace_back(u, v);
+            u = v;
+        }
+        // the windows of kRingDepth consecutive stages share the ring
+        int64_t dmax = 0;
+        for (size_t k = 1; k < cen.size(); ++k)
+            dmax = std::max(dmax, cen[k] - cen[k >= (size_t)kRingDepth - 1 ? k - (kRingDepth - 1) : 0]);
+        const int64_t h = std::max<int64_t>(0, (W - dmax - 4) / 2);
+        for (size_t k = 0; k < cen.size(); ++k) {
+            int64_t lo = std::max<int64_t>(0, ((cen[k] - h) >> 1) << 1);
+            int64_t hi = std::min<int64_t>(nx_even, ((cen[k] + h + 1) >> 1) << 1);
+            if (h == 0 || hi < lo) hi = lo;
+            rp->stage.push_back(make_int4((int32_t)lo, (int32_t)hi, (int32_t)su[k].first, (int32_t)su[k].second));
+            cols.clear();
+            for (int64_t u = su[k].first; u < su[k].second; ++u) unit_cols(u, &cols);
+            stored += (int64_t)cols.size();
+            for (int32_t col : cols) hit += (col >= lo && col < hi);
+        }
+        rp->cta.push_back((int32_t)rp->stage.size());
+    }
+    rp->unit = std::move(unit);
+    rp->cover = stored > 0 ? (double)hit / (double)stored : 0.0;
+}
+
+// ELL index compression: the ELL kernel is bound by the bytes it
+// streams, 12 per slot (fp64 value + int32 column).  Where the columns sit at
+// (nearly) fixed offsets from the row -- stencils, banded reservoir matrices
+// -- slot j of row i stores d = col - i - base_j as an int16 next to the
+// int32 array, base_j the most common offset of slot j; padding stores
+// kIdxPad, and a slot whose delta does not fit stores kIdxEsc and the kernel
+// reads its int32 column instead.  10 bytes per slot instead of 12; the
+// arithmetic and every result are unchanged.  Opt-in (HEC_IDX16=1): measured
+// no faster (256^3 0.253 vs 0.245 ms, 150^3 and SPE10 within 2%), DESIGN §5.
+static hec_status plan_idx16(hec_matrix_s* m, const HostHec& h, cudaStream_t s, int64_t* bytes) {
+    const char* e = std::getenv("HEC_IDX16");
+    const int32_t w = h.width, n = h.n_rows;
+    if (!e || std::atoi(e) == 0 || w < 1 || w > kIdx16MaxW || n == 0) return HEC_OK;
+    const int64_t sstr = h.stride;
+    // base_j: the mode of (col - row) over every row, or over 2^16 rows drawn
+    // by a hash (a fixed stride would alias with grid periods: every 256th row
+    // of 256^3 is an x = 0 boundary row)
+    std::vector<int32_t> rows;
+    if (n <= (1 << 16)) {
+        rows.resize(n);
+        for (int32_t i = 0; i < n; ++i) rows[i] = i;
+    } else {
+        rows.resize(1 << 16);
+        for (uint64_t k = 0; k < rows.size(); ++k) {
+            uint64_t z = (k + 1) * 0x9E3779B97F4A7C15ULL;
+            z = (z ^ (z >> 30)) * 0xBF58476D1CE4E5B9ULL;
+            z = (z ^ (z >> 27)) * 0x94D049BB133111EBULL;
+            rows[k] = (int32_t)((z ^ (z >> 31)) % (uint64_t)n);
+        }
+    }
+    std::vector<int64_t> dl;
+    for (int32_t j = 0; j < w; ++j) {
+        dl.clear();
+        const int32_t* cj = h.ell_col.data() + (size_t)j * sstr;
+        for (int32_t i : rows)
+            if (cj[i] >= 0) dl.push_back((int64_t)cj[i] - i);
+        int64_t best = 0, bc = 0;
+        std::sort(dl.begin(), dl.end());
+        for (size_t a = 0; a < dl.size();) {
+            size_t b = a;
+            while (b < dl.size() && dl[b] == dl[a]) ++b;
+            if ((int64_t)(b - a) > bc) { bc = (int64_t)(b - a); best = dl[a]; }
+            a = b;
+        }
+        m->idx16_base[j] = (int32_t)std::max<int64_t>(INT32_MIN / 2, std::min<int64_t>(INT32_MAX / 2, best));
+    }
+    std::vector<int16_t> d16((size_t)w * sstr, kIdxPad);  // rows past n_rows: padding
+    int64_t esc = 0;
+    for (int32_t j = 0; j < w; ++j) {
+        const int32_t* cj = h.ell_col.data() + (size_t)j * sstr;
+        int16_t* dj = d16.data() + (size_t)j * sstr;
+        for (int32_t i = 0; i < n; ++i) {
+            const int64_t d = (int64_t)cj[i] - i - m->idx16_base[j];
+            if (cj[i] < 0) dj[i] = kIdxPad;
+            else if (d > kIdxPad && d <= INT16_MAX) dj[i] = (int16_t)d;
+            else { dj[i] = kIdxEsc; ++esc; }
+        }
+    }
+    m->idx16_esc = (double)esc / ((double)w * n);
+    hec_status st = dmalloc_copy(&m->d_ell_d16, d16.data(), d16.size(), s, bytes);
+    if (st != HEC_OK) return st;
+    HEC_CUDA_TRY(cudaStreamSynchronize(s));  // d16 dies after return
+    return HEC_OK;
 }
 
 hec_status make_matrix(HostHec&& h, int32_t device, cudaStream_t s, const int32_t* rowmap,
@@ -202,11 +376,20 @@ hec_status make_matrix(HostHec&& h, int32_t device, cudaStream_t s, const int32_
     m->tail_coo = coo_tail;
     std::vector<int32_t> order;
     std::vector<int4> blk, warp;
+    std::vector<int64_t> sb_blk;
     int64_t entries = 0;
-    plan_chunks(m.get(), h, n_loc < 0 && !rowmap && !coo_tail, &order, &blk, &warp, &entries);
+    // x-ring schedule (opt-in HEC_TAIL_RING=1, measured slower
+    // than the one-CTA-per-descriptor grid on the power-law tail: 269 vs 248
+    // us at best): planned with the ring's super-block size
+    int ring_env = 0;
+    if (const char* e = std::getenv("HEC_TAIL_RING")) ring_env = std::atoi(e) != 0 ? 1 : 0;
+    const bool ring_cand = !coo_tail && !h.tail_rows.empty() && ring_env == 1;
+    plan_chunks(m.get(), h, n_loc < 0 && !rowmap && !coo_tail, &order, &blk, &warp, &entries,
+                ring_cand ? kRingSuperRows : kTailSuperRows, &sb_blk);
     int64_t bytes = 0;
     hec_status st;
     if ((st = dmalloc_copy(&m->d_ell_col, h.ell_col.data(), h.ell_col.size(), s, &bytes))) return st;
+    if ((st = plan_idx16(m.get(), h, s, &bytes))) return st;
     if (coo_tail) {  // HYB comparison variant: remainder as row-sorted COO triplets
         std::vector<int32_t> rows(h.tail_col.size());
         for (size_t t = 0; t < h.tail_rows.size(); ++t)
@@ -236,6 +419,31 @@ hec_status make_matrix(HostHec&& h, int32_t device, cudaStream_t s, const int32_
             dval[(size_t)pos] = h.tail_val[k];
         });
         for (size_t p = 0; p < tr; ++p) dout[p] = rowmap ? rowmap[h.tail_rows[order[p]]] : row_off + h.tail_rows[order[p]];
+        int n_sm = 0;
+        cudaDeviceGetAttribute(&n_sm, cudaDevAttrMultiProcessorCount, device);
+        if (ring_cand && n_sm > 0) {
+            RingPlan rp;
+            plan_ring(blk, warp, sb_blk, dcol, n_loc >= 0 ? n_loc : h.n_cols, n_sm, &rp);
+            m->ring_cover = rp.cover;
+            if (!rp.stage.empty()) {
+                const size_t b4 = sizeof(int4) * (rp.stage.size() + rp.unit.size());
+                HEC_CUDA_TRY(cudaMalloc(&m->d_ring, b4 + sizeof(int32_t) * rp.cta.size()));
+                bytes += (int64_t)(b4 + sizeof(int32_t) * rp.cta.size());
+                int4* p4 = static_cast<int4*>(m->d_ring);
+                HEC_CUDA_TRY(cudaMemcpyAsync(p4, rp.stage.data(), sizeof(int4) * rp.stage.size(),
+                                             cudaMemcpyHostToDevice, s));
+                HEC_CUDA_TRY(cudaMemcpyAsync(p4 + rp.stage.size(), rp.unit.data(), sizeof(int4) * rp.unit.size(),
+                                             cudaMemcpyHostToDevice, s));
+                int32_t* pc = reinterpret_cast<int32_t*>(p4 + rp.stage.size() + rp.unit.size());
+                HEC_CUDA_TRY(cudaMemcpyAsync(pc, rp.cta.data(), sizeof(int32_t) * rp.cta.size(),
+                                             cudaMemcpyHostToDevice, s));
+                HEC_CUDA_TRY(cudaStreamSynchronize(s));  // rp dies after this scope
+                m->d_ring_stage = p4;
+                m->d_ring_unit = p4 + rp.stage.size();
+                m->d_ring_cta = pc;
+                m->ring_ctas = n_sm;
+            }
+        }
         m->h_tail_order = order;
         m->h_tail_ptr = h.tail_ptr;
         m->h_tail_blk = blk;
@@ -249,8 +457,6 @@ hec_status make_matrix(HostHec&& h, int32_t device, cudaStream_t s, const int32_
         // SM-local persistent schedule, warp by warp (opt-in HEC_TAIL_WARP=1,
         // big tails: more descriptors than one wave): warp units cut into one
         // region per SM with equal entries.  DESIGN §5 has the measurements.
-        int n_sm = 0;
-        cudaDeviceGetAttribute(&n_sm, cudaDevAttrMultiProcessorCount, device);
         bool warp_sched = false;
         if (const char* e = std::getenv("HEC_TAIL_WARP"))
             warp_sched = n_sm > 0 && (int64_t)blk.size() > (int64_t)n_sm * 6 && std::atoi(e) != 0;
@@ -367,6 +573,11 @@ static hec_status launch_chunks(const hec_matrix_s* A, int c, const double* x, c
     e.row_off = A->row_off;
     e.alpha = alpha;
     e.beta = beta;
+    if (A->d_ell_d16) {  // compressed column indices (plan_idx16)
+        e.d16 = A->d_ell_d16 + r0;
+        e.row0 = r0;
+        for (int j = 0; j < A->width && j < kIdx16MaxW; ++j) e.base[j] = A->idx16_base[j];
+    }
     e.diag = jd;  // Jacobi epilogue (whole matrix only: c < 0)
     e.b = jb;
     e.omega = omega;
@@ -407,6 +618,12 @@ static hec_status launch_chunks(const hec_matrix_s* A, int c, const double* x, c
         t.n_regions = A->tail_regions;
         t.region_ctr = A->d_tail_ctr;
         t.region_done = A->d_tail_ctr + A->tail_regions;
+    }
+    if (c < 0 && A->d_ring_stage) {  // whole launch: the x-ring schedule
+        t.ring_stage = A->d_ring_stage;
+        t.ring_unit = A->d_ring_unit;
+        t.ring_cta = A->d_ring_cta;
+        t.ring_ctas = A->ring_ctas;
     }
     cudaError_t err;
     if (A->tail_conc && c < 0 && !pw && !jd && alpha == 1.0 && beta == 0.0 && !x_halo) {
@@ -534,6 +751,10 @@ hec_status hec_info(hec_matrix A, hec_matrix_info* o) {
     o->device_bytes = A->device_bytes;
     o->device = A->device;
     o->tail_fused = A->fuse_tile > 0 && A->fuse_tile == 2 * ell_block_threads(A->width) ? 1 : 0;
+    o->tail_ring = A->d_ring_stage ? 1 : 0;
+    o->ell_idx16 = A->d_ell_d16 ? 1 : 0;
+    o->ell_idx16_escaped = A->idx16_esc;
+    o->tail_ring_cover = A->ring_cover;
     return HEC_OK;
 }
 

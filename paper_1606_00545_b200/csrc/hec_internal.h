@@ -81,6 +81,14 @@ constexpr int kTailSuperRows = 2048;   // tail rows regrouped by length within b
 // lives in one warp (shuffle reduction); 64-256 lanes span 2-8 warps of one
 // CTA (shuffle, then the warps' partials combined through shared memory).
 constexpr int kTailMaxLg = 8;
+// x ring (tail_ring_kernel): columns per CTA ring (a power of two; 128 KiB of
+// fp64) and tail rows per super-block when the ring schedule is used
+constexpr int kRingCols = 16384;
+#ifndef HEC_RING_DEPTH
+#define HEC_RING_DEPTH 3
+#endif
+constexpr int kRingDepth = HEC_RING_DEPTH;  // stages in flight per ring CTA (its windows share the ring)
+constexpr int kRingSuperRows = 1024;
 #ifndef HEC_TAIL_EPL_BIG
 #define HEC_TAIL_EPL_BIG 32  // measured with the batched tail loop: 8 -> 316/335 us, 16 -> 274, 32 -> 262
 #endif
@@ -165,6 +173,17 @@ struct hec_matrix_s {
     int32_t* d_tail_uwidx = nullptr;   // ... and its index in the warp-meta array
     unsigned int* d_tail_ctr = nullptr;  // [n_regions] claim counters + 1 done counter
     int32_t tail_regions = 0;
+    // x-ring schedule (TailArgs::ring_*): one allocation holding
+    // the stages, the per-CTA stage prefix and the units
+    void* d_ring = nullptr;
+    const int4 *d_ring_stage = nullptr, *d_ring_unit = nullptr;
+    const int32_t* d_ring_cta = nullptr;
+    int32_t ring_ctas = 0;
+    double ring_cover = 0.0;
+    // ELL index compression (EllArgs::d16): int16 deltas beside d_ell_col
+    int16_t* d_ell_d16 = nullptr;
+    int32_t idx16_base[16] = {};
+    double idx16_esc = -1.0;           // escaped fraction of the ELL slots (-1: not evaluated)           // fraction of the tail's stored entries inside their stage's window
     // concurrent tail (big tails, whole plain launches): the tail kernel on its
     // own stream beside the ELL kernel, sums into tsum, then one combine pass
     bool tail_conc = false;
@@ -255,6 +274,9 @@ struct PushArgs {                     // fused pack + NVLink store + release
     unsigned int* done;               // CTA completion counter (self-resetting)
 };
 
+constexpr int kIdx16MaxW = 16;      // widths with compiled-in slot loops (the compressed path needs one)
+constexpr int16_t kIdxEsc = INT16_MIN;      // the int32 column must be read
+constexpr int16_t kIdxPad = INT16_MIN + 1;  // padding slot (column -1)
 struct EllArgs {
     const int32_t* col;
     const double* val;
@@ -280,6 +302,13 @@ struct EllArgs {
     // rows fuse_row[fuse_cta[b] .. fuse_cta[b+1]) (ascending)
     const int32_t* fuse_cta = nullptr;
     const int32_t* fuse_row = nullptr;
+    // 16-bit column deltas ("ELL index compression"): when d16 !=
+    // null, slot j of row i stores d = col - (row0 + i) - base[j] as an int16
+    // (same column-major position as col), kIdxPad for a padding slot and
+    // kIdxEsc where the delta does not fit -- then the int32 column is read
+    const int16_t* d16 = nullptr;
+    int32_t row0 = 0;                 // row index of this launch's first row
+    int32_t base[kIdx16MaxW] = {};   // per-slot delta base
 };
 struct TailArgs {
     const int4* blk;            // block descriptors {first row position, count, lg, first warp} (diag)
@@ -307,6 +336,15 @@ struct TailArgs {
     unsigned int* region_done = nullptr; // CTA completion counter (self-resetting)
     const double* diag = nullptr;  // Jacobi (A22): the tail adds -omega * (its part / diag[row])
     double omega = 0.0;
+    // x-ring schedule (tail_ring_kernel; whole launches of big banded tails):
+    // CTA b walks stages [ring_cta[b], ring_cta[b+1]); a stage {lo, hi, u0, u1}
+    // is a run of warp units of one super-block whose x columns [lo, hi) sit in
+    // the CTA's shared-memory ring; ring_unit[u] = {warp meta, metas, warp index
+    // in its descriptor, 0}
+    const int4* ring_stage = nullptr;
+    const int32_t* ring_cta = nullptr;
+    const int4* ring_unit = nullptr;
+    int32_t ring_ctas = 0;
 };
 struct CooArgs {               // HYB remainder: row-sorted (row, col, val) triplets
     int64_t nnz;

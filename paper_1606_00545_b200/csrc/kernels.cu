@@ -207,17 +207,52 @@ constexpr int kTailUnroll = HEC_TAIL_UNROLL;
 #define HEC_ELL_PHASE 8  // widths above this load their slots in two phases (measured: 8 > 16 > 6)
 #endif
 
+__device__ __forceinline__ uint32_t ld_stream_u32v(const void* ptr, uint64_t pol) {
+    uint32_t r;
+    asm volatile("ld.global.nc.L1::no_allocate.L2::cache_hint.b32 %0, [%1], %2;" : "=r"(r) : "l"(ptr), "l"(pol));
+    return r;
+}
+
+// c = *p when d is the escape code (a predicated load in straight-line PTX)
+__device__ __forceinline__ void ld_if_esc(int32_t& c, int32_t d, const int32_t* p) {
+    asm volatile("{\n.reg .pred e;\nsetp.eq.s32 e, %1, -32768;\n@e ld.global.nc.s32 %0, [%2];\n}"
+                 : "+r"(c) : "r"(d), "l"(p));
+}
+
 // Slots [J0, J1) of a row pair: loads, then gathers, then FMAs in slot order.
-template <int J0, int J1, bool HALO>
+// C16: the column indices come as the pair's two int16 deltas in one 32-bit
+// load (EllArgs::d16); an escaped delta reads the slot's int32 column.
+template <int J0, int J1, bool HALO, bool C16 = false>
 __device__ __forceinline__ void ell_phase(const EllArgs& a, const int32_t* cp, const double* vp, int64_t s,
-                                          uint64_t pol, double& acc0, double& acc1) {
+                                          uint64_t pol, double& acc0, double& acc1, int64_t i0 = 0) {
     constexpr int N = J1 - J0;
     int2 c[N];
     double2 v[N];
+    if constexpr (C16) {
+        uint32_t p[N];
+        const int16_t* dp = a.d16 + i0;
 #pragma unroll
-    for (int j = 0; j < N; ++j) c[j] = ld_stream_i2v(cp + (J0 + j) * s, pol);
+        for (int j = 0; j < N; ++j) p[j] = ld_stream_u32v(dp + (J0 + j) * s, pol);
 #pragma unroll
-    for (int j = 0; j < N; ++j) v[j] = ld_stream_d2v(vp + (J0 + j) * s, pol);
+        for (int j = 0; j < N; ++j) v[j] = ld_stream_d2v(vp + (J0 + j) * s, pol);
+        // decode; an escaped slot (a few % of a stencil's row pairs have one)
+        // reads its int32 column with a predicated load -- straight-line code,
+        // so the stream loads above stay ahead of every wait
+        const int32_t r = a.row0 + (int32_t)i0;
+#pragma unroll
+        for (int j = 0; j < N; ++j) {
+            const int32_t d0 = (int32_t)(int16_t)(p[j] & 0xffffu), d1 = (int32_t)(int16_t)(p[j] >> 16);
+            c[j].x = d0 == kIdxPad ? -1 : r + a.base[J0 + j] + d0;
+            c[j].y = d1 == kIdxPad ? -1 : r + 1 + a.base[J0 + j] + d1;
+            ld_if_esc(c[j].x, d0, cp + (J0 + j) * s);
+            ld_if_esc(c[j].y, d1, cp + (J0 + j) * s + 1);
+        }
+    } else {
+#pragma unroll
+        for (int j = 0; j < N; ++j) c[j] = ld_stream_i2v(cp + (J0 + j) * s, pol);
+#pragma unroll
+        for (int j = 0; j < N; ++j) v[j] = ld_stream_d2v(vp + (J0 + j) * s, pol);
+    }
     double x0[N], x1[N];
 #pragma unroll
     for (int j = 0; j < N; ++j) {
@@ -247,7 +282,7 @@ __device__ __forceinline__ bool fuse_has(const EllArgs& a, int32_t q0, int32_t q
     return false;
 }
 
-template <int W, bool HALO, bool ROWMAP, int EPI, bool FUSE = false>
+template <int W, bool HALO, bool ROWMAP, int EPI, bool FUSE = false, bool C16 = false>
 __global__ void __launch_bounds__(256, EPI == EPI_JACOBI ? HEC_JAC_MINB : 0) ell_kernel(EllArgs a) {
     constexpr bool AXPBY = EPI == EPI_AXPBY;
     int32_t q0 = 0, q1 = 0;
@@ -281,8 +316,8 @@ __global__ void __launch_bounds__(256, EPI == EPI_JACOBI ? HEC_JAC_MINB : 0) ell
             // registers, more resident warps).
             constexpr int WW = W > 0 ? W : 1;
             constexpr int P1 = WW > HEC_ELL_PHASE ? (WW + 1) / 2 : WW;
-            ell_phase<0, P1, HALO>(a, cp, vp, s, pol, acc0, acc1);
-            if constexpr (P1 < WW) ell_phase<P1, WW, HALO>(a, cp, vp, s, pol, acc0, acc1);
+            ell_phase<0, P1, HALO, C16>(a, cp, vp, s, pol, acc0, acc1, i0);
+            if constexpr (P1 < WW) ell_phase<P1, WW, HALO, C16>(a, cp, vp, s, pol, acc0, acc1, i0);
         } else {
 #pragma unroll 4
             for (int j = 0; j < width; ++j) {
@@ -707,6 +742,164 @@ __global__ void __launch_bounds__(256, HEC_TAIL_MINB) tail_warp_kernel(TailArgs 
     }
 }
 
+// ------------------------------------------------------ x-ring tail kernel --
+// The tail is bound by the L1 wavefronts of its x gathers (one 128-byte line
+// per lane: ncu ~82% of the L1 throughput), and most of its columns
+// sit in a band around the row (power-law: 90% within +-4,096).  So one CTA
+// per SM walks a contiguous run of warp units (plan_ring, api.cpp) stage by
+// stage, and the x columns a stage mostly reads, [lo, hi), are staged into a
+// shared-memory ring of kRingCols columns by the bulk-copy engine: a
+// producer warp copies only each stage's NEW columns (the windows slide
+// along the rows), two stages ahead of their use (full/empty mbarriers, no
+// CTA-wide barrier), and the consumer warps gather in-window columns from
+// shared memory, the rest from global memory.  Same lanes, partial sums,
+// reduction order and one red.add per row as tail_kernel: bitwise equal.
+#ifndef HEC_RING_BATCH
+#define HEC_RING_BATCH 4  // iterations whose loads a lane issues together (8 spills at 31 warps)
+#endif
+template <bool HALO>
+__device__ __forceinline__ double warp_chunk_sum_ring(const TailArgs& a, int4 wm, int l, uint64_t pol,
+                                                      const double* ring, int32_t lo, uint32_t span) {
+    double acc = 0.0;
+    constexpr int B = HALO ? (HEC_RING_BATCH + 1) / 2 : HEC_RING_BATCH;
+    const int32_t k0 = wm.x + 2 * l, k1 = k0 + kTailChunk * wm.y;
+    for (int32_t kb = k0; kb < k1; kb += B * kTailChunk) {
+        int2 c[B];
+        double2 v[B];
+#pragma unroll
+        for (int u = 0; u < B; ++u) {
+            const int32_t k = kb + u * kTailChunk;
+            c[u] = k < k1 ? ld_stream_i2(a.col + k, pol) : make_int2(-1, -1);
+            v[u] = k < k1 ? ld_stream_d2(a.val + k, pol) : make_double2(0.0, 0.0);
+        }
+        double xs[2 * B];
+#pragma unroll
+        for (int u = 0; u < B; ++u) {
+            // in the window: the ring slot (the window lies inside [0, n_loc));
+            // padding (-1) reads nothing
+            xs[2 * u] = (uint32_t)(c[u].x - lo) < span ? ring[c[u].x & (kRingCols - 1)]
+                        : c[u].x >= 0                ? gather_x<HALO>(a.x, a.x_halo, a.n_loc, c[u].x)
+                                                     : 0.0;
+            xs[2 * u + 1] = (uint32_t)(c[u].y - lo) < span ? ring[c[u].y & (kRingCols - 1)]
+                            : c[u].y >= 0                ? gather_x<HALO>(a.x, a.x_halo, a.n_loc, c[u].y)
+                                                         : 0.0;
+        }
+#pragma unroll
+        for (int u = 0; u < B; ++u) {
+            if (c[u].x >= 0) acc = fma(v[u].x, xs[2 * u], acc);
+            if (c[u].y >= 0) acc = fma(v[u].y, xs[2 * u + 1], acc);
+        }
+    }
+    return acc;
+}
+
+template <bool HALO, bool JACOBI>
+__device__ __forceinline__ void tail_ring_unit(const TailArgs& a, int4 un, int l, uint64_t pol, const double* ring,
+                                               int32_t lo, uint32_t span) {
+    const int4 wm0 = __ldg(a.warp + un.x);
+    const int lg = wm0.w & 255, G = 1 << lg;
+    const int grp = ((un.z << 5) + l) >> lg;  // the lane's row within its descriptor
+    double acc;
+    if (G <= 32) {
+        acc = warp_chunk_sum_ring<HALO>(a, wm0, l, pol, ring, lo, span);
+        for (int off = G >> 1; off > 0; off >>= 1) acc += __shfl_xor_sync(0xffffffffu, acc, off, G);
+    } else {  // one row over G / 32 warps: each a full-warp tree, added in warp order
+        acc = 0.0;
+        for (int j = 0; j < un.y; ++j) {
+            double p = warp_chunk_sum_ring<HALO>(a, j == 0 ? wm0 : __ldg(a.warp + un.x + j), l, pol, ring, lo, span);
+            for (int off = 16; off > 0; off >>= 1) p += __shfl_xor_sync(0xffffffffu, p, off);
+            acc = j == 0 ? p : acc + p;
+        }
+    }
+    if ((l & (G - 1)) == 0 && grp < (wm0.w >> 8)) {
+        const int32_t orow = __ldg(a.out_rows + wm0.z + grp);
+        const double q = JACOBI ? -__dmul_rn(a.omega, __ddiv_rn(acc, __ldg(a.diag + orow))) : __dmul_rn(a.alpha, acc);
+        asm volatile("griddepcontrol.wait;" ::: "memory");
+        asm volatile("red.global.add.f64 [%0], %1;" ::"l"(a.y + orow), "d"(q) : "memory");
+    }
+}
+
+__device__ __forceinline__ void mbar_init(uint64_t* bar, uint32_t count) {
+    asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(smem_addr(bar)), "r"(count) : "memory");
+}
+__device__ __forceinline__ void mbar_arrive(uint64_t* bar) {
+    asm volatile("mbarrier.arrive.release.cta.shared::cta.b64 _, [%0];" ::"r"(smem_addr(bar)) : "memory");
+}
+__device__ __forceinline__ void bulk_g2s(void* dst, const void* src, uint32_t bytes, uint64_t* bar) {
+    asm volatile(
+        "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];"
+        ::"r"(smem_addr(dst)), "l"(src), "r"(bytes), "r"(smem_addr(bar))
+        : "memory");
+}
+
+#ifndef HEC_RING_NW
+#define HEC_RING_NW 31  // consumer warps per ring CTA (one CTA per SM; measured 16/24/31: 380/447/269 us)
+#endif
+
+template <bool HALO, bool JACOBI>
+__global__ void __launch_bounds__((HEC_RING_NW + 1) * 32, 1) tail_ring_kernel(TailArgs a) {
+    extern __shared__ __align__(128) double ring[];  // kRingCols columns
+    constexpr int NW = HEC_RING_NW, D = kRingDepth;
+    __shared__ __align__(8) uint64_t full[D], empty[D];
+    __shared__ uint32_t claim[D];  // per stage slot: the next unit to claim
+    const int w = threadIdx.x >> 5, l = threadIdx.x & 31;
+    const int32_t s0 = __ldg(a.ring_cta + blockIdx.x), s1 = __ldg(a.ring_cta + blockIdx.x + 1);
+    if (threadIdx.x == 0) {
+        for (int d = 0; d < D; ++d) {
+            mbar_init(&full[d], 1);
+            mbar_init(&empty[d], NW);
+        }
+        asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+    }
+    __syncthreads();
+    if (w == NW) {  // producer: lane 0 copies each stage's new columns
+        if (l != 0) return;
+        int32_t loaded = INT32_MIN;
+        for (int32_t s = s0; s < s1; ++s) {
+            const int k = s - s0, d = k % D;
+            const int4 st = __ldg(a.ring_stage + s);
+            // stage s's new columns overwrite only columns of stages <= s - D
+            // (plan_ring: hi_s - lo_(s-D+1) <= kRingCols), and slot d's claim
+            // counter is free once stage s - D is done
+            if (k >= D) mbar_wait_parity(&empty[d], ((k - D) / D) & 1);
+            claim[d] = 0;
+            const int32_t c0 = max(loaded, st.x), c1 = st.y;
+            if (c1 > c0) {
+                asm volatile("fence.proxy.async.shared::cta;" ::: "memory");  // consumers' reads came first
+                asm volatile("mbarrier.arrive.expect_tx.release.cta.shared::cta.b64 _, [%0], %1;"
+                             ::"r"(smem_addr(&full[d])), "r"((uint32_t)(c1 - c0) * 8u) : "memory");
+                const int32_t p0 = c0 & (kRingCols - 1);
+                const int32_t n0 = min(c1 - c0, kRingCols - p0);
+                bulk_g2s(ring + p0, a.x + c0, (uint32_t)n0 * 8u, &full[d]);
+                if (c1 - c0 > n0) bulk_g2s(ring, a.x + c0 + n0, (uint32_t)(c1 - c0 - n0) * 8u, &full[d]);
+                loaded = c1;
+            } else {
+                mbar_arrive(&full[d]);
+            }
+        }
+        return;
+    }
+    const uint64_t pol = policy_evict_first();
+    for (int32_t s = s0; s < s1; ++s) {
+        const int k = s - s0, d = k % D;
+        const int4 st = __ldg(a.ring_stage + s);
+        mbar_wait_parity(&full[d], (k / D) & 1);
+        const uint32_t span = (uint32_t)(st.y - st.x);
+        // units claimed one at a time, the biggest first (a super-block's
+        // units are sorted by ascending row length), so the stage's last
+        // units are small ones and the warps finish together
+        while (true) {
+            uint32_t c = 0;
+            if (l == 0) c = atomicAdd(&claim[d], 1u);
+            c = __shfl_sync(0xffffffffu, c, 0);
+            if ((int32_t)c >= st.w - st.z) break;
+            tail_ring_unit<HALO, JACOBI>(a, __ldg(a.ring_unit + st.w - 1 - (int32_t)c), l, pol, ring, st.x, span);
+        }
+        __syncwarp();
+        if (l == 0) mbar_arrive(&empty[d]);
+    }
+}
+
 // ------------------------------------------------------- HYB: COO kernel --
 // Comparison variant: the Bell-Garland HYB remainder in
 // COO instead of CSR.  Lane l of a warp owns 8 consecutive row-sorted
@@ -844,8 +1037,8 @@ static int ell_block(int32_t width) {
 int ell_block_threads(int32_t width) { return ell_block(width); }
 int64_t ell_grid_cap() { return (int64_t)num_sms() * 8 * 64; }
 
-template <bool HALO, bool ROWMAP, int EPI, bool FUSE = false>
-static cudaError_t launch_ell_t(const EllArgs& a, cudaStream_t s) {
+template <bool HALO, bool ROWMAP, int EPI, bool FUSE, bool C16>
+static cudaError_t launch_ell_t2(const EllArgs& a, cudaStream_t s) {
     const int64_t n_pairs = ((int64_t)a.n_rows + 1) >> 1;
     const int threads = ell_block(a.width);
     int64_t blocks = (n_pairs + threads - 1) / threads;
@@ -865,12 +1058,20 @@ static cudaError_t launch_ell_t(const EllArgs& a, cudaStream_t s) {
     const dim3 g((unsigned)blocks), b(threads);
     switch (a.width) {
 #define HEC_W(w) \
-    case w: return launch_k(ell_kernel<w, HALO, ROWMAP, EPI, FUSE>, g, b, s, a.pdl, 0, a);
+    case w: return launch_k(ell_kernel<w, HALO, ROWMAP, EPI, FUSE, C16>, g, b, s, a.pdl, 0, a);
         HEC_W(1) HEC_W(2) HEC_W(3) HEC_W(4) HEC_W(5) HEC_W(6) HEC_W(7) HEC_W(8)
         HEC_W(9) HEC_W(10) HEC_W(11) HEC_W(12) HEC_W(13) HEC_W(14) HEC_W(15) HEC_W(16)
 #undef HEC_W
-        default: return launch_k(ell_kernel<0, HALO, ROWMAP, EPI, FUSE>, g, b, s, a.pdl, 0, a);
+        default:
+            if constexpr (C16) return cudaErrorInvalidValue;  // compressed indices need a compiled width
+            else return launch_k(ell_kernel<0, HALO, ROWMAP, EPI, FUSE>, g, b, s, a.pdl, 0, a);
     }
+}
+
+template <bool HALO, bool ROWMAP, int EPI, bool FUSE = false>
+static cudaError_t launch_ell_t(const EllArgs& a, cudaStream_t s) {
+    if (a.d16 && a.width >= 1 && a.width <= kIdx16MaxW) return launch_ell_t2<HALO, ROWMAP, EPI, FUSE, true>(a, s);
+    return launch_ell_t2<HALO, ROWMAP, EPI, FUSE, false>(a, s);
 }
 
 // ELL kernel choice: "reg" (register-streaming ell_kernel) or "tma" (bulk-copy
@@ -916,6 +1117,22 @@ cudaError_t launch_tail(const TailArgs& a, cudaStream_t s) {
     const bool pdl = tail_pdl() && !a.store_only;  // store_only runs first: an ordinary launch
     if (a.diag && a.x_halo) return cudaErrorInvalidValue;
     if (a.store_only && (a.diag || a.x_halo || a.alpha != 1.0)) return cudaErrorInvalidValue;
+    if (a.ring_stage && !a.store_only && a.ring_ctas > 0 && (reinterpret_cast<uintptr_t>(a.x) & 15) == 0) {
+        // x-ring schedule: one CTA per SM, the ring in dynamic shared memory
+        const size_t smem = sizeof(double) * kRingCols;
+        static bool attr[3] = {false, false, false};
+        auto go = [&](auto kern, int which) {
+            if (!attr[which]) {
+                cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+                if (e != cudaSuccess) return e;
+                attr[which] = true;
+            }
+            return launch_k(kern, dim3((unsigned)a.ring_ctas), dim3((HEC_RING_NW + 1) * 32), s, pdl, smem, a);
+        };
+        if (a.diag) return go(tail_ring_kernel<false, true>, 0);
+        if (a.x_halo) return go(tail_ring_kernel<true, false>, 1);
+        return go(tail_ring_kernel<false, false>, 2);
+    }
     if (a.region && !a.store_only) {  // SM-local persistent schedule, warp by warp: 6 CTAs per SM
         const int64_t g = std::min<int64_t>(blocks, (int64_t)num_sms() * HEC_TAIL_MINB);
         if (a.diag) return launch_k(tail_warp_kernel<false, true>, dim3((unsigned)g), dim3(256), s, pdl, 0, a);

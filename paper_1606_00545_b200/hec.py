@@ -49,7 +49,9 @@ class OptsT(ctypes.Structure):
 class MatrixInfoT(ctypes.Structure):
     _fields_ = [("n_rows", i32), ("n_cols", i32), ("ell_width", i32), ("ell_stride", i32),
                 ("nnz", i64), ("ell_nnz", i64), ("tail_rows", i32), ("tail_group", i32),
-                ("tail_nnz", i64), ("device_bytes", i64), ("device", i32), ("tail_fused", i32)]
+                ("tail_nnz", i64), ("device_bytes", i64), ("device", i32), ("tail_fused", i32),
+                ("tail_ring", i32), ("ell_idx16", i32), ("tail_ring_cover", ctypes.c_double),
+                ("ell_idx16_escaped", ctypes.c_double)]
 
 
 class HostArraysT(ctypes.Structure):
