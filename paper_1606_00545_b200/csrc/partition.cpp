@@ -364,6 +364,66 @@ static void refine(const Graph& g, int32_t P, std::vector<int32_t>& part, int pa
     }
 }
 
+// FM refinement with hill climbing (Fiduccia-Mattheyses, k-way) for the
+// small coarse levels: moves the unlocked vertex with the best gain to an
+// adjacent part -- also when the gain is negative -- under a balance bound of
+// the average part weight + one heaviest vertex, locks it, and after the
+// pass rolls back to the prefix of moves with the smallest edge cut.  A
+// negative first move lets a whole run of vertices follow, which the greedy
+// refine() (gain >= 0 only) cannot: the folds the coarsest spectral order
+// leaves are such runs.
+static void fm_refine(const Graph& g, int32_t P, std::vector<int32_t>& part, int passes) {
+    const int32_t n = g.n;
+    int64_t maxv = 0;
+    for (int32_t v = 0; v < n; ++v) maxv = std::max(maxv, g.vw[v]);
+    const int64_t maxw = (int64_t)((double)g.total / P * 1.03) + maxv;
+    std::vector<int64_t> pw(P, 0), conn((size_t)n * P, 0);
+    for (int pass = 0; pass < passes; ++pass) {
+        std::fill(pw.begin(), pw.end(), 0);
+        std::fill(conn.begin(), conn.end(), 0);
+        for (int32_t v = 0; v < n; ++v) {
+            pw[part[v]] += g.vw[v];
+            for (int64_t k = g.xadj[v]; k < g.xadj[v + 1]; ++k)
+                conn[(size_t)v * P + part[g.adj[(size_t)k]]] += g.ew[(size_t)k];
+        }
+        std::vector<char> locked(n, 0);
+        std::vector<std::pair<int32_t, int32_t>> moves;  // (vertex, from)
+        int64_t cut = 0, best = 0;
+        size_t best_len = 0;
+        for (int32_t step = 0; step < n; ++step) {
+            int32_t bv = -1, bq = -1;
+            int64_t bg = INT64_MIN;
+            for (int32_t v = 0; v < n; ++v) {
+                if (locked[v]) continue;
+                const int32_t own = part[v];
+                if (pw[own] - g.vw[v] <= 0) continue;  // never empty a part
+                const int64_t in = conn[(size_t)v * P + own];
+                for (int32_t q = 0; q < P; ++q) {
+                    if (q == own || conn[(size_t)v * P + q] == 0 || pw[q] + g.vw[v] > maxw) continue;
+                    const int64_t gain = conn[(size_t)v * P + q] - in;
+                    if (gain > bg) { bg = gain; bv = v; bq = q; }
+                }
+            }
+            if (bv < 0) break;
+            const int32_t from = part[bv];
+            part[bv] = bq;
+            pw[from] -= g.vw[bv];
+            pw[bq] += g.vw[bv];
+            for (int64_t k = g.xadj[bv]; k < g.xadj[bv + 1]; ++k) {
+                const int32_t u = g.adj[(size_t)k];
+                conn[(size_t)u * P + from] -= g.ew[(size_t)k];
+                conn[(size_t)u * P + bq] += g.ew[(size_t)k];
+            }
+            locked[bv] = 1;
+            moves.emplace_back(bv, from);
+            cut -= bg;  // relative to the pass's start
+            if (cut < best) { best = cut; best_len = moves.size(); }
+        }
+        for (size_t i = moves.size(); i > best_len; --i) part[moves[i - 1].first] = moves[i - 1].second;
+        if (best_len == 0) break;
+    }
+}
+
 // Final order: parts in order, inside a part the vertices keep the order of
 // their coarsest ancestors (a level-set order of the coarse graph), children
 // of one coarse vertex adjacent -- locality for the x gathers.
@@ -431,11 +491,19 @@ hec_status hec_partition_order(const hec_csr* A, int32_t n_parts, int32_t method
         // multilevel: a few independent trials (matching orders), the smallest
         // edge cut wins -- the result of one trial depends on where the
         // coarsening happens to fold the graph
+        // (each matching order is run twice: plain greedy refinement, and with
+        // FM hill climbing on the small levels first -- neither wins always)
         int trials = 3;
         if (const char* e = std::getenv("HEC_PART_TRIALS")) trials = std::max(1, std::atoi(e));
-        int64_t best_cut = -1;
+        int32_t fm_max = 2048;  // FM on the levels up to this many vertices (HEC_PART_FM, tuning; 0: off)
+        if (const char* e = std::getenv("HEC_PART_FM")) fm_max = std::max(0, std::atoi(e));
+        const int runs = fm_max > 0 ? 2 * trials : trials;
+        int64_t best_cut = -1, best_vol = -1;
+        std::vector<int32_t> seen_part(n_parts, 0);
         std::vector<int32_t> bperm(v.n_rows), bpp(n_parts + 1);
-        for (int trial = 0; trial < trials; ++trial) {
+        for (int run = 0; run < runs; ++run) {
+            const int trial = run % trials;
+            const int32_t fm_lvl = run >= trials ? fm_max : 0;
             std::vector<Graph> G;
             G.push_back(g0);
             std::vector<std::vector<int32_t>> cmaps;
@@ -473,21 +541,33 @@ hec_status hec_partition_order(const hec_csr* A, int32_t n_parts, int32_t method
                 std::iota(all.begin(), all.end(), 0);
                 recursive_bisect(gc, all, n_parts, 0, part, in, in_stamp, seen, seen_stamp, &coarse_order);
             }
+            if (gc.n <= fm_lvl) fm_refine(gc, n_parts, part, 8);
             refine(gc, n_parts, part, 8);
             for (int l = (int)G.size() - 2; l >= 0; --l) {
                 std::vector<int32_t> fine(G[l].n);
                 for (int32_t u = 0; u < G[l].n; ++u) fine[u] = part[cmaps[l][u]];
                 part.swap(fine);
+                if (G[l].n <= fm_lvl) fm_refine(G[l], n_parts, part, 4);
                 refine(G[l], n_parts, part, 4);
             }
-            int64_t cut = 0;
-            for (int32_t u = 0; u < g0.n; ++u)
-                for (int64_t k = g0.xadj[u]; k < g0.xadj[u + 1]; ++k)
-                    if (part[g0.adj[(size_t)k]] != part[u]) cut += g0.ew[(size_t)k];
-            if (best_cut < 0 || cut < best_cut) {
+            // the run's halo volume: sum over vertices u of the other parts
+            // adjacent to u (each is one x entry that part receives) -- what
+            // the exchange moves; the edge cut breaks ties
+            int64_t cut = 0, vol = 0;
+            for (int32_t u = 0; u < g0.n; ++u) {
+                const int32_t pu = part[u];
+                for (int64_t k = g0.xadj[u]; k < g0.xadj[u + 1]; ++k) {
+                    const int32_t q = part[g0.adj[(size_t)k]];
+                    if (q == pu) continue;
+                    cut += g0.ew[(size_t)k];
+                    if (seen_part[q] != u + 1) { seen_part[q] = u + 1; ++vol; }
+                }
+            }
+            if (best_cut < 0 || vol < best_vol || (vol == best_vol && cut < best_cut)) {
                 st = order_from_parts(G, cmaps, coarse_order, part, n_parts, bperm.data(), bpp.data());
                 if (st != HEC_OK) continue;
                 best_cut = cut;
+                best_vol = vol;
             }
         }
         if (best_cut < 0) return fail(HEC_ERR_PARTS, "a part came out empty");

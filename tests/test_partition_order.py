@@ -106,7 +106,7 @@ def test_multilevel_recovers_the_scrambled_power_law():
     B = hec.permute(S, perm)
     got = halo(B, 8, hec.PART_EXPLICIT, pp)
     assert halo(S, 8) > 2.5 * nat
-    assert got <= 1.1 * nat, (got, nat)
+    assert got <= 1.05 * nat, (got, nat)   # round 2 with FM runs: 1.010-1.014
     nnz = np.diff(B.row_ptr[pp])
     assert nnz.max() <= 1.03 * nnz.mean() + 2000
 
