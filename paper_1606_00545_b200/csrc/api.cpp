@@ -124,12 +124,12 @@ static void plan_chunks(hec_matrix_s* m, const HostHec& h, bool pipelined, std::
             std::stable_sort(order->begin() + sb, order->begin() + se,
                              [&](int32_t a, int32_t b) { return key(a) < key(b); });
             for (int32_t f = sb; f < se;) {
-                const int g = key((*order)[f]).first, G = 1 << g, per_blk = 256 >> g;
+                const int g = key((*order)[f]).first, G = 1 << g, per_blk = kTailThreads >> g;
                 int32_t cnt = 0;
                 while (cnt < per_blk && f + cnt < se && key((*order)[f + cnt]).first == g) ++cnt;
                 blk->push_back(make_int4(f, cnt, g, (int32_t)warp->size()));
-                // the descriptor's 8 warps: thread tid = 32 w + l serves row tid >> g
-                for (int w = 0; w < 8; ++w) {
+                // the descriptor's warps: thread tid = 32 w + l serves row tid >> g
+                for (int w = 0; w < kTailWarps; ++w) {
                     int32_t iters = 0;
                     const int32_t r_lo = (32 * w) >> g, r_hi = std::min(cnt, ((32 * w + 31) >> g) + 1);
                     for (int32_t r = r_lo; r < r_hi; ++r) {
@@ -158,7 +158,7 @@ static void for_each_tail_entry(const std::vector<int4>& blk, const std::vector<
                                 const std::vector<int32_t>& order, const std::vector<int32_t>& tail_ptr, F f) {
     for (const int4& d : blk) {
         const int g = d.z, G = 1 << g;
-        for (int w = 0; w < 8; ++w) {
+        for (int w = 0; w < kTailWarps; ++w) {
             const int4 wm = warp[(size_t)d.w + w];
             for (int l = 0; l < 32; ++l) {
                 const int tid = 32 * w + l, r = tid >> g, lr = tid & (G - 1);
@@ -203,7 +203,7 @@ static void plan_ring(const std::vector<int4>& blk, const std::vector<int4>& war
             const int g = blk[(size_t)d].z, G = 1 << g, cnt = blk[(size_t)d].y;
             const int32_t w0 = blk[(size_t)d].w;
             if (G <= 32) {
-                for (int w = 0; w < 8 && ((32 * w) >> g) < cnt; ++w) {
+                for (int w = 0; w < kTailWarps && ((32 * w) >> g) < cnt; ++w) {
                     unit.push_back(make_int4(w0 + w, 1, w, 0));
                     usb.push_back((int32_t)q);
                     upre.push_back(upre.back() + (int64_t)warp[(size_t)w0 + w].y * kTailChunk);
@@ -459,7 +459,7 @@ hec_status make_matrix(HostHec&& h, int32_t device, cudaStream_t s, const int32_
         // region per SM with equal entries.  DESIGN §5 has the measurements.
         bool warp_sched = false;
         if (const char* e = std::getenv("HEC_TAIL_WARP"))
-            warp_sched = n_sm > 0 && (int64_t)blk.size() > (int64_t)n_sm * 6 && std::atoi(e) != 0;
+            warp_sched = n_sm > 0 && (int64_t)blk.size() > (int64_t)n_sm * (48 / kTailWarps) && std::atoi(e) != 0;
         if (warp_sched) {
             std::vector<int4> units;
             std::vector<int32_t> uwidx;
@@ -468,7 +468,7 @@ hec_status make_matrix(HostHec&& h, int32_t device, cudaStream_t s, const int32_
                 const int g = blk[d].z, G = 1 << g, cnt = blk[d].y;
                 const int32_t w0 = blk[d].w;
                 if (G <= 32) {
-                    for (int w = 0; w < 8; ++w) {
+                    for (int w = 0; w < kTailWarps; ++w) {
                         if (((32 * w) >> g) >= cnt) break;  // no rows in this warp (nor later ones)
                         units.push_back(warp[(size_t)w0 + w]);
                         uwidx.push_back(w0 + w);
@@ -504,7 +504,7 @@ hec_status make_matrix(HostHec&& h, int32_t device, cudaStream_t s, const int32_
         // (power-law 0.484 vs 0.436 ms: the two kernels share the memory system
         // and the scattered combine pass costs 48 us), DESIGN §5
         if (const char* e = std::getenv("HEC_TAIL_CONC"))
-            if (std::atoi(e) != 0 && (int64_t)blk.size() > (int64_t)n_sm * 6 && n_loc < 0 && !rowmap) {
+            if (std::atoi(e) != 0 && (int64_t)blk.size() > (int64_t)n_sm * (48 / kTailWarps) && n_loc < 0 && !rowmap) {
                 HEC_CUDA_TRY(cudaMalloc(&m->d_tsum, sizeof(double) * h.tail_rows.size()));
                 bytes += (int64_t)(sizeof(double) * h.tail_rows.size());
                 HEC_CUDA_TRY(cudaStreamCreateWithFlags(&m->s_tail, cudaStreamNonBlocking));
@@ -521,7 +521,7 @@ hec_status make_matrix(HostHec&& h, int32_t device, cudaStream_t s, const int32_
     // of rows (no grid stride).  HEC_FUSE_TAIL=0 disables; HEC_FUSE_TAIL_MAX =
     // most tail-kernel CTAs (default: one wave, 148 x 6).
     if (!h.tail_rows.empty() && n_loc < 0 && !rowmap && row_off == 0) {
-        int64_t fmax = (int64_t)148 * 6;
+        int64_t fmax = (int64_t)148 * (48 / kTailWarps);
         if (const char* e = std::getenv("HEC_FUSE_TAIL_MAX")) fmax = std::atol(e);
         bool fuse = (int64_t)blk.size() <= fmax;
         if (const char* e = std::getenv("HEC_FUSE_TAIL")) fuse = fuse && std::atoi(e) != 0;

@@ -80,7 +80,15 @@ constexpr int kTailSuperRows = 2048;   // tail rows regrouped by length within b
 // 2^kTailMaxLg, where epl = target entries per lane.  Up to 32 lanes a row
 // lives in one warp (shuffle reduction); 64-256 lanes span 2-8 warps of one
 // CTA (shuffle, then the warps' partials combined through shared memory).
-constexpr int kTailMaxLg = 8;
+// Warps per tail descriptor (one CUDA block of 32 kTailWarps threads takes
+// one descriptor); rows span at most all of them: G <= 32 kTailWarps lanes.
+#ifndef HEC_TAIL_WARPS
+#define HEC_TAIL_WARPS 8
+#endif
+constexpr int kTailWarps = HEC_TAIL_WARPS;
+constexpr int kTailThreads = 32 * kTailWarps;
+static_assert(kTailWarps == 2 || kTailWarps == 4 || kTailWarps == 8, "tail descriptor warps: 2, 4 or 8");
+constexpr int kTailMaxLg = kTailWarps == 8 ? 8 : kTailWarps == 4 ? 7 : 6;
 // x ring (tail_ring_kernel): columns per CTA ring (a power of two; 128 KiB of
 // fp64) and tail rows per super-block when the ring schedule is used
 constexpr int kRingCols = 16384;

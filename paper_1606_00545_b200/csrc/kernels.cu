@@ -553,7 +553,7 @@ __device__ __forceinline__ void tail_desc(const TailArgs& a, int64_t desc, int t
     // one load per warp: {first entry, iterations, first row, count << 8 | lg}
     // (warp-chunk layout, hec_internal.h) -- no dependent metadata loads
     // before the stream starts
-    const int4 wm = __ldg(a.warp + desc * 8 + (tid >> 5));
+    const int4 wm = __ldg(a.warp + desc * kTailWarps + (tid >> 5));
     const int lg = wm.w & 255;
     const int G = 1 << lg;
     const int lane = tid & (G - 1);
@@ -609,20 +609,20 @@ __device__ __forceinline__ void tail_desc(const TailArgs& a, int64_t desc, int t
 }
 
 #ifndef HEC_TAIL_MINB
-#define HEC_TAIL_MINB 6  // CTAs per SM: 6 leaves the batched loads 40 registers (8: 32 regs, 275 us; 4: 277 us)
+#define HEC_TAIL_MINB (48 / kTailWarps)  // CTAs per SM: 48 warps leave the batched loads 40 registers (64 warps: 32 regs, 275 us; 32 warps: 277 us)
 #endif
 
 template <bool HALO, bool JACOBI>
-__global__ void __launch_bounds__(256, HEC_TAIL_MINB) tail_kernel(TailArgs a) {
-    __shared__ double wsum[8];  // per-warp partials of rows wider than a warp
+__global__ void __launch_bounds__(kTailThreads, HEC_TAIL_MINB) tail_kernel(TailArgs a) {
+    __shared__ double wsum[kTailWarps];  // per-warp partials of rows wider than a warp
     // store_only: the ELL kernel is this grid's programmatic dependent -- let
     // it start streaming right away (it waits for these stores where it needs them)
     if (a.store_only) asm volatile("griddepcontrol.launch_dependents;");
     const uint64_t pol = policy_evict_first();
 #if HEC_TAIL_V == 5
     constexpr int B = HALO ? (HEC_TAIL_BATCH + 1) / 2 : HEC_TAIL_BATCH;
-    __shared__ __align__(128) double sval[8][B * kTailChunk];  // per warp: one batch of values
-    __shared__ __align__(8) uint64_t sbar[8];
+    __shared__ __align__(128) double sval[kTailWarps][B * kTailChunk];  // per warp: one batch of values
+    __shared__ __align__(8) uint64_t sbar[kTailWarps];
     const int w = threadIdx.x >> 5;
     if ((threadIdx.x & 31) == 0) mbar_init1(&sbar[w]);
     __syncwarp();
@@ -656,7 +656,7 @@ template <bool HALO, bool JACOBI>
 __device__ __forceinline__ void tail_unit(const TailArgs& a, int4 wm0, int64_t u, int l, uint64_t pol) {
     const int lg = wm0.w & 255, G = 1 << lg;
     const int32_t widx = __ldg(a.unit_widx + u);
-    const int grp = (((widx & 7) << 5) + l) >> lg;  // the lane's row within its descriptor
+    const int grp = (((widx & (kTailWarps - 1)) << 5) + l) >> lg;  // the lane's row within its descriptor
     double acc;
     if (G <= 32) {
         acc = warp_chunk_sum<HALO>(a, wm0, l, pol);
@@ -705,7 +705,7 @@ __device__ __forceinline__ void tail_region(const TailArgs& a, int r, int l, uin
 }
 
 template <bool HALO, bool JACOBI>
-__global__ void __launch_bounds__(256, HEC_TAIL_MINB) tail_warp_kernel(TailArgs a) {
+__global__ void __launch_bounds__(kTailThreads, HEC_TAIL_MINB) tail_warp_kernel(TailArgs a) {
     const uint64_t pol = policy_evict_first();
     const int l = threadIdx.x & 31;
     const int R = a.n_regions;
@@ -1135,13 +1135,13 @@ cudaError_t launch_tail(const TailArgs& a, cudaStream_t s) {
     }
     if (a.region && !a.store_only) {  // SM-local persistent schedule, warp by warp: 6 CTAs per SM
         const int64_t g = std::min<int64_t>(blocks, (int64_t)num_sms() * HEC_TAIL_MINB);
-        if (a.diag) return launch_k(tail_warp_kernel<false, true>, dim3((unsigned)g), dim3(256), s, pdl, 0, a);
-        if (a.x_halo) return launch_k(tail_warp_kernel<true, false>, dim3((unsigned)g), dim3(256), s, pdl, 0, a);
-        return launch_k(tail_warp_kernel<false, false>, dim3((unsigned)g), dim3(256), s, pdl, 0, a);
+        if (a.diag) return launch_k(tail_warp_kernel<false, true>, dim3((unsigned)g), dim3(kTailThreads), s, pdl, 0, a);
+        if (a.x_halo) return launch_k(tail_warp_kernel<true, false>, dim3((unsigned)g), dim3(kTailThreads), s, pdl, 0, a);
+        return launch_k(tail_warp_kernel<false, false>, dim3((unsigned)g), dim3(kTailThreads), s, pdl, 0, a);
     }
-    if (a.diag) return launch_k(tail_kernel<false, true>, dim3((unsigned)blocks), dim3(256), s, pdl, 0, a);
-    if (a.x_halo) return launch_k(tail_kernel<true, false>, dim3((unsigned)blocks), dim3(256), s, pdl, 0, a);
-    return launch_k(tail_kernel<false, false>, dim3((unsigned)blocks), dim3(256), s, pdl, 0, a);
+    if (a.diag) return launch_k(tail_kernel<false, true>, dim3((unsigned)blocks), dim3(kTailThreads), s, pdl, 0, a);
+    if (a.x_halo) return launch_k(tail_kernel<true, false>, dim3((unsigned)blocks), dim3(kTailThreads), s, pdl, 0, a);
+    return launch_k(tail_kernel<false, false>, dim3((unsigned)blocks), dim3(kTailThreads), s, pdl, 0, a);
 }
 
 // Concurrent tail: y[out_rows[p]] += tsum[p] once the ELL kernel and the
@@ -1190,9 +1190,9 @@ __global__ void __launch_bounds__(256) diag_ell_kernel(const int32_t* __restrict
 // The tail's diagonal entries in the warp-chunk layout: one CTA per
 // descriptor, each lane scans its pairs; at most one entry per row matches,
 // so every d[row] has a single writer (after diag_ell_kernel, stream order).
-__global__ void __launch_bounds__(256) diag_tail_kernel(TailArgs a, double* __restrict__ d) {
+__global__ void __launch_bounds__(kTailThreads) diag_tail_kernel(TailArgs a, double* __restrict__ d) {
     const int tid = threadIdx.x;
-    const int4 wm = __ldg(a.warp + (int64_t)blockIdx.x * 8 + (tid >> 5));
+    const int4 wm = __ldg(a.warp + (int64_t)blockIdx.x * kTailWarps + (tid >> 5));
     const int grp = tid >> (wm.w & 255);
     if (grp >= (wm.w >> 8)) return;
     const int32_t r = __ldg(a.out_rows + wm.z + grp);
@@ -1275,7 +1275,7 @@ cudaError_t launch_diag(const hec_matrix_s* A, double* d, cudaStream_t s) {
         t.out_rows = A->d_tail_out;
         t.col = A->d_tail_col;
         t.val = A->d_tail_val;
-        diag_tail_kernel<<<(unsigned)A->h_tail_blk.size(), 256, 0, s>>>(t, d);
+        diag_tail_kernel<<<(unsigned)A->h_tail_blk.size(), kTailThreads, 0, s>>>(t, d);
     }
     return cudaGetLastError();
 }
