@@ -243,6 +243,53 @@ static std::vector<int32_t> spectral_order(const Graph& g) {
     return order;
 }
 
+// Recursive spectral bisection of the vertex subset V (a small coarse graph):
+// each split orders V by the Fiedler vector of V's own induced subgraph and
+// cuts where the prefix weight reaches the proportional share.  A chain
+// segment's own Fiedler vector is sharper than the whole chain's (lambda_2
+// grows as the segment shortens, the far couplings' noise does not), so the
+// deeper splits fold less than one P-way cut of the global order.
+static void spectral_bisect(const Graph& g, const std::vector<int32_t>& V, int32_t P, int32_t part0,
+                            std::vector<int32_t>& part, std::vector<int32_t>& loc) {
+    if (P == 1 || V.size() <= 1) {
+        for (int32_t v : V) part[v] = part0;
+        return;
+    }
+    Graph h;
+    h.n = (int32_t)V.size();
+    for (int32_t i = 0; i < h.n; ++i) loc[V[i]] = i;
+    h.xadj.assign((size_t)h.n + 1, 0);
+    h.vw.resize(h.n);
+    for (int32_t i = 0; i < h.n; ++i) {
+        const int32_t v = V[i];
+        h.vw[i] = g.vw[v];
+        for (int64_t k = g.xadj[v]; k < g.xadj[v + 1]; ++k) {
+            const int32_t u = g.adj[(size_t)k];
+            if (loc[u] >= 0) {
+                h.adj.push_back(loc[u]);
+                h.ew.push_back(g.ew[(size_t)k]);
+            }
+        }
+        h.xadj[i + 1] = (int64_t)h.adj.size();
+    }
+    std::vector<int32_t> ord = spectral_order(h);
+    for (int32_t v : V) loc[v] = -1;
+    const int32_t P1 = P / 2;
+    int64_t W = 0;
+    for (int32_t v : V) W += g.vw[v];
+    const int64_t target = W * P1 / P;
+    size_t k = 0;
+    int64_t acc = 0;
+    while (k < ord.size() && acc + h.vw[ord[k]] <= target) acc += h.vw[ord[k++]];
+    if (k < ord.size() && (target - acc) * 2 > h.vw[ord[k]]) acc += h.vw[ord[k++]];
+    k = std::max<size_t>(k, (size_t)P1);
+    k = std::min<size_t>(k, ord.size() - (size_t)(P - P1));
+    std::vector<int32_t> L, R;
+    for (size_t i = 0; i < ord.size(); ++i) (i < k ? L : R).push_back(V[ord[i]]);
+    spectral_bisect(g, L, P1, part0, part, loc);
+    spectral_bisect(g, R, P - P1, part0 + P1, part, loc);
+}
+
 static uint64_t mix64(uint64_t z) {
     z += 0x9e3779b97f4a7c15ULL;
     z = (z ^ (z >> 30)) * 0xbf58476d1ce4e5b9ULL;
@@ -497,13 +544,15 @@ hec_status hec_partition_order(const hec_csr* A, int32_t n_parts, int32_t method
         if (const char* e = std::getenv("HEC_PART_TRIALS")) trials = std::max(1, std::atoi(e));
         int32_t fm_max = 2048;  // FM on the levels up to this many vertices (HEC_PART_FM, tuning; 0: off)
         if (const char* e = std::getenv("HEC_PART_FM")) fm_max = std::max(0, std::atoi(e));
-        const int runs = fm_max > 0 ? 2 * trials : trials;
+        // and a third time from a recursive spectral bisection of the coarsest graph
+        const int runs = (fm_max > 0 ? 2 : 1) * trials + trials;
         int64_t best_cut = -1, best_vol = -1;
         std::vector<int32_t> seen_part(n_parts, 0);
         std::vector<int32_t> bperm(v.n_rows), bpp(n_parts + 1);
         for (int run = 0; run < runs; ++run) {
             const int trial = run % trials;
-            const int32_t fm_lvl = run >= trials ? fm_max : 0;
+            const bool rsb = run >= runs - trials;
+            const int32_t fm_lvl = (run >= trials && !rsb) || (rsb && fm_max > 0) ? fm_max : 0;
             std::vector<Graph> G;
             G.push_back(g0);
             std::vector<std::vector<int32_t>> cmaps;
@@ -522,7 +571,11 @@ hec_status hec_partition_order(const hec_csr* A, int32_t n_parts, int32_t method
             std::vector<int32_t> part(gc.n, 0), in(gc.n, 0), seen(gc.n, 0), coarse_order;
             int32_t in_stamp = 0, seen_stamp = 0;
             if (gc.n <= kSpectralMax) coarse_order = spectral_order(gc);
-            if (!coarse_order.empty()) {
+            if (rsb && !coarse_order.empty()) {
+                std::vector<int32_t> all(gc.n), loc(gc.n, -1);
+                std::iota(all.begin(), all.end(), 0);
+                spectral_bisect(gc, all, n_parts, 0, part, loc);
+            } else if (!coarse_order.empty()) {
                 // the coarsest order cut into n_parts consecutive pieces of (nearly) equal weight
                 int64_t acc = 0;
                 int32_t p = 0;
