@@ -26,6 +26,7 @@ for b in sorted(glob.glob(os.path.join(d, "b_*.json"))):
                 per.setdefault(k, {})[m] = v  # last launch of each kernel wins
     ks = "  ".join(f"{k} {v.get('gpu__time_duration.sum', 0) / 1e3:.1f}us "
                    f"{v.get('dram__bytes_read.sum', 0) / 1e9:.3f}GB "
+                   f"w{v.get('dram__bytes_write.sum', 0) / 1e9:.3f}GB "
                    f"{v.get('l1tex__t_sectors_pipe_lsu_mem_global_op_ld.sum', 0) / 1e6:.1f}Ms"
                    for k, v in sorted(per.items()))
     print(f"{name:22s} step {ms} ms frac {frac}   {ks}")
