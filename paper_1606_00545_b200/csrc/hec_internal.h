@@ -181,6 +181,7 @@ struct hec_matrix_s {
     int32_t* d_tail_uwidx = nullptr;   // ... and its index in the warp-meta array
     unsigned int* d_tail_ctr = nullptr;  // [n_regions] claim counters + 1 done counter
     int32_t tail_regions = 0;
+    bool tail_reverse = false;         // tail launch walks its descriptors last to first (api.cpp)
     // x-ring schedule (TailArgs::ring_*): one allocation holding
     // the stages, the per-CTA stage prefix and the units
     void* d_ring = nullptr;
@@ -330,6 +331,7 @@ struct TailArgs {
     int32_t n_loc;
     double* y;
     double alpha = 1.0;  // the tail adds alpha * (its part of A x)
+    bool reverse = false;     // CTA b takes descriptor blk_end - 1 - b (the ELL kernel's last rows first)
     bool store_only = false;  // store the row sums instead of adding them: into y (small tails first,
                               // the ELL kernel adds them) or into tsum (concurrent tail, combined after)
     double* tsum = nullptr;   // [tail rows], indexed by device row position

@@ -626,9 +626,14 @@ __global__ void __launch_bounds__(kTailThreads, HEC_TAIL_MINB) tail_kernel(TailA
     const int w = threadIdx.x >> 5;
     if ((threadIdx.x & 31) == 0) mbar_init1(&sbar[w]);
     __syncwarp();
-    tail_desc<HALO, JACOBI>(a, a.blk_begin + blockIdx.x, threadIdx.x, pol, wsum, sval[w], &sbar[w]);
+    tail_desc<HALO, JACOBI>(a, a.reverse ? a.blk_end - 1 - blockIdx.x : a.blk_begin + blockIdx.x, threadIdx.x, pol,
+                            wsum, sval[w], &sbar[w]);
 #else
-    tail_desc<HALO, JACOBI>(a, a.blk_begin + blockIdx.x, threadIdx.x, pol, wsum);
+    // reverse: the descriptors from the last to the first, so the first CTAs
+    // gather the x band (and red.add into the y lines) the ELL kernel's last
+    // CTAs just left in L2
+    tail_desc<HALO, JACOBI>(a, a.reverse ? a.blk_end - 1 - blockIdx.x : a.blk_begin + blockIdx.x, threadIdx.x, pol,
+                            wsum);
 #endif
 }
 

@@ -149,3 +149,20 @@ def test_tail_concurrent_stream_bitwise():
     yp = run(Mp, x)
     for _ in range(3):
         assert run(Mc, x).tobytes() == yp.tobytes()
+
+
+@pytest.mark.parametrize("integer", [False, True])
+def test_tail_reverse_descriptor_order_bitwise(integer):
+    # the tail launch may walk its descriptors last to first (the default for
+    # tails without heavy leading descriptors): every row still gets exactly
+    # one red.add of the same sum -- bitwise equal to the forward order
+    A = hecgen.powerlaw(1 << 18, integer_values=integer, seed=13)
+    x = hecgen.vector(A.n_cols, "int" if integer else "uniform", seed=6)
+    ys = []
+    for rev in (0, 1):
+        with env(HEC_TAIL_REVERSE=rev, HEC_FUSE_TAIL=0):
+            M = hec.from_csr(A)
+        ys.append(run(M, x))
+    assert ys[0].tobytes() == ys[1].tobytes()
+    if integer:
+        assert ys[0].tobytes() == oracle.csr_spmv(A, x).tobytes()
