@@ -33,7 +33,7 @@ static void release(hec_matrix_s* m) {
         void* ptrs[] = {m->d_ell_col, m->d_ell_val, m->d_tail_out, m->d_tail_blk, m->d_fuse, m->d_tail_region,
                         m->d_tail_ctr, m->d_tsum, m->d_tail_units, m->d_tail_uwidx,
                         m->d_tail_warp, m->d_tail_col, m->d_tail_val, m->d_rowmap, m->d_coo_row, m->d_stage_x,
-                        m->d_stage_y, m->d_ring, m->d_ell_d16};
+                        m->d_stage_y, m->d_ring, m->d_ell_d16, m->d_tile_w, m->d_ell_perm};
         for (void* p : ptrs)
             if (p) cudaFree(p);
         for (cudaEvent_t e : m->ev_x) cudaEventDestroy(e);
@@ -53,7 +53,7 @@ static void release(hec_matrix_s* m) {
 // matrices), the x prefix each chunk reads, and the tail-kernel work list.
 static void plan_chunks(hec_matrix_s* m, const HostHec& h, bool pipelined, std::vector<int32_t>* order,
                         std::vector<int4>* blk, std::vector<int4>* warp, int64_t* entries, int32_t super,
-                        std::vector<int64_t>* sb_blk) {
+                        std::vector<int64_t>* sb_blk, int32_t row_align = 512) {
     const int32_t n = h.n_rows;
     // ~1M-row chunks, at most 16 (32 chunks measured slower: 3.62 vs 3.41 ms on
     // 256^3; smaller first/last chunks too: 3.36 vs 3.31 ms; the floor is the
@@ -61,7 +61,7 @@ static void plan_chunks(hec_matrix_s* m, const HostHec& h, bool pipelined, std::
     int32_t K = pipelined ? n / (1 << 20) : 1;
     K = K < 1 ? 1 : (K > 16 ? 16 : K);
     int64_t per = ((int64_t)n + K - 1) / K;
-    per = (per + 511) / 512 * 512;
+    per = (per + row_align - 1) / row_align * row_align;  // grouped rows never straddle a chunk
     m->chunk_row.assign(1, 0);
     while (m->chunk_row.back() < n)
         m->chunk_row.push_back((int32_t)std::min<int64_t>(n, m->chunk_row.back() + per));
@@ -346,6 +346,97 @@ static hec_status plan_idx16(hec_matrix_s* m, const HostHec& h, cudaStream_t s, 
     return HEC_OK;
 }
 
+// ELL rows grouped by length: inside windows of kGroupRows rows,
+// rows are stably sorted by their ELL length (longest first), so a warp's 64
+// rows are nearly equally long and the second-phase slots past the longest
+// of them -- padding for all 64 -- are skipped (plan_tile_w).  The ELL part
+// of row perm[p] is stored at position p; the ELL launch writes y[perm[p]]
+// (the tail, keyed by row, is unaffected).  Whole-matrix handles with a
+// two-phase width and >= 2^20 rows, when grouping makes at least 5% more
+// slots skippable than the natural order already does (HEC_ELL_GROUP=0
+// never, =1 always).
+static void skip_fraction(const HostHec& h, const int32_t* len_at, double* out) {
+    const int32_t w = h.width, P1 = (w + 1) / 2;
+    const int64_t nt = ((int64_t)h.stride + 63) / 64;
+    int64_t read = 0;
+    for (int64_t t = 0; t < nt; ++t) {
+        int32_t mx = 0;
+        for (int64_t i = t * 64; i < std::min<int64_t>((t + 1) * 64, h.n_rows); ++i) mx = std::max(mx, len_at[i]);
+        read += 64 * (int64_t)std::max(P1, mx);
+    }
+    *out = 1.0 - (double)read / ((double)w * 64.0 * (double)nt);
+}
+static void plan_group(HostHec& h, std::vector<int32_t>* perm) {
+    perm->clear();
+    const int32_t w = h.width, n = h.n_rows;
+    int env = -1;
+    if (const char* e = std::getenv("HEC_ELL_GROUP")) env = std::atoi(e) != 0 ? 1 : 0;
+    // (bandwidth-bound sizes only: below 2^20 rows the launch dominates and a
+    // small tail is better run first, fused with the ELL launch)
+    if (env == 0 || w <= HEC_ELL_PHASE || w > kIdx16MaxW || n < 64 || (env < 0 && n < (1 << 20))) return;
+    std::vector<int32_t> len((size_t)n, 0);
+    for (int32_t j = 0; j < w; ++j) {
+        const int32_t* cj = h.ell_col.data() + (size_t)j * h.stride;
+        for (int32_t i = 0; i < n; ++i) len[i] += cj[i] >= 0;
+    }
+    std::vector<int32_t> p((size_t)n);
+    for (int32_t i = 0; i < n; ++i) p[i] = i;
+    for (int32_t b = 0; b < n; b += kGroupRows) {
+        const int32_t e = std::min(n, b + kGroupRows);
+        std::stable_sort(p.begin() + b, p.begin() + e, [&](int32_t a, int32_t c) { return len[a] > len[c]; });
+    }
+    bool ident = true;
+    for (int32_t i = 0; i < n && ident; ++i) ident = p[i] == i;
+    if (ident) return;
+    std::vector<int32_t> lp((size_t)n);
+    for (int32_t i = 0; i < n; ++i) lp[i] = len[p[i]];
+    double nat = 0.0, grp = 0.0;
+    skip_fraction(h, len.data(), &nat);
+    skip_fraction(h, lp.data(), &grp);
+    if (env != 1 && grp - nat < 0.05) return;
+    std::vector<int32_t> tc((size_t)n);
+    std::vector<double> tv((size_t)n);
+    for (int32_t j = 0; j < w; ++j) {
+        int32_t* cj = h.ell_col.data() + (size_t)j * h.stride;
+        double* vj = h.ell_val.data() + (size_t)j * h.stride;
+        for (int32_t i = 0; i < n; ++i) {
+            tc[i] = cj[p[i]];
+            tv[i] = vj[p[i]];
+        }
+        std::copy(tc.begin(), tc.end(), cj);
+        std::copy(tv.begin(), tv.end(), vj);
+    }
+    perm->swap(p);
+}
+
+// Second-phase slot skipping: ELL widths loaded in two phases
+// (w > HEC_ELL_PHASE) read the second phase's slots only up to the longest
+// row of each warp's 64 rows.  Worth it where rows of similar length sit
+// together (degree-sorted inputs); planned when at least 5% of the slots go
+// unread (HEC_TILE_SKIP=0 never, =1 always).
+static hec_status plan_tile_w(hec_matrix_s* m, const HostHec& h, cudaStream_t s, int64_t* bytes) {
+    const int32_t w = h.width, n = h.n_rows;
+    const int P1 = (w + 1) / 2;
+    int env = -1;
+    if (const char* e = std::getenv("HEC_TILE_SKIP")) env = std::atoi(e) != 0 ? 1 : 0;
+    if (env == 0 || w <= HEC_ELL_PHASE || w > kIdx16MaxW || n == 0) return HEC_OK;
+    const int64_t nt = ((int64_t)h.stride + 63) / 64;
+    std::vector<uint8_t> tw((size_t)nt, 0);
+    for (int32_t j = 0; j < w; ++j) {
+        const int32_t* cj = h.ell_col.data() + (size_t)j * h.stride;
+        for (int32_t i = 0; i < n; ++i)
+            if (cj[i] >= 0) tw[(size_t)(i >> 6)] = (uint8_t)std::max<int>(tw[(size_t)(i >> 6)], j + 1);
+    }
+    int64_t read = 0;
+    for (int64_t t = 0; t < nt; ++t) read += 64 * (int64_t)std::max<int>(P1, tw[(size_t)t]);
+    m->tile_skip = 1.0 - (double)read / ((double)w * 64.0 * (double)nt);
+    if (env != 1 && m->tile_skip < 0.05) return HEC_OK;
+    hec_status st = dmalloc_copy(&m->d_tile_w, tw.data(), tw.size(), s, bytes);
+    if (st != HEC_OK) return st;
+    HEC_CUDA_TRY(cudaStreamSynchronize(s));
+    return HEC_OK;
+}
+
 hec_status make_matrix(HostHec&& h, int32_t device, cudaStream_t s, const int32_t* rowmap,
                        int32_t n_rowmap, int32_t row_off, int32_t n_loc, hec_matrix* out, bool coo_tail) {
     std::unique_ptr<hec_matrix_s, void (*)(hec_matrix_s*)> m(new (std::nothrow) hec_matrix_s(),
@@ -384,12 +475,18 @@ hec_status make_matrix(HostHec&& h, int32_t device, cudaStream_t s, const int32_
     int ring_env = 0;
     if (const char* e = std::getenv("HEC_TAIL_RING")) ring_env = std::atoi(e) != 0 ? 1 : 0;
     const bool ring_cand = !coo_tail && !h.tail_rows.empty() && ring_env == 1;
+    if (!coo_tail && n_loc < 0 && !rowmap && row_off == 0) plan_group(h, &m->h_ell_perm);
     plan_chunks(m.get(), h, n_loc < 0 && !rowmap && !coo_tail, &order, &blk, &warp, &entries,
-                ring_cand ? kRingSuperRows : kTailSuperRows, &sb_blk);
+                ring_cand ? kRingSuperRows : kTailSuperRows, &sb_blk, m->h_ell_perm.empty() ? 512 : kGroupRows);
     int64_t bytes = 0;
     hec_status st;
     if ((st = dmalloc_copy(&m->d_ell_col, h.ell_col.data(), h.ell_col.size(), s, &bytes))) return st;
+    if (!m->h_ell_perm.empty()) {
+        if ((st = dmalloc_copy(&m->d_ell_perm, m->h_ell_perm.data(), m->h_ell_perm.size(), s, &bytes))) return st;
+        HEC_CUDA_TRY(cudaStreamSynchronize(s));
+    }
     if ((st = plan_idx16(m.get(), h, s, &bytes))) return st;
+    if ((st = plan_tile_w(m.get(), h, s, &bytes))) return st;
     if (coo_tail) {  // HYB comparison variant: remainder as row-sorted COO triplets
         std::vector<int32_t> rows(h.tail_col.size());
         for (size_t t = 0; t < h.tail_rows.size(); ++t)
@@ -528,7 +625,7 @@ hec_status make_matrix(HostHec&& h, int32_t device, cudaStream_t s, const int32_
     // instead of trailing it.  Whole matrices whose ELL CTAs each take one tile
     // of rows (no grid stride).  HEC_FUSE_TAIL=0 disables; HEC_FUSE_TAIL_MAX =
     // most tail-kernel CTAs (default: one wave, 148 x 6).
-    if (!h.tail_rows.empty() && n_loc < 0 && !rowmap && row_off == 0) {
+    if (!h.tail_rows.empty() && n_loc < 0 && !rowmap && row_off == 0 && m->h_ell_perm.empty()) {
         int64_t fmax = (int64_t)148 * (48 / kTailWarps);
         if (const char* e = std::getenv("HEC_FUSE_TAIL_MAX")) fmax = std::atol(e);
         bool fuse = (int64_t)blk.size() <= fmax;
@@ -576,8 +673,8 @@ static hec_status launch_chunks(const hec_matrix_s* A, int c, const double* x, c
     e.x = x;
     e.x_halo = x_halo;
     e.n_loc = A->n_loc >= 0 ? A->n_loc : A->n_cols;
-    e.y = A->d_rowmap ? y : y + r0;
-    e.rowmap = A->d_rowmap ? A->d_rowmap + r0 : nullptr;
+    e.y = (A->d_rowmap || A->d_ell_perm) ? y : y + r0;
+    e.rowmap = A->d_rowmap ? A->d_rowmap + r0 : A->d_ell_perm ? A->d_ell_perm + r0 : nullptr;
     e.row_off = A->row_off;
     e.alpha = alpha;
     e.beta = beta;
@@ -586,6 +683,7 @@ static hec_status launch_chunks(const hec_matrix_s* A, int c, const double* x, c
         e.row0 = r0;
         for (int j = 0; j < A->width && j < kIdx16MaxW; ++j) e.base[j] = A->idx16_base[j];
     }
+    if (A->d_tile_w) e.tile_w = A->d_tile_w + r0 / 64;  // r0: a multiple of 512
     e.diag = jd;  // Jacobi epilogue (whole matrix only: c < 0)
     e.b = jb;
     e.omega = omega;
@@ -763,6 +861,9 @@ hec_status hec_info(hec_matrix A, hec_matrix_info* o) {
     o->tail_ring = A->d_ring_stage ? 1 : 0;
     o->ell_idx16 = A->d_ell_d16 ? 1 : 0;
     o->ell_idx16_escaped = A->idx16_esc;
+    o->ell_tile_skip = A->tile_skip;
+    o->ell_tile_w = A->d_tile_w ? 1 : 0;
+    o->ell_grouped = A->d_ell_perm ? 1 : 0;
     o->tail_ring_cover = A->ring_cover;
     return HEC_OK;
 }
@@ -784,6 +885,26 @@ hec_status hec_export(hec_matrix A, hec_host_arrays* o) {
     DeviceGuard g(A->device);
     if (o->ell_col && slots) HEC_CUDA_TRY(cudaMemcpy(o->ell_col, A->d_ell_col, slots * sizeof(int32_t), cudaMemcpyDeviceToHost));
     if (o->ell_val && slots) HEC_CUDA_TRY(cudaMemcpy(o->ell_val, A->d_ell_val, slots * sizeof(double), cudaMemcpyDeviceToHost));
+    if (!A->h_ell_perm.empty() && slots) {  // rows grouped by length on the device: back to row order
+        const std::vector<int32_t>& p = A->h_ell_perm;
+        try {
+            std::vector<int32_t> tc(p.size());
+            std::vector<double> tv(p.size());
+            for (int32_t j = 0; j < A->width; ++j) {
+                const size_t b = (size_t)j * A->stride;
+                if (o->ell_col) {
+                    for (size_t i = 0; i < p.size(); ++i) tc[(size_t)p[i]] = o->ell_col[b + i];
+                    std::copy(tc.begin(), tc.end(), o->ell_col + b);
+                }
+                if (o->ell_val) {
+                    for (size_t i = 0; i < p.size(); ++i) tv[(size_t)p[i]] = o->ell_val[b + i];
+                    std::copy(tv.begin(), tv.end(), o->ell_val + b);
+                }
+            }
+        } catch (...) {
+            return fail(HEC_ERR_NOMEM, "host allocation failed in hec_export");
+        }
+    }
     if (!A->tail_rows) {
         if (o->tail_ptr) o->tail_ptr[0] = 0;
         return HEC_OK;

@@ -189,6 +189,13 @@ struct hec_matrix_s {
     const int32_t* d_ring_cta = nullptr;
     int32_t ring_ctas = 0;
     double ring_cover = 0.0;
+    // rows grouped by ELL length inside windows of kGroupRows (device position
+    // p holds row ell_perm[p]; the ELL launch writes y through it as a row map)
+    int32_t* d_ell_perm = nullptr;
+    std::vector<int32_t> h_ell_perm;
+    // second-phase slot skipping (EllArgs::tile_w): longest ELL row per 64-row tile
+    uint8_t* d_tile_w = nullptr;
+    double tile_skip = 0.0;            // fraction of the ELL slots the kernel does not read
     // ELL index compression (EllArgs::d16): int16 deltas beside d_ell_col
     int16_t* d_ell_d16 = nullptr;
     int32_t idx16_base[16] = {};
@@ -283,7 +290,14 @@ struct PushArgs {                     // fused pack + NVLink store + release
     unsigned int* done;               // CTA completion counter (self-resetting)
 };
 
-constexpr int kIdx16MaxW = 16;      // widths with compiled-in slot loops (the compressed path needs one)
+#ifndef HEC_ELL_PHASE
+#define HEC_ELL_PHASE 8  // ELL widths above this load their slots in two phases (measured: 8 > 16 > 6)
+#endif
+constexpr int kIdx16MaxW = 16;
+#ifndef HEC_GROUP_ROWS
+#define HEC_GROUP_ROWS 4096
+#endif
+constexpr int32_t kGroupRows = HEC_GROUP_ROWS;  // windows in which rows are grouped by ELL length (a multiple of 512)      // widths with compiled-in slot loops (the compressed path needs one)
 constexpr int16_t kIdxEsc = INT16_MIN;      // the int32 column must be read
 constexpr int16_t kIdxPad = INT16_MIN + 1;  // padding slot (column -1)
 struct EllArgs {
@@ -306,6 +320,10 @@ struct EllArgs {
     const double* b = nullptr;
     double omega = 0.0;
     bool pdl = false;  // launch as a programmatic dependent (peer-memory boundary rows)
+    // per 64-row tile (one warp's rows): the tile's longest ELL row, when the
+    // tiles' second-phase slots are worth skipping (rows grouped by length);
+    // slots >= tile_w[i >> 6] are padding for every row of the tile and are not read
+    const uint8_t* tile_w = nullptr;
     // small tails, tail first (plain y = A x of a whole matrix): the tail kernel
     // stored the tail rows' sums into y just before; CTA b adds them to its
     // rows fuse_row[fuse_cta[b] .. fuse_cta[b+1]) (ascending)

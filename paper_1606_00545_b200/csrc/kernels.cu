@@ -203,9 +203,6 @@ __device__ __forceinline__ double jacobi_row(double x, double b, double d, doubl
 #define HEC_TAIL_UNROLL 2  // entry-pair iterations per lane unrolled
 #endif
 constexpr int kTailUnroll = HEC_TAIL_UNROLL;
-#ifndef HEC_ELL_PHASE
-#define HEC_ELL_PHASE 8  // widths above this load their slots in two phases (measured: 8 > 16 > 6)
-#endif
 
 __device__ __forceinline__ uint32_t ld_stream_u32v(const void* ptr, uint64_t pol) {
     uint32_t r;
@@ -266,6 +263,32 @@ __device__ __forceinline__ void ell_phase(const EllArgs& a, const int32_t* cp, c
     }
 }
 
+// ell_phase for slots [J0, J1) of which only [J0, wt) can hold entries (wt
+// warp-uniform): the rest are neither loaded nor gathered.  A skipped slot
+// adds nothing, exactly as a padding slot (col -1, +0.0) would.
+template <int J0, int J1, bool HALO>
+__device__ __forceinline__ void ell_phase_upto(const EllArgs& a, const int32_t* cp, const double* vp, int64_t s,
+                                               uint64_t pol, double& acc0, double& acc1, int wt) {
+    constexpr int N = J1 - J0;
+    int2 c[N];
+    double2 v[N];
+#pragma unroll
+    for (int j = 0; j < N; ++j) c[j] = J0 + j < wt ? ld_stream_i2v(cp + (J0 + j) * s, pol) : make_int2(-1, -1);
+#pragma unroll
+    for (int j = 0; j < N; ++j) v[j] = J0 + j < wt ? ld_stream_d2v(vp + (J0 + j) * s, pol) : make_double2(0.0, 0.0);
+    double x0[N], x1[N];
+#pragma unroll
+    for (int j = 0; j < N; ++j) {
+        x0[j] = c[j].x >= 0 ? gather_x<HALO>(a.x, a.x_halo, a.n_loc, c[j].x) : 0.0;
+        x1[j] = c[j].y >= 0 ? gather_x<HALO>(a.x, a.x_halo, a.n_loc, c[j].y) : 0.0;
+    }
+#pragma unroll
+    for (int j = 0; j < N; ++j) {  // a skipped slot adds +0.0 x 0.0, as padding does
+        acc0 = fma(v[j].x, x0[j], acc0);
+        acc1 = fma(v[j].y, x1[j], acc1);
+    }
+}
+
 // FUSE (small tails, "tail first"): the tail kernel ran just before this
 // launch and stored each tail row's sum into y; this kernel is its
 // programmatic dependent, so its CTAs stream their ELL rows while the tail
@@ -316,8 +339,14 @@ __global__ void __launch_bounds__(256, EPI == EPI_JACOBI ? HEC_JAC_MINB : 0) ell
             // registers, more resident warps).
             constexpr int WW = W > 0 ? W : 1;
             constexpr int P1 = WW > HEC_ELL_PHASE ? (WW + 1) / 2 : WW;
+            // rows grouped by length: the warp's longest row (one byte per 64
+            // rows, loaded beside the first phase) bounds the second phase
+            const int wt = (P1 < WW && a.tile_w) ? (int)__ldg(a.tile_w + (i0 >> 6)) : WW;
             ell_phase<0, P1, HALO, C16>(a, cp, vp, s, pol, acc0, acc1, i0);
-            if constexpr (P1 < WW) ell_phase<P1, WW, HALO, C16>(a, cp, vp, s, pol, acc0, acc1, i0);
+            if constexpr (P1 < WW) {
+                if (wt >= WW) ell_phase<P1, WW, HALO, C16>(a, cp, vp, s, pol, acc0, acc1, i0);
+                else if (wt > P1) ell_phase_upto<P1, WW, HALO>(a, cp, vp, s, pol, acc0, acc1, wt);
+            }
         } else {
 #pragma unroll 4
             for (int j = 0; j < width; ++j) {
@@ -333,8 +362,13 @@ __global__ void __launch_bounds__(256, EPI == EPI_JACOBI ? HEC_JAC_MINB : 0) ell
         // exact, and y is then never read)
         const bool two = i0 + 1 < a.n_rows;
         if (ROWMAP) {
-            double* y0 = a.y + a.rowmap[i0];
-            double* y1 = two ? a.y + a.rowmap[i0 + 1] : nullptr;
+            const int32_t g0 = __ldg(a.rowmap + i0), g1 = two ? __ldg(a.rowmap + i0 + 1) : 0;
+            double* y0 = a.y + g0;
+            double* y1 = two ? a.y + g1 : nullptr;
+            if (EPI == EPI_JACOBI) {  // grouped rows of a square matrix: x, b, d indexed by the output row
+                acc0 = jacobi_row(__ldg(a.x + g0), __ldg(a.b + g0), __ldg(a.diag + g0), a.omega, acc0);
+                if (two) acc1 = jacobi_row(__ldg(a.x + g1), __ldg(a.b + g1), __ldg(a.diag + g1), a.omega, acc1);
+            }
             if (AXPBY && a.beta != 0.0) {
                 acc0 = a.alpha * acc0 + a.beta * *y0;
                 if (two) acc1 = a.alpha * acc1 + a.beta * *y1;
@@ -1099,13 +1133,14 @@ cudaError_t launch_ell(const EllArgs& a, cudaStream_t s) {
     }
     const bool halo = a.x_halo != nullptr;
     const bool rowmap = a.rowmap != nullptr;
-    if (a.diag) {  // hec_jacobi (single square matrix: no halo, no row map)
-        if (halo || rowmap) return cudaErrorInvalidValue;
-        return launch_ell_t<false, false, EPI_JACOBI>(a, s);
+    // (single square matrices: no halo; a row map only for rows grouped by length)
+    if (a.diag) {  // hec_jacobi
+        if (halo) return cudaErrorInvalidValue;
+        return rowmap ? launch_ell_t<false, true, EPI_JACOBI>(a, s) : launch_ell_t<false, false, EPI_JACOBI>(a, s);
     }
-    if (a.alpha != 1.0 || a.beta != 0.0) {  // hec_spmv_axpby (single matrix: no halo, no row map)
-        if (halo || rowmap) return cudaErrorInvalidValue;
-        return launch_ell_t<false, false, EPI_AXPBY>(a, s);
+    if (a.alpha != 1.0 || a.beta != 0.0) {  // hec_spmv_axpby
+        if (halo) return cudaErrorInvalidValue;
+        return rowmap ? launch_ell_t<false, true, EPI_AXPBY>(a, s) : launch_ell_t<false, false, EPI_AXPBY>(a, s);
     }
     if (a.fuse_cta) {  // plain whole-matrix product with its small tail fused in
         if (halo || rowmap) return cudaErrorInvalidValue;
@@ -1183,12 +1218,14 @@ cudaError_t launch_pack(const int32_t* idx, int32_t n, const double* x, double* 
 // the tail rows, which overwrite only where the diagonal spilled.
 __global__ void __launch_bounds__(256) diag_ell_kernel(const int32_t* __restrict__ col,
                                                        const double* __restrict__ val, int64_t stride,
-                                                       int32_t width, int32_t n, double* __restrict__ d) {
+                                                       int32_t width, int32_t n, const int32_t* __restrict__ perm,
+                                                       double* __restrict__ d) {
     for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x) {
+        const int32_t r = perm ? perm[i] : (int32_t)i;  // the row stored at position i
         double v = 0.0;
         for (int32_t j = 0; j < width; ++j)
-            if (col[j * stride + i] == (int32_t)i) v = val[j * stride + i];
-        d[i] = v;
+            if (col[j * stride + i] == r) v = val[j * stride + i];
+        d[r] = v;
     }
 }
 
@@ -1270,7 +1307,7 @@ cudaError_t launch_diag(const hec_matrix_s* A, double* d, cudaStream_t s) {
     const int cap = num_sms() * 8;
     auto grid = [cap](int64_t n) { int64_t g = (n + 255) / 256; return (unsigned)(g < 1 ? 1 : (g > cap ? cap : g)); };
     diag_ell_kernel<<<grid(A->n_rows), 256, 0, s>>>(A->d_ell_col, A->d_ell_val, A->stride,
-                                                    A->d_ell_col ? A->width : 0, A->n_rows, d);
+                                                    A->d_ell_col ? A->width : 0, A->n_rows, A->d_ell_perm, d);
     if (A->tail_rows > 0 && A->tail_coo)
         diag_coo_kernel<<<grid(A->tail_nnz), 256, 0, s>>>(A->d_coo_row, A->d_tail_col, A->d_tail_val, A->tail_nnz, d);
     else if (A->tail_rows > 0 && !A->h_tail_blk.empty()) {

@@ -51,7 +51,8 @@ class MatrixInfoT(ctypes.Structure):
                 ("nnz", i64), ("ell_nnz", i64), ("tail_rows", i32), ("tail_group", i32),
                 ("tail_nnz", i64), ("device_bytes", i64), ("device", i32), ("tail_fused", i32),
                 ("tail_ring", i32), ("ell_idx16", i32), ("tail_ring_cover", ctypes.c_double),
-                ("ell_idx16_escaped", ctypes.c_double)]
+                ("ell_idx16_escaped", ctypes.c_double), ("ell_tile_skip", ctypes.c_double),
+                ("ell_tile_w", i32), ("ell_grouped", i32)]
 
 
 class HostArraysT(ctypes.Structure):
