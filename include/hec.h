@@ -118,7 +118,7 @@ typedef struct {
     double ell_tile_skip;  /* fraction of the ELL slots the kernel skips: second-phase slots past the
                               longest row of a warp's 64 rows (two-phase widths) */
     int32_t ell_tile_w;    /* 1: the skipping is on for this handle */
-    int32_t ell_grouped;   /* 1: the device ELL rows are grouped by length inside windows of 4096
+    int32_t ell_grouped;   /* 1: the device ELL rows are grouped by length inside windows of 1024
                               rows (y is written through the permutation; hec_export returns row order) */
 } hec_matrix_info;
 

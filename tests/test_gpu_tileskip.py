@@ -8,7 +8,7 @@ equal to it in the integer regime.  Covered: the default choice (on for
 degree-sorted rows, off for the natural power-law), forced skipping, the
 Eq. (2) and Jacobi epilogues, the chunked host path (row offsets) and the
 distributed sub-matrices (row maps, halo columns); and the grouping of ELL
-rows by length inside 4096-row windows that makes the natural power-law's
+rows by length inside 1024-row windows that makes the natural power-law's
 slots skippable (y through the permutation, hec_export back in row order)."""
 import os
 
@@ -83,7 +83,7 @@ def test_tileskip_integer_bitwise_vs_oracle():
 
 def test_grouping_natural_powerlaw_bitwise():
     # natural order: rows of every length side by side, so the ELL rows are
-    # grouped by length inside 4096-row windows first (y written through the
+    # grouped by length inside 1024-row windows first (y written through the
     # permutation) -- bitwise equal to the ungrouped, unskipped product
     A = hecgen.powerlaw((1 << 17) + 4321, seed=43)
     x = hecgen.vector(A.n_cols, "uniform", seed=3)
@@ -114,7 +114,7 @@ def test_grouping_integer_bitwise_vs_oracle():
 
 def test_grouping_epilogues_and_host_chunks_bitwise():
     # Eq. (2), the diagonal and the Jacobi sweep through the permutation; and
-    # hec_spmv_host's chunks (aligned to the 4096-row windows)
+    # hec_spmv_host's chunks (aligned to the grouping windows)
     A = hecgen.powerlaw(3 << 20, seed=48)
     n = A.n_rows
     x = hecgen.vector(n, "uniform", seed=5)
