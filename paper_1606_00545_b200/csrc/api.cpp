@@ -8,6 +8,7 @@
 #include <cstdlib>
 #include <cstring>
 #include <memory>
+#include <new>
 
 #include "hec_internal.h"
 
@@ -437,8 +438,25 @@ static hec_status plan_tile_w(hec_matrix_s* m, const HostHec& h, cudaStream_t s,
     return HEC_OK;
 }
 
+static hec_status make_matrix_impl(HostHec&& h, int32_t device, cudaStream_t s, const int32_t* rowmap,
+                                   int32_t n_rowmap, int32_t row_off, int32_t n_loc, hec_matrix* out, bool coo_tail);
+
+// Every host planning step (tail layout, grouping, rings) allocates: a failed
+// allocation is reported, never thrown across the C ABI (the handle's device
+// memory is released by its owner on the way out).
 hec_status make_matrix(HostHec&& h, int32_t device, cudaStream_t s, const int32_t* rowmap,
                        int32_t n_rowmap, int32_t row_off, int32_t n_loc, hec_matrix* out, bool coo_tail) {
+    try {
+        return make_matrix_impl(std::move(h), device, s, rowmap, n_rowmap, row_off, n_loc, out, coo_tail);
+    } catch (const std::bad_alloc&) {
+        return fail(HEC_ERR_NOMEM, "host allocation failed while building the device HEC");
+    } catch (...) {
+        return fail(HEC_ERR_STATE, "unexpected exception while building the device HEC");
+    }
+}
+
+static hec_status make_matrix_impl(HostHec&& h, int32_t device, cudaStream_t s, const int32_t* rowmap,
+                                   int32_t n_rowmap, int32_t row_off, int32_t n_loc, hec_matrix* out, bool coo_tail) {
     std::unique_ptr<hec_matrix_s, void (*)(hec_matrix_s*)> m(new (std::nothrow) hec_matrix_s(),
                                                              release);
     if (!m) return fail(HEC_ERR_NOMEM, "host allocation failed");
