@@ -357,7 +357,7 @@ static hec_status plan_idx16(hec_matrix_s* m, const HostHec& h, cudaStream_t s, 
 // slots skippable than the natural order already does (HEC_ELL_GROUP=0
 // never, =1 always).
 static void skip_fraction(const HostHec& h, const int32_t* len_at, double* out) {
-    const int32_t w = h.width, P1 = (w + 1) / 2;
+    const int32_t w = h.width, P1 = ell_first_phase(w);
     const int64_t nt = ((int64_t)h.stride + 63) / 64;
     int64_t read = 0;
     for (int64_t t = 0; t < nt; ++t) {
@@ -417,7 +417,7 @@ static void plan_group(HostHec& h, std::vector<int32_t>* perm) {
 // unread (HEC_TILE_SKIP=0 never, =1 always).
 static hec_status plan_tile_w(hec_matrix_s* m, const HostHec& h, cudaStream_t s, int64_t* bytes) {
     const int32_t w = h.width, n = h.n_rows;
-    const int P1 = (w + 1) / 2;
+    const int P1 = ell_first_phase(w);
     int env = -1;
     if (const char* e = std::getenv("HEC_TILE_SKIP")) env = std::atoi(e) != 0 ? 1 : 0;
     if (env == 0 || w <= HEC_ELL_PHASE || w > kIdx16MaxW || n == 0) return HEC_OK;

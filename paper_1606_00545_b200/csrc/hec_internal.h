@@ -293,6 +293,12 @@ struct PushArgs {                     // fused pack + NVLink store + release
 #ifndef HEC_ELL_PHASE
 #define HEC_ELL_PHASE 8  // ELL widths above this load their slots in two phases (measured: 8 > 16 > 6)
 #endif
+// slots of a two-phase width loaded in the first phase (HEC_ELL_P1_DELTA
+// shifts the split from the middle; tuning)
+#ifndef HEC_ELL_P1_DELTA
+#define HEC_ELL_P1_DELTA 0
+#endif
+__host__ __device__ constexpr int ell_first_phase(int w) { return (w + 1) / 2 + HEC_ELL_P1_DELTA; }
 constexpr int kIdx16MaxW = 16;  // widths with compiled-in slot loops (compressed indices and slot skipping need one)
 #ifndef HEC_GROUP_ROWS
 #define HEC_GROUP_ROWS 1024  // measured 512 / 1024 / 4096: -0.1% / -1.0% / -0.6% on the power-law step

@@ -338,7 +338,7 @@ __global__ void __launch_bounds__(256, EPI == EPI_JACOBI ? HEC_JAC_MINB : 0) ell
             // Widths above HEC_ELL_PHASE run in two such phases (fewer live
             // registers, more resident warps).
             constexpr int WW = W > 0 ? W : 1;
-            constexpr int P1 = WW > HEC_ELL_PHASE ? (WW + 1) / 2 : WW;
+            constexpr int P1 = WW > HEC_ELL_PHASE ? ell_first_phase(WW) : WW;
             // rows grouped by length: the warp's longest row (one byte per 64
             // rows, loaded beside the first phase) bounds the second phase
             const int wt = (P1 < WW && a.tile_w) ? (int)__ldg(a.tile_w + (i0 >> 6)) : WW;
