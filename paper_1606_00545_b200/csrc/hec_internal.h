@@ -293,10 +293,13 @@ struct PushArgs {                     // fused pack + NVLink store + release
 #ifndef HEC_ELL_PHASE
 #define HEC_ELL_PHASE 8  // ELL widths above this load their slots in two phases (measured: 8 > 16 > 6)
 #endif
-// slots of a two-phase width loaded in the first phase (HEC_ELL_P1_DELTA
-// shifts the split from the middle; tuning)
+// slots of a two-phase width loaded in the first phase: one before the
+// middle (w = 9: 4 + 5), so warps whose rows all have <= 4 ELL entries skip
+// the whole second phase (power-law step 0.4347 -> 0.4210 ms; 5 + 4 and 6 + 3
+// measured, degree-sorted within +-1.3%: profiles/round2/phase/).
+// HEC_ELL_P1_DELTA (tuning) shifts the split.
 #ifndef HEC_ELL_P1_DELTA
-#define HEC_ELL_P1_DELTA 0
+#define HEC_ELL_P1_DELTA (-1)
 #endif
 __host__ __device__ constexpr int ell_first_phase(int w) { return (w + 1) / 2 + HEC_ELL_P1_DELTA; }
 constexpr int kIdx16MaxW = 16;  // widths with compiled-in slot loops (compressed indices and slot skipping need one)
