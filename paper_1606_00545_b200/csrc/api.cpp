@@ -351,9 +351,9 @@ static hec_status plan_idx16(hec_matrix_s* m, const HostHec& h, cudaStream_t s, 
 // rows are stably sorted by their ELL length (longest first), so a warp's 64
 // rows are nearly equally long and the second-phase slots past the longest
 // of them -- padding for all 64 -- are skipped (plan_tile_w).  The ELL part
-// of row perm[p] is stored at position p; the ELL launch writes y[perm[p]]
-// (the tail, keyed by row, is unaffected).  Whole-matrix handles with a
-// two-phase width and >= 2^20 rows, when grouping makes at least 5% more
+// of row perm[p] is stored at position p; the ELL launch writes that row's
+// output (the tail, keyed by row, is unaffected).  Handles with a two-phase
+// width and at least min_rows rows, when grouping makes at least 5% more
 // slots skippable than the natural order already does (HEC_ELL_GROUP=0
 // never, =1 always).
 static void skip_fraction(const HostHec& h, const int32_t* len_at, double* out) {
@@ -367,14 +367,12 @@ static void skip_fraction(const HostHec& h, const int32_t* len_at, double* out) 
     }
     *out = 1.0 - (double)read / ((double)w * 64.0 * (double)nt);
 }
-static void plan_group(HostHec& h, std::vector<int32_t>* perm) {
+static void plan_group(HostHec& h, int32_t min_rows, std::vector<int32_t>* perm) {
     perm->clear();
     const int32_t w = h.width, n = h.n_rows;
     int env = -1;
     if (const char* e = std::getenv("HEC_ELL_GROUP")) env = std::atoi(e) != 0 ? 1 : 0;
-    // (bandwidth-bound sizes only: below 2^20 rows the launch dominates and a
-    // small tail is better run first, fused with the ELL launch)
-    if (env == 0 || w <= HEC_ELL_PHASE || w > kIdx16MaxW || n < 64 || (env < 0 && n < (1 << 20))) return;
+    if (env == 0 || w <= HEC_ELL_PHASE || w > kIdx16MaxW || n < 64 || (env < 0 && n < min_rows)) return;
     std::vector<int32_t> len((size_t)n, 0);
     for (int32_t j = 0; j < w; ++j) {
         const int32_t* cj = h.ell_col.data() + (size_t)j * h.stride;
@@ -493,14 +491,25 @@ static hec_status make_matrix_impl(HostHec&& h, int32_t device, cudaStream_t s, 
     int ring_env = 0;
     if (const char* e = std::getenv("HEC_TAIL_RING")) ring_env = std::atoi(e) != 0 ? 1 : 0;
     const bool ring_cand = !coo_tail && !h.tail_rows.empty() && ring_env == 1;
-    if (!coo_tail && n_loc < 0 && !rowmap && row_off == 0) plan_group(h, &m->h_ell_perm);
+    // rows grouped by ELL length: whole matrices from 2^20 rows (below, the
+    // launch dominates and a small tail is better run first, fused with the
+    // ELL launch), distributed sub-matrices from 2^16 rows
+    const bool whole = n_loc < 0 && !rowmap && row_off == 0;
+    if (!coo_tail) plan_group(h, whole ? (1 << 20) : (1 << 16), &m->h_ell_perm);
     plan_chunks(m.get(), h, n_loc < 0 && !rowmap && !coo_tail, &order, &blk, &warp, &entries,
                 ring_cand ? kRingSuperRows : kTailSuperRows, &sb_blk, m->h_ell_perm.empty() ? 512 : kGroupRows);
     int64_t bytes = 0;
     hec_status st;
     if ((st = dmalloc_copy(&m->d_ell_col, h.ell_col.data(), h.ell_col.size(), s, &bytes))) return st;
     if (!m->h_ell_perm.empty()) {
-        if ((st = dmalloc_copy(&m->d_ell_perm, m->h_ell_perm.data(), m->h_ell_perm.size(), s, &bytes))) return st;
+        // the ELL launch's output row of device position p: the stored row's
+        // own output row (row map or offset) -- for whole matrices perm[p]
+        std::vector<int32_t> out(m->h_ell_perm.size());
+        for (size_t p = 0; p < out.size(); ++p) {
+            const int32_t r = m->h_ell_perm[p];
+            out[p] = rowmap ? rowmap[r] : row_off + r;
+        }
+        if ((st = dmalloc_copy(&m->d_ell_perm, out.data(), out.size(), s, &bytes))) return st;
         HEC_CUDA_TRY(cudaStreamSynchronize(s));
     }
     if ((st = plan_idx16(m.get(), h, s, &bytes))) return st;
@@ -692,7 +701,7 @@ static hec_status launch_chunks(const hec_matrix_s* A, int c, const double* x, c
     e.x_halo = x_halo;
     e.n_loc = A->n_loc >= 0 ? A->n_loc : A->n_cols;
     e.y = (A->d_rowmap || A->d_ell_perm) ? y : y + r0;
-    e.rowmap = A->d_rowmap ? A->d_rowmap + r0 : A->d_ell_perm ? A->d_ell_perm + r0 : nullptr;
+    e.rowmap = A->d_ell_perm ? A->d_ell_perm + r0 : A->d_rowmap ? A->d_rowmap + r0 : nullptr;
     e.row_off = A->row_off;
     e.alpha = alpha;
     e.beta = beta;

@@ -190,7 +190,8 @@ struct hec_matrix_s {
     int32_t ring_ctas = 0;
     double ring_cover = 0.0;
     // rows grouped by ELL length inside windows of kGroupRows (device position
-    // p holds row ell_perm[p]; the ELL launch writes y through it as a row map)
+    // p holds row h_ell_perm[p]; d_ell_perm[p] = that row's output row, the
+    // ELL launch's row map)
     int32_t* d_ell_perm = nullptr;
     std::vector<int32_t> h_ell_perm;
     // second-phase slot skipping (EllArgs::tile_w): longest ELL row per 64-row tile

@@ -205,3 +205,26 @@ def test_grouping_full_size_powerlaw_every_row():
         Mp = hec.from_csr(A)
     assert yg.tobytes() == run(Mp, x).tobytes()
     assert np.all(np.abs(yg - oracle.csr_spmv(A, x)) <= oracle.tolerance(A, x))
+
+
+@pytest.mark.parametrize("P", [2, 3])
+def test_grouping_distributed_submatrices_bitwise(P):
+    # sub-matrices of >= 2^16 rows are grouped too: the ELL launch writes each
+    # stored row's own output row (row map / offset composed with the grouping)
+    A = hecgen.powerlaw(1 << 18, seed=49)
+    x = hecgen.vector(A.n_cols, "uniform", seed=9)
+    plan = hec.partition(A, P, hec.PART_CONTIG_NNZ)
+    pp = plan.part_ptr()
+    ys = {}
+    for flag in (1, 0):
+        with env(HEC_ELL_GROUP=flag, HEC_TILE_SKIP=flag):
+            grp = hec.LocalDistGroup(A, plan, 0, None, p2p=True)
+        xs = [dev(x[pp[p]:pp[p + 1]]) for p in range(P)]
+        yl = [torch.full((int(pp[p + 1] - pp[p]),), float("nan"), dtype=torch.float64, device="cuda")
+              for p in range(P)]
+        grp.spmv(xs, yl)
+        torch.cuda.synchronize()
+        ys[flag] = np.concatenate([t.cpu().numpy() for t in yl])
+        grp.free()
+    assert ys[1].tobytes() == ys[0].tobytes()
+    assert np.all(np.abs(ys[1] - oracle.csr_spmv(A, x)) <= oracle.tolerance(A, x))
