@@ -127,3 +127,17 @@ def test_dist_create_without_device_fails_loudly():
     with pytest.raises(hec.HecError) as e:
         hec.Dist(A, P, 0, None, 0)
     assert e.value.status in (5, 9)
+
+
+def test_matrix_info_layout_of_the_round2_fields():
+    # hec_matrix_info grew fields in round 2 (x-ring, index compression, slot
+    # skipping, row grouping): on a host-only handle they read as "off", and
+    # the struct the binding declares is exactly as large as the C one (the
+    # last field lands where C puts it, or the values below would be garbage)
+    import ctypes
+    A = hecgen.powerlaw(3000, seed=12)
+    inf = hec.from_csr(A, device=-1).info
+    assert inf.n_rows == 3000 and inf.device == -1
+    assert inf.tail_ring == 0 and inf.ell_idx16 == 0 and inf.ell_tile_w == 0 and inf.ell_grouped == 0
+    assert inf.tail_ring_cover == 0.0 and inf.ell_idx16_escaped == -1.0 and inf.ell_tile_skip == 0.0
+    assert ctypes.sizeof(type(inf)) % 8 == 0
