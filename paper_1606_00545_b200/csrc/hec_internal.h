@@ -98,7 +98,7 @@ constexpr int kRingCols = 16384;
 constexpr int kRingDepth = HEC_RING_DEPTH;  // stages in flight per ring CTA (its windows share the ring)
 constexpr int kRingSuperRows = 1024;
 #ifndef HEC_TAIL_EPL_BIG
-#define HEC_TAIL_EPL_BIG 32  // measured with the batched tail loop: 8 -> 316/335 us, 16 -> 274, 32 -> 262
+#define HEC_TAIL_EPL_BIG 48  // measured with the batched tail loop: 8 -> 316/335 us, 16 -> 274, 32 -> 262; final tree: 24 / 32 / 48 -> step 0.4264 / 0.4211 / 0.4184 ms
 #endif
 constexpr int kTailEplBig = HEC_TAIL_EPL_BIG;  // entries per lane for tails of >= 2^22 entries
 inline int tail_max_lg() {             // HEC_TAIL_MAXLG (tuning): 5..8
